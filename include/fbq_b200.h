@@ -1,0 +1,144 @@
+/* fbq_b200.h -- C ABI of the B200 (sm_100a) Fallback-Quantization hot path.
+ *
+ * Drop-in boundary for the reference C++ operator API (/root/reference/proj,
+ * namespace fbq).  Each entry point below names the reference interface it
+ * replaces (file:line).  The reference API takes host DenseMatrix /
+ * QuantizedTensor values; here every DEVICE entry point (fbq_cuda_*) takes
+ * plain device pointers + sizes, runs asynchronously on the caller's
+ * cudaStream_t, never allocates, never synchronises, and returns an int status
+ * (nothing throws across the ABI).  The HOST entry points (fbq_host_*) take
+ * host buffers, exactly like the reference's value-semantics API, and do the
+ * host<->device copies themselves (e2e path).
+ *
+ * Fixed hot-path geometry: 128 x 128 quantization blocks, b = 8 (L = 127) for
+ * GEMM operands (SPEC.md gemm module; PAPER.md 4.5).  Other block sides or
+ * bit-widths return FBQ_ERR_UNSUPPORTED -- there is no CPU fallback.
+ *
+ * Device layouts (row-major everywhere):
+ *   x          fp32 or bf16, rows x ldx elements
+ *   codes      int8, rows x ldq        (reference: int16 QuantizedTensor::codes, quant.hpp:31)
+ *   scales     fp32, ceil(rows/128) x ceil(cols/128)            (quant.hpp:32)
+ *   mask_bits  uint32, ceil(grid/32) words; bit b <-> linear block b (row-major),
+ *              the compact form of FallbackTensor::mask (quant.hpp:42)
+ *   res_codes  int8, rows x ldq: dense residual ("lo") plane; only flagged
+ *              blocks are written / read (FallbackTensor::residuals, quant.hpp:46-52)
+ *   res_scales fp32 grid (0 for unflagged blocks)
+ * int8 planes that feed the GEMM need ldq % 16 == 0 (TMA stride rule).
+ */
+#ifndef FBQ_B200_H
+#define FBQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fbq_stream_t; /* == cudaStream_t */
+
+enum fbq_status {
+  FBQ_OK = 0,
+  FBQ_ERR_SHAPE = 1,       /* dimension / geometry mismatch (reference: std::invalid_argument) */
+  FBQ_ERR_UNSUPPORTED = 2, /* block side != 128, bits != 8, bad alignment */
+  FBQ_ERR_CUDA = 3,        /* launch or runtime failure; see fbq_last_cuda_error() */
+  FBQ_ERR_ARG = 4          /* null pointer / bad enum / out-of-range value */
+};
+enum fbq_dtype { FBQ_F32 = 0, FBQ_BF16 = 1 };
+enum fbq_mask_mode {
+  FBQ_MASK_NONE = 0,      /* quantize_rtn only */
+  FBQ_MASK_THRESHOLD = 1, /* u = absmax > theta (policy.cpp:73-80), written to mask_bits */
+  FBQ_MASK_GIVEN = 2      /* u read from mask_bits (e.g. mask_topk, policy.cpp:56-71) */
+};
+enum fbq_major { FBQ_K_MAJOR = 0, FBQ_MN_MAJOR = 1 };
+enum fbq_epilogue {
+  FBQ_EPI_EXACT = 0, /* bit-identical to gemm.cpp's fl(acc + fl(s*P)) chain */
+  FBQ_EPI_FMA = 1    /* acc = fma(P, s, acc): ~5e-8 rel. Frobenius from EXACT */
+};
+
+const char* fbq_version(void);
+const char* fbq_status_string(int status);
+int fbq_last_cuda_error(void); /* cudaError_t of the last FBQ_ERR_CUDA on this thread */
+int fbq_block_side(void);      /* 128 */
+
+/* score_blocks(AbsMax) -- policy.cpp:12-28 / policy.hpp:18-19.
+ * amax[blk] = max |x| over the block (float; the reference widens to double). */
+int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                          float* amax, fbq_stream_t stream);
+
+/* K1: fused quantize_rtn (quant.cpp:36-53) + score_blocks(AbsMax) + mask_threshold
+ * (policy.cpp:73-80) + fallback_quantize (quant.cpp:128-176, quant.hpp:74-75) +
+ * masked-block count (mask_rate numerator, policy.cpp:82-87) + optional fused
+ * quantize_stochastic context codes (quant.cpp:55-84, trainsim.cpp:100-102).
+ * One read of x.  Any output pointer may be NULL to skip that output except
+ * that mask modes != NONE need mask_bits, and res_codes/res_scales go together.
+ * mask_bits is zeroed by this call in THRESHOLD mode; *masked_count is
+ * overwritten.  sr_codes (if non-NULL) shares `scales` with the RTN codes and
+ * uses RNG index (sr_row_offset + r) * cols + c (row offset = token-shard
+ * start; 0 reproduces the reference). */
+int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                               int mask_mode, double theta, uint32_t* mask_bits, int8_t* codes,
+                               int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
+                               int32_t* masked_count, float* amax_out, int8_t* sr_codes,
+                               uint64_t sr_seed, int64_t sr_row_offset, fbq_stream_t stream);
+
+/* quantize_rtn -- quant.cpp:36-53 / quant.hpp:61 */
+int fbq_cuda_quantize_rtn(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                          int8_t* codes, int64_t ldq, float* scales, fbq_stream_t stream);
+
+/* K2: quantize_stochastic -- quant.cpp:55-84 / quant.hpp:65-66 (seed = the
+ * DeterministicRng seed, e.g. derive_seed(base, layer*4+tag, step), trainsim.cpp:16-19) */
+int fbq_cuda_quantize_stochastic(const void* x, int dtype, int64_t rows, int64_t cols,
+                                 int64_t ldx, uint64_t seed, int64_t row_offset, int8_t* codes,
+                                 int64_t ldq, float* scales, fbq_stream_t stream);
+
+/* K3: block_quant_gemm (gemm.cpp:190-193, gemm.hpp:41-42) when mask_bits == NULL,
+ * fallback_gemm (gemm.cpp:195-198, gemm.hpp:47-48) otherwise.
+ *   out[M x N] (+)= sum over ascending k-blocks of the scaled int32 block products.
+ *   A[m,k] = a_codes[m*lda + k]  (K-major)   or  a_codes[k*lda + m]  (MN-major)
+ *   B[k,n] = b_codes[n*ldb + k]  (K-major)   or  b_codes[k*ldb + n]  (MN-major)
+ * Scale grids are the STORED tensors' own grids (row-major): A K-major
+ * [ceil(M/128)][ceil(K/128)], A MN-major [ceil(K/128)][ceil(M/128)], B K-major
+ * [ceil(N/128)][ceil(K/128)], B MN-major [ceil(K/128)][ceil(N/128)].  mask_bits,
+ * res_codes (same layout/ld as A) and res_scales index A's stored grid.
+ * The reference's B operand (quantize_rtn(transpose(W)), trainsim.cpp:96-97)
+ * is MN-major; W's own quantization (trainsim.cpp:121) used K-major is the same
+ * bytes transposed, so one W quantization serves forward and dgrad.
+ * accumulate=1 performs out = fl(out + acc) (trainsim.cpp:125 grad_w_ += gw).
+ * out_dtype FBQ_F32 (parity) or FBQ_BF16. */
+int fbq_cuda_gemm(const int8_t* a_codes, int64_t lda, const float* a_scales, int a_major,
+                  const int8_t* b_codes, int64_t ldb, const float* b_scales, int b_major,
+                  const uint32_t* mask_bits, const int8_t* res_codes, const float* res_scales,
+                  int64_t M, int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo,
+                  int accumulate, int epilogue, fbq_stream_t stream);
+
+/* Debug/parity: the raw per-block int32 products of the same tcgen05 path
+ * (gemm.cpp:140-145 pbuf), out[((bi*NB+bj)*KB+bk)*16384 + r*128 + c]; the
+ * residual products (fallback) follow at element offset MB*NB*KB*16384. */
+int fbq_cuda_gemm_block_products(const int8_t* a_codes, int64_t lda, int a_major,
+                                 const int8_t* b_codes, int64_t ldb, int b_major,
+                                 const uint32_t* mask_bits, const int8_t* res_codes, int64_t M,
+                                 int64_t N, int64_t K, int32_t* out, fbq_stream_t stream);
+
+/* K4: dequantize (quant.cpp:86-104) / dequantize_fallback (quant.cpp:178-202)
+ * when mask_bits != NULL.  out fp32 rows x ldo. */
+int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
+                        const uint32_t* mask_bits, const int8_t* res_codes,
+                        const float* res_scales, int64_t rows, int64_t cols, float* out,
+                        int64_t ldo, fbq_stream_t stream);
+
+/* Rounding probes for exhaustive tests: out_rtn[i] = RTN code of x[i]/a[i]
+ * (kernels.cpp:24-40), out_sr[i] = SR code with RNG bits[i] (quant.cpp:69-77). */
+int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
+                         int8_t* out_sr, int64_t n, fbq_stream_t stream);
+
+/* ---- host entry points (reference value semantics; host buffers) --------
+ * A fallback-quantized linear layer + SwiGLU MLP driver mirroring
+ * QuantLinearLayer::forward/backward (trainsim.cpp:61-127) and the gate/up ->
+ * GluCombine -> down data flow (trainsim.cpp:294-308) for B200.  Declared in
+ * fbq_b200_host.h. */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBQ_B200_H */

@@ -1,0 +1,371 @@
+"""TEST INFRASTRUCTURE ONLY -- numpy/ctypes front-end to the CPU checkers.
+
+Two libraries with the same vocabulary:
+
+* ``C``   -> ``oracle/liboracle.so``: our plain-C restatement (fbq_oracle.c) of
+  the reference arithmetic, each function citing the reference file:line.
+* ``REF`` -> ``oracle/_ref/libfbq_ref.so``: the UNMODIFIED reference library
+  (/root/reference/proj/src compiled by oracle/Makefile) behind a C shim.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+cpu_baseline / ``--impl reference`` legs may import this module.  The product
+package (paper_2503_08040_b200) never does.
+
+Layout conventions follow fbq_oracle.h: int16 codes, row-major block grids, a
+dense residual plane for fallback tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libfbq_ref.so")
+REF_SRC = "/root/reference/proj"
+
+_p = np.ctypeslib.ndpointer
+F32 = _p(np.float32, flags="C_CONTIGUOUS")
+F64 = _p(np.float64, flags="C_CONTIGUOUS")
+I16 = _p(np.int16, flags="C_CONTIGUOUS")
+I32 = _p(np.int32, flags="C_CONTIGUOUS")
+U8 = _p(np.uint8, flags="C_CONTIGUOUS")
+i64, u64, dbl, cint = C.c_int64, C.c_uint64, C.c_double, C.c_int
+
+
+def build(ref: bool | None = None) -> None:
+    """Build liboracle.so (always) and _ref (when the reference tree exists)."""
+    subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
+    if ref is None:
+        ref = os.path.isdir(REF_SRC)
+    if ref:
+        subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+
+
+def cdiv(a: int, b: int) -> int:
+    return (a + b - 1) // b
+
+
+class _Lib:
+    def __init__(self, path: str, prefix: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (run `make -C oracle` / `make -C oracle ref`)")
+        self.lib = C.CDLL(path)
+        self.p = prefix
+        self.path = path
+
+    def f(self, name, res, *args):
+        fn = getattr(self.lib, self.p + name)
+        fn.restype = res
+        fn.argtypes = list(args)
+        return fn
+
+
+class Oracle:
+    """Reference-shaped numpy API over either library (``prefix`` orc_ / ref_)."""
+
+    def __init__(self, path: str, prefix: str):
+        self._l = _Lib(path, prefix)
+        f = self._l.f
+        self.is_ref = prefix == "ref_"
+        self._bits_at = f("bits_at", u64, u64, u64)
+        self._uniform_at = f("uniform_at", dbl, u64, u64)
+        self._normal_at = f("normal_at", C.c_float, u64, u64)
+        self._derive_seed = f("derive_seed", u64, u64, u64, u64)
+        self._qrtn = f("quantize_rtn", cint, F32, i64, i64, i64, i64, cint, I16, F32)
+        if self.is_ref:
+            self._qsr = f("quantize_stochastic", cint, F32, i64, i64, i64, i64, cint, u64, I16, F32)
+            self._fq = f("fallback_quantize", cint, F32, i64, i64, i64, U8, I16, F32, I16, F32, I32,
+                         C.POINTER(i64))
+            self._bqg = f("block_quant_gemm", cint, I16, F32, I16, F32, i64, i64, i64, i64, F32)
+            self._fbg = f("fallback_gemm", cint, I16, F32, U8, I16, F32, I16, F32, i64, i64, i64,
+                          i64, F32)
+            self._tbg = f("tiled_block_gemm", cint, I16, F32, I16, F32, i64, i64, i64, i64, i64,
+                          i64, i64, F32)
+            self._dqf = f("dequantize_fallback", cint, I16, F32, U8, I16, F32, i64, i64, i64, F32)
+            self._ctl = f("controller_update", cint, dbl, dbl, dbl, dbl, dbl, dbl,
+                          C.POINTER(dbl), C.POINTER(dbl))
+            self._set_threads = f("set_gemm_threads", None, cint)
+            self._err = f("last_error", C.c_char_p)
+        else:
+            self._qsr = f("quantize_stochastic", cint, F32, i64, i64, i64, i64, cint, u64, i64, I16,
+                          F32)
+            self._fq = f("fallback_quantize", cint, F32, i64, i64, i64, U8, I16, F32, I16, F32)
+            self._bg = f("block_gemm", cint, I16, F32, C.c_void_p, C.c_void_p, C.c_void_p, I16,
+                         F32, i64, i64, i64, i64, i64, i64, i64, F32)
+            self._bp = f("block_products", cint, I16, I16, i64, i64, i64, i64, I32)
+            self._dqf = f("dequantize_fallback", cint, I16, F32, U8, I16, F32, i64, i64, i64, F32)
+            self._ctl = f("controller_update", cint, dbl, dbl, dbl, dbl, dbl, C.POINTER(dbl))
+            self._cmp = f("compare", cint, F32, F32, i64, F64)
+        self._dq = f("dequantize", cint, I16, F32, i64, i64, i64, i64, *( [cint] if self.is_ref else []), F32)
+        self._tqt = f("transpose_qt", cint, I16, F32, i64, i64, i64, i64, I16, F32)
+        self._oracle = f("gemm_oracle", cint, F32, F32, i64, i64, i64, F32)
+        self._score = f("score_blocks_absmax", cint, F32, i64, i64, i64, F64)
+        self._mthr = f("mask_threshold", cint, F64, i64, dbl, U8)
+        self._mtopk = f("mask_topk", cint, F64, i64, dbl, U8)
+        self._mrate = f("mask_rate", dbl, U8, i64)
+
+    # -- helpers -------------------------------------------------------------
+    def _chk(self, rc, what):
+        if rc != 0:
+            msg = self._err().decode() if self.is_ref else "invalid argument"
+            raise ValueError(f"{what}: {msg}")
+
+    def set_gemm_threads(self, n: int) -> None:
+        if self.is_ref:
+            self._set_threads(int(n))
+
+    # -- rng.hpp -------------------------------------------------------------
+    def bits_at(self, seed, n):
+        return self._bits_at(seed, n)
+
+    def uniform_at(self, seed, n):
+        return self._uniform_at(seed, n)
+
+    def normal_at(self, seed, n):
+        return self._normal_at(seed, n)
+
+    def derive_seed(self, base, a, b=0):
+        return self._derive_seed(base, a, b)
+
+    def layer_seed(self, base, layer_id, tag, step):  # trainsim.cpp:16-19
+        return self.derive_seed(base, layer_id * 4 + tag, step)
+
+    # -- quant.hpp -----------------------------------------------------------
+    def quantize_rtn(self, x, gr=128, gc=128, bits=8):
+        x = np.ascontiguousarray(x, np.float32)
+        r, c = x.shape
+        codes = np.zeros((r, c), np.int16)
+        scales = np.zeros((cdiv(r, gr), cdiv(c, gc)), np.float32)
+        self._chk(self._qrtn(x, r, c, gr, gc, bits, codes, scales), "quantize_rtn")
+        return codes, scales
+
+    def quantize_stochastic(self, x, seed, gr=128, gc=128, bits=8, row_offset=0):
+        x = np.ascontiguousarray(x, np.float32)
+        r, c = x.shape
+        codes = np.zeros((r, c), np.int16)
+        scales = np.zeros((cdiv(r, gr), cdiv(c, gc)), np.float32)
+        if self.is_ref:
+            if row_offset:
+                raise ValueError("reference has no row offset")
+            rc = self._qsr(x, r, c, gr, gc, bits, seed, codes, scales)
+        else:
+            rc = self._qsr(x, r, c, gr, gc, bits, seed, row_offset, codes, scales)
+        self._chk(rc, "quantize_stochastic")
+        return codes, scales
+
+    def dequantize(self, codes, scales, gr=128, gc=128):
+        codes = np.ascontiguousarray(codes, np.int16)
+        r, c = codes.shape
+        out = np.zeros((r, c), np.float32)
+        args = [codes, np.ascontiguousarray(scales, np.float32), r, c, gr, gc]
+        if self.is_ref:
+            args.append(8)
+        self._chk(self._dq(*args, out), "dequantize")
+        return out
+
+    def transpose_qt(self, codes, scales, gr=128, gc=128):
+        r, c = codes.shape
+        oc = np.zeros((c, r), np.int16)
+        os_ = np.zeros((scales.shape[1], scales.shape[0]), np.float32)
+        self._chk(self._tqt(np.ascontiguousarray(codes, np.int16),
+                            np.ascontiguousarray(scales, np.float32), r, c, gr, gc, oc, os_),
+                  "transpose")
+        return oc, os_
+
+    def fallback_quantize(self, x, mask, g=128):
+        """-> codes, scales, res_codes (dense plane), res_scales (grid; 0 unmasked)."""
+        x = np.ascontiguousarray(x, np.float32)
+        r, c = x.shape
+        gr, gc = cdiv(r, g), cdiv(c, g)
+        mask = np.ascontiguousarray(mask, np.uint8).reshape(gr, gc)
+        codes = np.zeros((r, c), np.int16)
+        scales = np.zeros((gr, gc), np.float32)
+        if self.is_ref:
+            n_mask = int(mask.sum())
+            rcomp = np.zeros((max(n_mask, 1), g, g), np.int16)
+            rsc = np.zeros(max(n_mask, 1), np.float32)
+            ridx = np.zeros((gr, gc), np.int32)
+            nres = i64(0)
+            self._chk(self._fq(x, r, c, g, mask, codes, scales, rcomp, rsc, ridx, C.byref(nres)),
+                      "fallback_quantize")
+            res_codes, res_scales = compact_to_dense(rcomp, rsc, ridx, r, c, g)
+            return codes, scales, res_codes, res_scales
+        res_codes = np.zeros((r, c), np.int16)
+        res_scales = np.zeros((gr, gc), np.float32)
+        self._chk(self._fq(x, r, c, g, mask, codes, scales, res_codes, res_scales),
+                  "fallback_quantize")
+        return codes, scales, res_codes, res_scales
+
+    def dequantize_fallback(self, codes, scales, mask, res_codes, res_scales, g=128):
+        r, c = codes.shape
+        out = np.zeros((r, c), np.float32)
+        mask = np.ascontiguousarray(mask, np.uint8)
+        if self.is_ref:
+            rcomp, rsc, _ = dense_to_compact(res_codes, res_scales, mask, g)
+            self._chk(self._dqf(codes, scales, mask, rcomp, rsc, r, c, g, out), "dequantize_fallback")
+        else:
+            self._chk(self._dqf(np.ascontiguousarray(codes, np.int16), np.ascontiguousarray(scales, np.float32),
+                                mask, np.ascontiguousarray(res_codes, np.int16),
+                                np.ascontiguousarray(res_scales, np.float32), r, c, g, out),
+                      "dequantize_fallback")
+        return out
+
+    # -- gemm.hpp ------------------------------------------------------------
+    def block_gemm(self, a_codes, a_scales, b_codes, b_scales, mask=None, res_codes=None,
+                   res_scales=None, g=128, tile=None):
+        """A: m x k codes, B: k x n codes (reference orientation, gemm.cpp:101)."""
+        a_codes = np.ascontiguousarray(a_codes, np.int16)
+        b_codes = np.ascontiguousarray(b_codes, np.int16)
+        a_scales = np.ascontiguousarray(a_scales, np.float32)
+        b_scales = np.ascontiguousarray(b_scales, np.float32)
+        m, k = a_codes.shape
+        k2, n = b_codes.shape
+        assert k == k2
+        out = np.zeros((m, n), np.float32)
+        if self.is_ref:
+            if tile is not None:
+                rc = self._tbg(a_codes, a_scales, b_codes, b_scales, m, n, k, g, *tile, out)
+            elif mask is None:
+                rc = self._bqg(a_codes, a_scales, b_codes, b_scales, m, n, k, g, out)
+            else:
+                mask = np.ascontiguousarray(mask, np.uint8)
+                rcomp, rsc, _ = dense_to_compact(res_codes, res_scales, mask, g)
+                rc = self._fbg(a_codes, a_scales, mask, rcomp, rsc, b_codes, b_scales, m, n, k, g,
+                               out)
+        else:
+            tm, tn, tk = tile if tile is not None else (0, 0, 0)
+            if mask is not None:
+                mask = np.ascontiguousarray(mask, np.uint8)
+                res_codes = np.ascontiguousarray(res_codes, np.int16)
+                res_scales = np.ascontiguousarray(res_scales, np.float32)
+                ptrs = [mask.ctypes.data, res_codes.ctypes.data, res_scales.ctypes.data]
+            else:
+                ptrs = [None, None, None]
+            rc = self._bg(a_codes, a_scales, *ptrs, b_codes, b_scales, m, n, k, g, tm, tn, tk, out)
+        self._chk(rc, "block_gemm")
+        return out
+
+    def block_products(self, a_codes, b_codes, g=128):
+        assert not self.is_ref
+        m, k = a_codes.shape
+        n = b_codes.shape[1]
+        out = np.zeros((cdiv(m, g), cdiv(n, g), cdiv(k, g), g, g), np.int32)
+        self._chk(self._bp(np.ascontiguousarray(a_codes, np.int16),
+                           np.ascontiguousarray(b_codes, np.int16), m, n, k, g, out),
+                  "block_products")
+        return out
+
+    def gemm_oracle(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        m, k = a.shape
+        n = b.shape[1]
+        out = np.zeros((m, n), np.float32)
+        self._chk(self._oracle(a, b, m, n, k, out), "gemm_oracle")
+        return out
+
+    def compare(self, actual, reference):
+        out = np.zeros(4, np.float64)
+        self._cmp(np.ascontiguousarray(actual, np.float32).ravel(),
+                  np.ascontiguousarray(reference, np.float32).ravel(), actual.size, out)
+        return dict(rmse=out[0], max_abs_err=out[1], cosine_similarity=out[2],
+                    underflow_fraction=out[3])
+
+    # -- policy.hpp ----------------------------------------------------------
+    def score_blocks_absmax(self, x, g=128):
+        x = np.ascontiguousarray(x, np.float32)
+        r, c = x.shape
+        s = np.zeros((cdiv(r, g), cdiv(c, g)), np.float64)
+        self._chk(self._score(x, r, c, g, s), "score_blocks")
+        return s
+
+    def mask_threshold(self, scores, theta):
+        s = np.ascontiguousarray(scores, np.float64)
+        m = np.zeros(s.shape, np.uint8)
+        self._chk(self._mthr(s.ravel(), s.size, theta, m.reshape(-1)), "mask_threshold")
+        return m
+
+    def mask_topk(self, scores, rate):
+        s = np.ascontiguousarray(scores, np.float64)
+        m = np.zeros(s.shape, np.uint8)
+        self._chk(self._mtopk(s.ravel(), s.size, rate, m.reshape(-1)), "mask_topk")
+        return m
+
+    def mask_rate(self, mask):
+        m = np.ascontiguousarray(mask, np.uint8).ravel()
+        return self._mrate(m, m.size)
+
+    def controller_update(self, threshold, observed, r_min=0.1, r_max=0.3, alpha=1.3):
+        out = dbl(0)
+        if self.is_ref:
+            lr = dbl(0)
+            self._chk(self._ctl(threshold, 0.0, observed, r_min, r_max, alpha, C.byref(out),
+                                C.byref(lr)), "controller_update")
+        else:
+            self._chk(self._ctl(threshold, observed, r_min, r_max, alpha, C.byref(out)),
+                      "controller_update")
+        return out.value
+
+
+def compact_to_dense(rcomp, rsc, ridx, rows, cols, g):
+    """Reference residuals[] + residual_index[] (quant.hpp:46-52) -> dense plane."""
+    gr, gc = ridx.shape
+    res_codes = np.zeros((rows, cols), np.int16)
+    res_scales = np.zeros((gr, gc), np.float32)
+    for bi in range(gr):
+        for bj in range(gc):
+            s = ridx[bi, bj]
+            if s < 0:
+                continue
+            er, ec = min(g, rows - bi * g), min(g, cols - bj * g)
+            blk = rcomp[s].reshape(-1)[: er * ec].reshape(er, ec)
+            res_codes[bi * g: bi * g + er, bj * g: bj * g + ec] = blk
+            res_scales[bi, bj] = rsc[s]
+    return res_codes, res_scales
+
+
+def dense_to_compact(res_codes, res_scales, mask, g):
+    rows, cols = res_codes.shape
+    gr, gc = mask.shape
+    n = int(mask.sum())
+    rcomp = np.zeros((max(n, 1), g, g), np.int16)
+    rsc = np.zeros(max(n, 1), np.float32)
+    ridx = -np.ones((gr, gc), np.int32)
+    s = 0
+    for bi in range(gr):
+        for bj in range(gc):
+            if not mask[bi, bj]:
+                continue
+            er, ec = min(g, rows - bi * g), min(g, cols - bj * g)
+            rcomp[s].reshape(-1)[: er * ec] = res_codes[bi * g: bi * g + er,
+                                                        bj * g: bj * g + ec].reshape(-1)
+            rsc[s] = res_scales[bi, bj]
+            ridx[bi, bj] = s
+            s += 1
+    return rcomp, rsc, ridx
+
+
+_C = None
+_REF = None
+
+
+def C_oracle() -> Oracle:
+    global _C
+    if _C is None:
+        if not os.path.exists(ORACLE_SO):
+            build(ref=False)
+        _C = Oracle(ORACLE_SO, "orc_")
+    return _C
+
+
+def REF_oracle() -> Oracle | None:
+    """The reference itself, or None when oracle/_ref was not built."""
+    global _REF
+    if _REF is None and os.path.exists(REF_SO):
+        _REF = Oracle(REF_SO, "ref_")
+    return _REF

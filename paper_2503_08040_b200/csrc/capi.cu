@@ -1,0 +1,208 @@
+// extern "C" boundary: argument checking + dispatch to the sm_100a kernels.
+// See include/fbq_b200.h for the contract of every entry point.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/fbq_b200.h"
+#include "gemm_kernel.cuh"
+#include "quant_kernels.cuh"
+
+namespace {
+
+thread_local int g_last_cuda = 0;
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FBQ_OK;
+  g_last_cuda = (int)e;
+  return FBQ_ERR_CUDA;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_x(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows > 0 && cols > 0 && (x == nullptr || ldx < cols)) return FBQ_ERR_ARG;
+  if (cdiv(rows, 128) > 65535) return FBQ_ERR_UNSUPPORTED;  // grid.y limit
+  return FBQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fbq_version(void) { return "fbq-b200 0.1 (sm_100a)"; }
+int fbq_block_side(void) { return 128; }
+int fbq_last_cuda_error(void) { return g_last_cuda; }
+
+const char* fbq_status_string(int s) {
+  switch (s) {
+    case FBQ_OK: return "ok";
+    case FBQ_ERR_SHAPE: return "shape/geometry mismatch";
+    case FBQ_ERR_UNSUPPORTED: return "unsupported geometry, bit-width or alignment";
+    case FBQ_ERR_CUDA: return "CUDA error";
+    case FBQ_ERR_ARG: return "invalid argument";
+    default: return "unknown status";
+  }
+}
+
+int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                               int mask_mode, double theta, uint32_t* mask_bits, int8_t* codes,
+                               int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
+                               int32_t* masked_count, float* amax_out, int8_t* sr_codes,
+                               uint64_t sr_seed, int64_t sr_row_offset, fbq_stream_t stream) {
+  if (int st = check_x(x, dtype, rows, cols, ldx)) return st;
+  if (mask_mode < FBQ_MASK_NONE || mask_mode > FBQ_MASK_GIVEN) return FBQ_ERR_ARG;
+  if (mask_mode != FBQ_MASK_NONE && mask_bits == nullptr) return FBQ_ERR_ARG;
+  if (mask_mode == FBQ_MASK_THRESHOLD && !(theta > 0.0)) return FBQ_ERR_ARG;  // policy.cpp:74
+  if ((res_codes == nullptr) != (res_scales == nullptr)) return FBQ_ERR_ARG;
+  if ((codes || res_codes || sr_codes) && ldq < cols) return FBQ_ERR_ARG;
+  if (sr_row_offset < 0) return FBQ_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t grid = cdiv(rows, 128) * cdiv(cols, 128);
+  if (mask_mode == FBQ_MASK_THRESHOLD && grid > 0) {
+    if (int st = cuda_status(cudaMemsetAsync(mask_bits, 0, (size_t)cdiv(grid, 32) * 4, s)))
+      return st;
+  }
+  if (masked_count) {
+    if (int st = cuda_status(cudaMemsetAsync(masked_count, 0, sizeof(int32_t), s))) return st;
+  }
+  if (grid == 0) return FBQ_OK;
+  fbq::QuantParams p{};
+  p.x = x;
+  p.rows = rows;
+  p.cols = cols;
+  p.ldx = ldx;
+  p.ldq = ldq;
+  p.mask_mode = mask_mode;
+  p.theta = theta;
+  p.mask_bits = mask_bits;
+  p.codes = codes;
+  p.scales = scales;
+  p.res_codes = res_codes;
+  p.res_scales = res_scales;
+  p.masked_count = masked_count;
+  p.amax_out = amax_out;
+  p.sr_codes = sr_codes;
+  p.sr_seed = sr_seed;
+  p.row_offset = sr_row_offset;
+  return cuda_status(fbq::launch_quantize(p, dtype == FBQ_BF16, s));
+}
+
+int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                          float* amax, fbq_stream_t stream) {
+  if (amax == nullptr && rows > 0 && cols > 0) return FBQ_ERR_ARG;
+  return fbq_cuda_quantize_fallback(x, dtype, rows, cols, ldx, FBQ_MASK_NONE, 1.0, nullptr,
+                                    nullptr, cols, nullptr, nullptr, nullptr, nullptr, amax,
+                                    nullptr, 0, 0, stream);
+}
+
+int fbq_cuda_quantize_rtn(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                          int8_t* codes, int64_t ldq, float* scales, fbq_stream_t stream) {
+  if ((codes == nullptr || scales == nullptr) && rows > 0 && cols > 0) return FBQ_ERR_ARG;
+  return fbq_cuda_quantize_fallback(x, dtype, rows, cols, ldx, FBQ_MASK_NONE, 1.0, nullptr, codes,
+                                    ldq, scales, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0,
+                                    stream);
+}
+
+int fbq_cuda_quantize_stochastic(const void* x, int dtype, int64_t rows, int64_t cols,
+                                 int64_t ldx, uint64_t seed, int64_t row_offset, int8_t* codes,
+                                 int64_t ldq, float* scales, fbq_stream_t stream) {
+  if ((codes == nullptr || scales == nullptr) && rows > 0 && cols > 0) return FBQ_ERR_ARG;
+  return fbq_cuda_quantize_fallback(x, dtype, rows, cols, ldx, FBQ_MASK_NONE, 1.0, nullptr,
+                                    nullptr, ldq, scales, nullptr, nullptr, nullptr, nullptr,
+                                    codes, seed, row_offset, stream);
+}
+
+static int gemm_common(const int8_t* a_codes, int64_t lda, const float* a_scales, int a_major,
+                       const int8_t* b_codes, int64_t ldb, const float* b_scales, int b_major,
+                       const uint32_t* mask_bits, const int8_t* res_codes,
+                       const float* res_scales, int64_t M, int64_t N, int64_t K, void* out,
+                       int out_dtype, int64_t ldo, int accumulate, int epi, int32_t* dump,
+                       cudaStream_t s) {
+  if (M < 0 || N < 0 || K < 0) return FBQ_ERR_SHAPE;
+  if ((a_major != 0 && a_major != 1) || (b_major != 0 && b_major != 1)) return FBQ_ERR_ARG;
+  if (out_dtype != FBQ_F32 && out_dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (M == 0 || N == 0) return FBQ_OK;
+  if (dump == nullptr && (out == nullptr || ldo < N)) return FBQ_ERR_ARG;
+  if (K == 0) {  // empty reduction: the reference returns zeros (gemm.cpp:128)
+    if (dump || accumulate) return FBQ_OK;
+    const size_t esz = out_dtype == FBQ_F32 ? 4 : 2;
+    return cuda_status(cudaMemset2DAsync(out, (size_t)ldo * esz, 0, (size_t)N * esz, (size_t)M, s));
+  }
+  if (!a_codes || !b_codes) return FBQ_ERR_ARG;
+  if (dump == nullptr && (!a_scales || !b_scales)) return FBQ_ERR_ARG;
+  if (mask_bits && (!res_codes || (dump == nullptr && !res_scales))) return FBQ_ERR_ARG;
+  // TMA: 16-byte aligned bases and row strides
+  if (!aligned16(a_codes) || !aligned16(b_codes) || (res_codes && !aligned16(res_codes)) ||
+      lda % 16 || ldb % 16)
+    return FBQ_ERR_UNSUPPORTED;
+  if (lda < (a_major == 0 ? K : M) || ldb < (b_major == 0 ? K : N)) return FBQ_ERR_SHAPE;
+  fbq::GemmOperands o{a_codes, lda, res_codes, b_codes, ldb};
+  fbq::GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.MB = (int)cdiv(M, 128);
+  p.NB = (int)cdiv(N, 128);
+  p.KB = (int)cdiv(K, 128);
+  p.a_major = a_major;
+  p.b_major = b_major;
+  p.a_scales = a_scales;
+  p.b_scales = b_scales;
+  p.mask_bits = mask_bits;
+  p.res_scales = res_scales;
+  p.out = out;
+  p.ldo = ldo;
+  p.out_bf16 = out_dtype == FBQ_BF16;
+  p.accumulate = accumulate ? 1 : 0;
+  p.vec_store = (out != nullptr) && aligned16(out) && (ldo % 4 == 0);
+  p.dump = dump;
+  p.dump_res_offset = (int64_t)p.MB * p.NB * p.KB * 128 * 128;
+  return cuda_status(fbq::launch_gemm(o, p, dump ? fbq::kEpiDump : epi, s));
+}
+
+int fbq_cuda_gemm(const int8_t* a_codes, int64_t lda, const float* a_scales, int a_major,
+                  const int8_t* b_codes, int64_t ldb, const float* b_scales, int b_major,
+                  const uint32_t* mask_bits, const int8_t* res_codes, const float* res_scales,
+                  int64_t M, int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo,
+                  int accumulate, int epilogue, fbq_stream_t stream) {
+  if (epilogue != FBQ_EPI_EXACT && epilogue != FBQ_EPI_FMA) return FBQ_ERR_ARG;
+  return gemm_common(a_codes, lda, a_scales, a_major, b_codes, ldb, b_scales, b_major, mask_bits,
+                     res_codes, res_scales, M, N, K, out, out_dtype, ldo, accumulate, epilogue,
+                     nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fbq_cuda_gemm_block_products(const int8_t* a_codes, int64_t lda, int a_major,
+                                 const int8_t* b_codes, int64_t ldb, int b_major,
+                                 const uint32_t* mask_bits, const int8_t* res_codes, int64_t M,
+                                 int64_t N, int64_t K, int32_t* out, fbq_stream_t stream) {
+  if (out == nullptr) return FBQ_ERR_ARG;
+  return gemm_common(a_codes, lda, nullptr, a_major, b_codes, ldb, nullptr, b_major, mask_bits,
+                     res_codes, nullptr, M, N, K, nullptr, FBQ_F32, 0, 0, FBQ_EPI_EXACT, out,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
+                        const uint32_t* mask_bits, const int8_t* res_codes,
+                        const float* res_scales, int64_t rows, int64_t cols, float* out,
+                        int64_t ldo, fbq_stream_t stream) {
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!codes || !scales || !out || ldq < cols || ldo < cols) return FBQ_ERR_ARG;
+  if (mask_bits && (!res_codes || !res_scales)) return FBQ_ERR_ARG;
+  fbq::DequantParams p{codes, scales, mask_bits, res_codes, res_scales, rows, cols, ldq, ldo, out};
+  return cuda_status(fbq::launch_dequantize(p, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
+                         int8_t* out_sr, int64_t n, fbq_stream_t stream) {
+  if (n < 0) return FBQ_ERR_SHAPE;
+  if (n == 0) return FBQ_OK;
+  if (!x || !a || (out_sr && !bits)) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_round_probe(x, a, bits, out_rtn, out_sr, n,
+                                             reinterpret_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Bit-exact rounding primitives shared by the quantizer kernels.
+//
+// The reference quantizes with a DOUBLE divide + nearbyint
+// (kernels.cpp:24-40 / kernels_avx2.cpp:42-77) and stochastic-rounds with a
+// double divide + floor + splitmix64 uniform (quant.cpp:66-80, rng.hpp:11-35).
+// Double division would cost ~10-20 FP64 instructions per element and make the
+// HBM-bound quantizers issue-bound, so we compute the same results from an
+// fp32 reciprocal estimate plus an EXACT fp32 FMA remainder:
+//
+//   n   = rint(x * (1/a))            (|x/a - n| <= 1/2 + 2^-16)
+//   rem = fma(-n, a, x)              exact: x - n*a is representable
+//   2|rem| >  a  -> n += sign(rem)   (n was off by one)
+//   2|rem| == a  -> exact tie x/a = n +- 1/2: pick the even neighbour
+//
+// A double rounding of x/a to 53 bits can neither create nor break a tie
+// (x and a have 24-bit significands, so a non-tie quotient is >= 2^-31
+// relatively away from any half-integer), hence the reference result equals
+// round_half_even(exact x/a), which the above computes.  Blocks whose scale
+// is tiny enough that 1/a could overflow take the plain double path.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fbq {
+
+constexpr int kBlock = 128;  // quantization block side (SPEC.md gemm module, §4.5)
+constexpr int kLevel = 127;  // L = 2^(8-1) - 1 for b = 8 (quant.hpp:16)
+constexpr float kTinyScale = 0x1p-120f;
+
+// a = amax > 0 ? fl(amax / 127) : 0        (quant.cpp:27-32, IEEE RN divide)
+__device__ __forceinline__ float block_scale(float amax) {
+  return amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
+}
+
+// clamp(round_half_even(x / a), -127, 127); a > 0.   kernels.cpp:24-40
+__device__ __forceinline__ int rtn_code(float x, float a, float inv_a) {
+  float n;
+  if (a >= kTinyScale) {
+    n = rintf(__fmul_rn(x, inv_a));
+    const float rem = __fmaf_rn(-n, a, x);
+    const float two = __fmul_rn(2.0f, fabsf(rem));
+    if (two > a) {
+      n = rem > 0.0f ? n + 1.0f : n - 1.0f;
+    } else if (two == a) {
+      // exact tie between n and n + sign(rem): keep the even one
+      const float alt = rem > 0.0f ? n + 1.0f : n - 1.0f;
+      if (fmodf(n, 2.0f) != 0.0f) n = alt;
+    }
+  } else {
+    n = (float)rint(__ddiv_rn((double)x, (double)a));
+  }
+  n = fminf(fmaxf(n, -127.0f), 127.0f);
+  return (int)n;
+}
+
+// splitmix64 finalizer (rng.hpp:11-15)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;  // rng.hpp:29
+
+// Stochastic rounding of x/a given the element's 64 RNG bits
+// (bits_at(lin), rng.hpp:28-35): reference quant.cpp:69-77
+//   t = RN53(x/a); f = floor(t); frac = t - f;
+//   if (frac > 0 && uniform(lin) < frac) f += 1; clamp(+-127)
+// Fast path decides u < frac with an fp32 estimate whenever the two are more
+// than 2^-20 apart (the estimate's error is < 2^-21); otherwise (probability
+// ~2^-19 per element) it recomputes the reference's double formula exactly.
+__device__ __forceinline__ int sr_code(float x, float a, float inv_a, uint64_t bits) {
+  float f;
+  bool slow = a < kTinyScale;
+  if (!slow) {
+    float n0 = floorf(__fmul_rn(x, inv_a));
+    float rem = __fmaf_rn(-n0, a, x);
+    if (rem < 0.0f) {
+      n0 -= 1.0f;
+      rem = __fmaf_rn(-n0, a, x);
+    } else if (rem >= a) {
+      n0 += 1.0f;
+      rem = __fmaf_rn(-n0, a, x);
+    }
+    // now n0 = floor(x/a) exactly, 0 <= rem < a, frac = rem / a
+    const float frac = __fmul_rn(rem, inv_a);
+    const float u = (float)(uint32_t)(bits >> 32) * 0x1p-32f;  // top bits of (bits>>11)*2^-53
+    const float d = u - frac;
+    if (fabsf(d) > 0x1p-20f) {
+      f = (rem > 0.0f && d < 0.0f) ? n0 + 1.0f : n0;
+    } else {
+      slow = true;
+    }
+  }
+  if (slow) {
+    const double t = __ddiv_rn((double)x, (double)a);
+    double fd = floor(t);
+    const double frac = t - fd;
+    const double u = (double)(bits >> 11) * 0x1.0p-53;
+    if (frac > 0.0 && u < frac) fd += 1.0;
+    f = (float)fd;
+  }
+  f = fminf(fmaxf(f, -127.0f), 127.0f);
+  return (int)f;
+}
+
+}  // namespace fbq

@@ -1,0 +1,38 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fbq {
+
+enum EpilogueMode : int { kEpiExact = 0, kEpiFma = 1, kEpiDump = 2 };
+
+struct GemmOperands {
+  const int8_t* a_codes;
+  int64_t lda;
+  const int8_t* res_codes;  // same layout/ld as A, may be null
+  const int8_t* b_codes;
+  int64_t ldb;
+};
+
+struct GemmParams {
+  int64_t M, N, K;
+  int MB, NB, KB;  // ceil(M/128), ceil(N/128), ceil(K/128)
+  int a_major, b_major;  // 0 = K-major, 1 = MN-major
+  const float* a_scales;
+  const float* b_scales;
+  const uint32_t* mask_bits;  // over A's stored block grid; null = block_quant_gemm
+  const float* res_scales;
+  void* out;
+  int64_t ldo;
+  int out_bf16;
+  int accumulate;
+  int vec_store;
+  int32_t* dump;            // kEpiDump: [MB][NB][KB][128][128] primary, then residual
+  int64_t dump_res_offset;  // element offset of the residual products
+  int num_tiles;
+};
+
+cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s);
+int gemm_num_sms();
+
+}  // namespace fbq
