@@ -157,8 +157,9 @@ static int gemm_common(const int8_t* a_codes, int64_t lda, const float* a_scales
   p.ldo = ldo;
   p.out_bf16 = out_dtype == FBQ_BF16;
   p.accumulate = accumulate ? 1 : 0;
-  p.vec_store = (out != nullptr) && aligned16(out) && (ldo % 4 == 0);
+  p.vec_store = (out != nullptr) && aligned16(out) && ((ldo * (out_dtype == FBQ_F32 ? 4 : 2)) % 16 == 0);
   p.dump = dump;
+  p.one = 1.0f;
   p.dump_res_offset = (int64_t)p.MB * p.NB * p.KB * 128 * 128;
   return cuda_status(fbq::launch_gemm(o, p, dump ? fbq::kEpiDump : epi, s));
 }

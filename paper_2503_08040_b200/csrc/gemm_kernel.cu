@@ -12,7 +12,7 @@
 // difference ~5e-8, inside SPEC.md's 1e-5 bound); kEpiDump writes the raw
 // per-block int32 products P (parity of the "per-block INT32 accumulators").
 //
-// Structure (one CTA per SM, persistent, warp-specialised, 320 threads):
+// Structure (one CTA per SM, persistent, warp-specialised, 12 warps):
 //   warp 0      TMA producer: A (128x128 int8), B (256x128 int8) and -- only for
 //               flagged A blocks -- the residual A tile, into a 3-stage
 //               128B-swizzled smem ring (mbarrier full/empty pipeline).
@@ -20,10 +20,16 @@
 //               k-block) issued by one thread into one of two 256-column int32
 //               TMEM slots; every k-block (and every residual) is one "item".
 //               A residual item re-uses the B tile already in smem.
-//   warps 2..9  epilogue: tcgen05.ld the item's int32 block products,
-//               int32->fp32 (exact magic-number conversion), scale and
-//               accumulate in registers; free the TMEM slot; after the last
-//               k-block store the 128x256 fp32/bf16 tile.
+//   warp 2      scale loader: per tile, stages fl(sA*sB), fl(rA*sB) and the
+//               fallback flag of every k-block into a double-buffered smem page
+//               (all roles read the flags from there; no global loads on the
+//               issue paths).
+//   warps 4-11  epilogue (2 warpgroups, setmaxnreg 224): tcgen05.ld the item's
+//               int32 products, restore the TMEM slot to the conversion bias,
+//               int32 -> fp32 with one FADD2 (the slot is pre-biased with
+//               0x4B400000, so as_float(D) = 1.5*2^23 + P exactly), scale and
+//               accumulate with FFMA2 (or FMUL2 + FADD2 in exact mode) in
+//               registers, and after the last k-block store the tile.
 // Operand majorness (K- or MN-major) is a descriptor bit, so the backward
 // products dX = dY W and dW = dY^T X read the SAME int8 code planes as the
 // forward without any transposed copies (reference transposes: quant.cpp:106-126).
@@ -31,7 +37,6 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
-#include <cstdio>
 
 #include "gemm_kernel.cuh"
 #include "sm100.cuh"
@@ -47,31 +52,60 @@ constexpr int kTileB = kBN * kBK;  // 32 KiB
 constexpr int kStageBytes = 2 * kTileA + kTileB;
 constexpr int kTmemCols = 512;     // 2 slots x 256 int32 columns
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + kEpiWarps * 32;
-constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kStageBytes + 256;
+constexpr int kThreads = 128 + kEpiWarps * 32;  // WG0: TMA, MMA, scales, idle; WG1-2: epilogue
+constexpr int kPage = 128;                      // k-blocks per staged scale page
+constexpr uint32_t kBias = 0x4B400000u;         // as_float = 1.5 * 2^23
+constexpr float kBiasF = 12582912.0f;
 
-struct SmemLayout {
-  static __device__ __forceinline__ uint8_t* base(uint8_t* raw) {
-    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  }
+struct ScalePage {
+  float prim[2][kPage];  // fl(sA * sB) for the two 128-column halves
+  float res[2][kPage];   // fl(rA * sB) (flagged k-blocks only)
+  uint8_t flag[kPage];   // fallback bit u(bm, bk)
 };
+
+constexpr size_t kSmemBytes =
+    1024 + (size_t)kStages * kStageBytes + 2 * sizeof(ScalePage) + 256;
 
 __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t blk) {
   return (bits[blk >> 5] >> (blk & 31)) & 1u;
 }
 
+// `one` is a runtime 1.0f: ptxas contracts FMUL2 + FADD2 into FFMA2 even for the
+// _rn intrinsics, but cannot fold a multiply by an unknown value, so the exact
+// chain fl(acc + fl(s*P)) is expressed as FMUL2 then FFMA2(t, one, acc).
 template <int kEpi>
-__global__ void __maxnreg__(200)
+__device__ __forceinline__ void consume(const uint32_t (&v)[32], float2* acc, float s, float one) {
+  const float2 nb = make_float2(-kBiasF, -kBiasF);
+  const float2 s2 = make_float2(s, s);
+  const float2 one2 = make_float2(one, one);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 f = make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+    const float2 pf = __fadd2_rn(f, nb);  // exact: 1.5*2^23 + P - 1.5*2^23
+    if constexpr (kEpi == kEpiExact) {
+      acc[i] = __ffma2_rn(__fmul2_rn(s2, pf), one2, acc[i]);  // fl(acc + fl(s * P))
+    } else {
+      acc[i] = __ffma2_rn(pf, s2, acc[i]);
+    }
+  }
+}
+
+template <int kEpi>
+__global__ void __launch_bounds__(kThreads, 1)
 fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_r,
                 const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = SmemLayout::base(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  ScalePage* pages = reinterpret_cast<ScalePage*>(smem + kStages * kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pages + 2);
   uint64_t* full = bars;                 // [kStages]
   uint64_t* empty = bars + kStages;      // [kStages]
   uint64_t* tfull = bars + 2 * kStages;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;          // [2]
+  uint64_t* sempty = sfull + 2;          // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -86,6 +120,8 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull + s, 1);
       mbar_init(tempty + s, kEpiWarps);
+      mbar_init(sfull + s, 32);
+      mbar_init(sempty + s, kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -102,40 +138,47 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     return p.b_major == 0 ? (int64_t)bn * p.KB + bk : (int64_t)bk * p.NB + bn;
   };
 
+  if (warp < 4) setmaxnreg_dec<56>();
+
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       tma_prefetch(&map_a);
       tma_prefetch(&map_b);
       if (has_res) tma_prefetch(&map_r);
-      const uint64_t pol_a = l2_policy_evict_last();
-      const uint64_t pol_b = l2_policy_evict_last();
+      const uint64_t pol = l2_policy_evict_last();
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, pc = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         const int bm = tile / NT, bn2 = tile % NT;
-        for (int bk = 0; bk < p.KB; ++bk) {
-          const bool masked = has_res && mask_bit(p.mask_bits, a_blk(bm, bk));
-          mbar_wait(empty + stage, phase ^ 1);
-          uint8_t* sa = smem + stage * kStageBytes;
-          uint8_t* sr = sa + kTileA;
-          uint8_t* sb = sa + 2 * kTileA;
-          mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
-          const int k0 = bk * kBK, m0 = bm * kBM, n0 = bn2 * kBN;
-          if (p.a_major == 0) {
-            tma_load_2d(sa, &map_a, full + stage, k0, m0, pol_a);
-            if (masked) tma_load_2d(sr, &map_r, full + stage, k0, m0, pol_a);
-          } else {
-            tma_load_2d(sa, &map_a, full + stage, m0, k0, pol_a);
-            if (masked) tma_load_2d(sr, &map_r, full + stage, m0, k0, pol_a);
+        for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
+          const ScalePage& sp = pages[pc & 1];
+          mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
+          const int nk = min(kPage, p.KB - pg);
+          for (int j = 0; j < nk; ++j) {
+            const int bk = pg + j;
+            const bool masked = sp.flag[j];
+            mbar_wait(empty + stage, phase ^ 1);
+            uint8_t* sa = smem + stage * kStageBytes;
+            uint8_t* sr = sa + kTileA;
+            uint8_t* sb = sa + 2 * kTileA;
+            mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
+            const int k0 = bk * kBK, m0 = bm * kBM, n0 = bn2 * kBN;
+            if (p.a_major == 0) {
+              tma_load_2d(sa, &map_a, full + stage, k0, m0, pol);
+              if (masked) tma_load_2d(sr, &map_r, full + stage, k0, m0, pol);
+            } else {
+              tma_load_2d(sa, &map_a, full + stage, m0, k0, pol);
+              if (masked) tma_load_2d(sr, &map_r, full + stage, m0, k0, pol);
+            }
+            if (p.b_major == 0) {
+              tma_load_2d(sb, &map_b, full + stage, k0, n0, pol);
+            } else {
+              tma_load_2d(sb, &map_b, full + stage, n0, k0, pol);
+              tma_load_2d(sb + kTileA, &map_b, full + stage, n0 + 128, k0, pol);
+            }
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          if (p.b_major == 0) {
-            tma_load_2d(sb, &map_b, full + stage, k0, n0, pol_b);
-          } else {
-            tma_load_2d(sb, &map_b, full + stage, n0, k0, pol_b);
-            tma_load_2d(sb + kTileA, &map_b, full + stage, n0 + 128, k0, pol_b);
-          }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -143,139 +186,237 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // ===================== MMA issuer =====================
     const uint32_t idesc = idesc_i8(kBM, kBN, p.a_major, p.b_major);
     int stage = 0;
-    uint32_t phase = 0;
-    uint32_t item = 0;
+    uint32_t phase = 0, item = 0, pc = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int bm = tile / NT;
-      for (int bk = 0; bk < p.KB; ++bk) {
-        const bool masked = has_res && mask_bit(p.mask_bits, a_blk(bm, bk));
-        mbar_wait(full + stage, phase);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-        const uint32_t sr = sa + kTileA;
-        const uint32_t sb = sa + 2 * kTileA;
-        for (int r = 0; r < (masked ? 2 : 1); ++r) {
-          const uint32_t slot = item & 1;
-          mbar_wait(tempty + slot, ((item >> 1) & 1) ^ 1);
+      for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
+        const ScalePage& sp = pages[pc & 1];
+        mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
+        const int nk = min(kPage, p.KB - pg);
+        for (int j = 0; j < nk; ++j) {
+          const bool masked = sp.flag[j];
+          mbar_wait(full + stage, phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a_base = r ? sr : sa;
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint32_t sr = sa + kTileA;
+          const uint32_t sb = sa + 2 * kTileA;
+          for (int r = 0; r < (masked ? 2 : 1); ++r) {
+            const uint32_t slot = item & 1;
+            mbar_wait(tempty + slot, (item >> 1) & 1);  // slot restored to the bias
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t a_base = r ? sr : sa;
 #pragma unroll
-            for (int kk = 0; kk < kBK / 32; ++kk) {
-              // K-major: advance 32 B inside the 128 B swizzle row;
-              // MN-major: advance 32 k-rows = 4 x (8-row core groups of 1 KiB).
-              const uint32_t a_off = p.a_major == 0 ? kk * 32 : kk * 4096;
-              const uint32_t b_off = p.b_major == 0 ? kk * 32 : kk * 4096;
-              const uint64_t ad = smem_desc_sw128(a_base + a_off, 16, 1024);
-              const uint64_t bd = p.b_major == 0 ? smem_desc_sw128(sb + b_off, 16, 1024)
-                                                 : smem_desc_sw128(sb + b_off, kTileA, 1024);
-              mma_i8(tmem_base + slot * 256, ad, bd, idesc, kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < kBK / 32; ++kk) {
+                // K-major: advance 32 B inside the 128 B swizzle row;
+                // MN-major: advance 32 k-rows = 4 x (8-row core groups of 1 KiB).
+                const uint32_t a_off = p.a_major == 0 ? kk * 32 : kk * 4096;
+                const uint32_t b_off = p.b_major == 0 ? kk * 32 : kk * 4096;
+                const uint64_t ad = smem_desc_sw128(a_base + a_off, 16, 1024);
+                const uint64_t bd = p.b_major == 0 ? smem_desc_sw128(sb + b_off, 16, 1024)
+                                                   : smem_desc_sw128(sb + b_off, kTileA, 1024);
+                mma_i8(tmem_base + slot * 256, ad, bd, idesc, 1u);  // accumulate onto the bias
+              }
+              mma_commit(tfull + slot);
             }
-            mma_commit(tfull + slot);
+            __syncwarp();
+            ++item;
           }
+          if (lane == 0) mma_commit(empty + stage);
           __syncwarp();
-          ++item;
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (lane == 0) mma_commit(empty + stage);
-        __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else {
+  } else if (warp == 2) {
+    // ===================== scale loader =====================
+    uint32_t pc = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int bm = tile / NT, bn2 = tile % NT;
+      const int bn0 = 2 * bn2, bn1 = 2 * bn2 + 1;
+      for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
+        ScalePage& sp = pages[pc & 1];
+        mbar_wait(sempty + (pc & 1), ((pc >> 1) & 1) ^ 1);
+        const int nk = min(kPage, p.KB - pg);
+        for (int j = lane; j < nk; j += 32) {
+          const int bk = pg + j;
+          const int64_t ab = a_blk(bm, bk);
+          const bool masked = has_res && mask_bit(p.mask_bits, ab);
+          float sa = 0.f, ra = 0.f, sb0 = 0.f, sb1 = 0.f;
+          if (p.a_scales) {
+            sa = p.a_scales[ab];
+            ra = masked ? p.res_scales[ab] : 0.0f;
+            sb0 = p.b_scales[b_blk(bk, bn0)];
+            sb1 = bn1 < p.NB ? p.b_scales[b_blk(bk, bn1)] : 0.0f;
+          }
+          sp.prim[0][j] = __fmul_rn(sa, sb0);  // gemm.cpp:163
+          sp.prim[1][j] = __fmul_rn(sa, sb1);
+          sp.res[0][j] = __fmul_rn(ra, sb0);   // gemm.cpp:172
+          sp.res[1][j] = __fmul_rn(ra, sb1);
+          sp.flag[j] = masked ? 1 : 0;
+        }
+        __syncwarp();
+        mbar_arrive(sfull + (pc & 1));
+      }
+    }
+  } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const int ew = warp - 2;
+    setmaxnreg_inc<224>();
+    const int ew = warp - 4;
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int h = ew >> 2;   // which 128-column half of the 256-wide tile
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    uint32_t item = 0;
+
+    // Pre-bias both TMEM slots, then hand them to the MMA warp.
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tmem_st32_const(tmem_base + lane_addr + s * 256 + h * 128 + c * 32, kBias);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(tempty + 0);
+      mbar_arrive(tempty + 1);
+    }
+
+    uint32_t item = 0, pc = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int bm = tile / NT, bn2 = tile % NT;
       const int bn = bn2 * 2 + h;
-      const bool bn_ok = bn < p.NB;
-      float acc[128];
+      float2 acc[64];
 #pragma unroll
-      for (int i = 0; i < 128; ++i) acc[i] = 0.0f;
-      for (int bk = 0; bk < p.KB; ++bk) {
-        const int64_t ab = a_blk(bm, bk);
-        const bool masked = has_res && mask_bit(p.mask_bits, ab);
-        const float sb = bn_ok ? p.b_scales[b_blk(bk, bn)] : 0.0f;
-        for (int r = 0; r < (masked ? 2 : 1); ++r) {
-          const uint32_t slot = item & 1;
-          const float sa = r ? p.res_scales[ab] : p.a_scales[ab];
-          const float s = __fmul_rn(sa, sb);  // gemm.cpp:163 / :172
-          mbar_wait(tfull + slot, (item >> 1) & 1);
-          tc_fence_after();
-          const uint32_t taddr = tmem_base + lane_addr + slot * 256 + h * 128;
+      for (int i = 0; i < 64; ++i) acc[i] = make_float2(0.0f, 0.0f);
+      for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
+        const ScalePage& sp = pages[pc & 1];
+        mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
+        const int nk = min(kPage, p.KB - pg);
+        for (int j = 0; j < nk; ++j) {
+          const bool masked = sp.flag[j];
+          for (int r = 0; r < (masked ? 2 : 1); ++r) {
+            const uint32_t slot = item & 1;
+            const float s = r ? sp.res[h][j] : sp.prim[h][j];
+            mbar_wait(tfull + slot, (item >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + lane_addr + slot * 256 + h * 128;
+            if constexpr (kEpi == kEpiDump) {
+              int32_t* d = p.dump + (r ? p.dump_res_offset : 0) +
+                           ((((int64_t)bm * p.NB + bn) * p.KB + pg + j) * kBM + row_in_tile) * 128;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
-            tmem_ld32(taddr + c * 32, v);
-            tmem_ld_wait();
-            if (c == 3) {
+              for (int c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tb + c * 32, v);
+                tmem_ld_wait();
+                tmem_st32_const(tb + c * 32, kBias);
+                if (bn < p.NB) {
+#pragma unroll
+                  for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<int4*>(d + c * 32 + i) =
+                        make_int4((int)(v[i] - kBias), (int)(v[i + 1] - kBias),
+                                  (int)(v[i + 2] - kBias), (int)(v[i + 3] - kBias));
+                }
+              }
+              tmem_st_wait();
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(tempty + slot);
-            }
-            if constexpr (kEpi == kEpiDump) {
-              const int64_t grow = (int64_t)bm * kBM + row_in_tile;
-              if (bn_ok) {
-                int32_t* d = p.dump + (r ? p.dump_res_offset : 0) +
-                             ((((int64_t)bm * p.NB + bn) * p.KB + bk) * kBM + row_in_tile) * 128 +
-                             c * 32;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) d[i] = (int32_t)v[i];
-              }
-              (void)grow;
             } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                // exact int32 -> fp32 for |P| < 2^22 (128*127^2 = 2,064,512)
-                const float pf = __fsub_rn(__int_as_float((int)v[i] + 0x4B400000), 12582912.0f);
-                if constexpr (kEpi == kEpiExact) {
-                  acc[c * 32 + i] = __fadd_rn(acc[c * 32 + i], __fmul_rn(s, pf));
-                } else {
-                  acc[c * 32 + i] = __fmaf_rn(pf, s, acc[c * 32 + i]);
-                }
-              }
+              uint32_t va[32], vb[32];
+              tmem_ld32(tb + 0, va);
+              tmem_ld_wait();
+              tmem_st32_const(tb + 0, kBias);
+              tmem_ld32(tb + 32, vb);
+              consume<kEpi>(va, acc + 0, s, p.one);
+              tmem_ld_wait();
+              tmem_st32_const(tb + 32, kBias);
+              tmem_ld32(tb + 64, va);
+              consume<kEpi>(vb, acc + 16, s, p.one);
+              tmem_ld_wait();
+              tmem_st32_const(tb + 64, kBias);
+              tmem_ld32(tb + 96, vb);
+              consume<kEpi>(va, acc + 32, s, p.one);
+              tmem_ld_wait();
+              tmem_st32_const(tb + 96, kBias);
+              tmem_st_wait();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(tempty + slot);
+              consume<kEpi>(vb, acc + 48, s, p.one);
             }
+            ++item;
           }
-          ++item;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty + (pc & 1));
       }
       if constexpr (kEpi != kEpiDump) {
         const int64_t grow = (int64_t)bm * kBM + row_in_tile;
         const int64_t gcol0 = (int64_t)bn * 128;
-        if (bn_ok && grow < p.M) {
+        if (bn < p.NB && grow < p.M) {
+          const bool full_row = p.vec_store && gcol0 + 128 <= p.N;
           if (p.out_bf16) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + gcol0;
+            if (full_row) {
 #pragma unroll
-            for (int i = 0; i < 128; ++i) {
-              if (gcol0 + i < p.N) {
-                float val = acc[i];
-                if (p.accumulate) val = __fadd_rn(__bfloat162float(o[i]), val);
-                o[i] = __float2bfloat16_rn(val);
+              for (int i = 0; i < 64; i += 4) {
+                uint4 w;
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+                uint4 old = make_uint4(0, 0, 0, 0);
+                if (p.accumulate) old = *reinterpret_cast<const uint4*>(o + 2 * i);
+                const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float2 v = acc[i + e];
+                  if (p.accumulate) {
+                    const float2 ov = __bfloat1622float2(op[e]);
+                    v = make_float2(__fadd_rn(ov.x, v.x), __fadd_rn(ov.y, v.y));
+                  }
+                  __nv_bfloat162 b = __float22bfloat162_rn(v);
+                  wp[e] = *reinterpret_cast<uint32_t*>(&b);
+                }
+                *reinterpret_cast<uint4*>(o + 2 * i) = w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int64_t col = gcol0 + 2 * i + e;
+                  if (col < p.N) {
+                    float v = e ? acc[i].y : acc[i].x;
+                    if (p.accumulate) v = __fadd_rn(__bfloat162float(o[2 * i + e]), v);
+                    o[2 * i + e] = __float2bfloat16_rn(v);
+                  }
+                }
               }
             }
           } else {
             float* o = reinterpret_cast<float*>(p.out) + grow * p.ldo + gcol0;
-            if (p.vec_store && gcol0 + 128 <= p.N) {
+            if (full_row) {
 #pragma unroll
-              for (int i = 0; i < 128; i += 4) {
-                float4 val = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+              for (int i = 0; i < 64; i += 2) {
+                float4 v = make_float4(acc[i].x, acc[i].y, acc[i + 1].x, acc[i + 1].y);
                 if (p.accumulate) {
-                  const float4 old = *reinterpret_cast<const float4*>(o + i);
-                  val.x = __fadd_rn(old.x, val.x);
-                  val.y = __fadd_rn(old.y, val.y);
-                  val.z = __fadd_rn(old.z, val.z);
-                  val.w = __fadd_rn(old.w, val.w);
+                  const float4 old = *reinterpret_cast<const float4*>(o + 2 * i);
+                  v.x = __fadd_rn(old.x, v.x);
+                  v.y = __fadd_rn(old.y, v.y);
+                  v.z = __fadd_rn(old.z, v.z);
+                  v.w = __fadd_rn(old.w, v.w);
                 }
-                *reinterpret_cast<float4*>(o + i) = val;
+                *reinterpret_cast<float4*>(o + 2 * i) = v;
               }
             } else {
 #pragma unroll
-              for (int i = 0; i < 128; ++i) {
-                if (gcol0 + i < p.N) o[i] = p.accumulate ? __fadd_rn(o[i], acc[i]) : acc[i];
+              for (int i = 0; i < 64; ++i) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int64_t col = gcol0 + 2 * i + e;
+                  if (col < p.N) {
+                    const float v = e ? acc[i].y : acc[i].x;
+                    o[2 * i + e] = p.accumulate ? __fadd_rn(o[2 * i + e], v) : v;
+                  }
+                }
               }
             }
           }
@@ -334,6 +475,22 @@ int gemm_num_sms() {
   return n;
 }
 
+template <int kEpi>
+static cudaError_t launch_typed(const CUtensorMap& ma, const CUtensorMap& mr,
+                                const CUtensorMap& mb, const GemmParams& p, int grid,
+                                cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fbq_gemm_kernel<kEpi>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  fbq_gemm_kernel<kEpi><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s) {
   CUtensorMap ma, mr, mb;
   const int64_t M = p.M, N = p.N, K = p.K;
@@ -352,28 +509,11 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
 
   p.num_tiles = p.MB * ((p.NB + 1) / 2);
   const int grid = p.num_tiles < gemm_num_sms() ? p.num_tiles : gemm_num_sms();
-  cudaError_t e;
   switch (epi) {
-    case kEpiExact:
-      e = cudaFuncSetAttribute(fbq_gemm_kernel<kEpiExact>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-      if (e != cudaSuccess) return e;
-      fbq_gemm_kernel<kEpiExact><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, p);
-      break;
-    case kEpiFma:
-      e = cudaFuncSetAttribute(fbq_gemm_kernel<kEpiFma>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-      if (e != cudaSuccess) return e;
-      fbq_gemm_kernel<kEpiFma><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, p);
-      break;
-    default:
-      e = cudaFuncSetAttribute(fbq_gemm_kernel<kEpiDump>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-      if (e != cudaSuccess) return e;
-      fbq_gemm_kernel<kEpiDump><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, p);
-      break;
+    case kEpiExact: return launch_typed<kEpiExact>(ma, mr, mb, p, grid, s);
+    case kEpiFma: return launch_typed<kEpiFma>(ma, mr, mb, p, grid, s);
+    default: return launch_typed<kEpiDump>(ma, mr, mb, p, grid, s);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace fbq

@@ -30,6 +30,7 @@ struct GemmParams {
   int32_t* dump;            // kEpiDump: [MB][NB][KB][128][128] primary, then residual
   int64_t dump_res_offset;  // element offset of the residual products
   int num_tiles;
+  float one;  // 1.0f (runtime constant for the exact epilogue)
 };
 
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s);

@@ -61,6 +61,16 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   return p;
 }
 
+// Warpgroup register re-balancing (all 4 warps of a warpgroup execute it).
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -114,6 +124,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
         "=r"(r[31])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// Broadcast one 32-bit value into 32 consecutive columns of the warp's 32
+// lanes (4 x .x8 stores: SASS needs consecutive registers, so a wider shape
+// would pin 32 registers to the constant).
+__device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                     taddr + i * 8),
+                 "r"(v)
+                 : "memory");
 }
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (sm_100 layout: version 1 at
