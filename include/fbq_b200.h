@@ -132,6 +132,16 @@ int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
 int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
                          int8_t* out_sr, int64_t n, fbq_stream_t stream);
 
+/* Performance diagnostics only (not part of the reference API): flags
+ * 1 = GEMM epilogue skips its math, 2 = GEMM producer skips the TMA loads,
+ * 4 = GEMM epilogue skips the output stores, 8 = MMA skips the TMEM-slot wait,
+ * 16 = MMA skips the operand-stage wait (races; timing experiments only).
+ * Results are garbage while set; 0 restores normal operation. */
+void fbq_debug_set_gemm_diag(int flags);
+/* device buffer of 5 x num_SMs int64 receiving, per CTA, the MMA warp's total,
+ * operand-wait, TMEM-slot-wait, scale-page-wait and MMA-issue cycles (null disables). */
+void fbq_debug_set_gemm_prof(long long* dev_buf);
+
 /* ---- host entry points (reference value semantics; host buffers) --------
  * A fallback-quantized linear layer + SwiGLU MLP driver mirroring
  * QuantLinearLayer::forward/backward (trainsim.cpp:61-127) and the gate/up ->

@@ -10,6 +10,8 @@
 namespace {
 
 thread_local int g_last_cuda = 0;
+int g_gemm_diag = 0;  // perf diagnostics only (fbq_debug_set_gemm_diag)
+long long* g_gemm_prof = nullptr;
 
 int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return FBQ_OK;
@@ -33,6 +35,11 @@ int check_x(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx) {
 extern "C" {
 
 const char* fbq_version(void) { return "fbq-b200 0.1 (sm_100a)"; }
+/* Performance diagnostics (not part of the reference API): 1 = GEMM epilogue
+ * skips its math, 2 = producer skips TMA loads.  Results are garbage when set. */
+void fbq_debug_set_gemm_diag(int flags) { g_gemm_diag = flags; }
+/* device buffer of 5 x num_SMs int64: MMA-warp total / full-wait / tmem-wait / page-wait / issue cycles */
+void fbq_debug_set_gemm_prof(long long* dev_buf) { g_gemm_prof = dev_buf; }
 int fbq_block_side(void) { return 128; }
 int fbq_last_cuda_error(void) { return g_last_cuda; }
 
@@ -160,6 +167,8 @@ static int gemm_common(const int8_t* a_codes, int64_t lda, const float* a_scales
   p.vec_store = (out != nullptr) && aligned16(out) && ((ldo * (out_dtype == FBQ_F32 ? 4 : 2)) % 16 == 0);
   p.dump = dump;
   p.one = 1.0f;
+  p.diag = g_gemm_diag;
+  p.prof = g_gemm_prof;
   p.dump_res_offset = (int64_t)p.MB * p.NB * p.KB * 128 * 128;
   return cuda_status(fbq::launch_gemm(o, p, dump ? fbq::kEpiDump : epi, s));
 }

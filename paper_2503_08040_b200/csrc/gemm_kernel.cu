@@ -25,11 +25,12 @@
 //               (all roles read the flags from there; no global loads on the
 //               issue paths).
 //   warps 4-11  epilogue (2 warpgroups, setmaxnreg 224): tcgen05.ld the item's
-//               int32 products, restore the TMEM slot to the conversion bias,
-//               int32 -> fp32 with one FADD2 (the slot is pre-biased with
-//               0x4B400000, so as_float(D) = 1.5*2^23 + P exactly), scale and
-//               accumulate with FFMA2 (or FMUL2 + FADD2 in exact mode) in
-//               registers, and after the last k-block store the tile.
+//               int32 products (double-buffered 32-column chunks), free the
+//               TMEM slot, I2F + FFMA2 (FMUL2 + FFMA2 in exact mode) into
+//               register accumulators, and after the last k-block store the
+//               tile.  Measured on B200: the FP32 pipe does 128 element-ops/clk/SM,
+//               so convert + scale-accumulate runs at 64 elements/clk/SM -- exactly
+//               the int8 MMA rate for 128-deep k-blocks (8192 MAC/clk/SM / 128).
 // Operand majorness (K- or MN-major) is a descriptor bit, so the backward
 // products dX = dY W and dW = dY^T X read the SAME int8 code planes as the
 // forward without any transposed copies (reference transposes: quant.cpp:106-126).
@@ -54,8 +55,6 @@ constexpr int kTmemCols = 512;     // 2 slots x 256 int32 columns
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // WG0: TMA, MMA, scales, idle; WG1-2: epilogue
 constexpr int kPage = 128;                      // k-blocks per staged scale page
-constexpr uint32_t kBias = 0x4B400000u;         // as_float = 1.5 * 2^23
-constexpr float kBiasF = 12582912.0f;
 
 struct ScalePage {
   float prim[2][kPage];  // fl(sA * sB) for the two 128-column halves
@@ -70,18 +69,18 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t blk) {
   return (bits[blk >> 5] >> (blk & 31)) & 1u;
 }
 
-// `one` is a runtime 1.0f: ptxas contracts FMUL2 + FADD2 into FFMA2 even for the
-// _rn intrinsics, but cannot fold a multiply by an unknown value, so the exact
-// chain fl(acc + fl(s*P)) is expressed as FMUL2 then FFMA2(t, one, acc).
+// int32 -> fp32 is I2F (one FMA-pipe slot, exact for |P| < 2^24), then one
+// FFMA2 per element pair (FMA mode).  `one` is a runtime 1.0f: ptxas
+// contracts FMUL2 + FADD2 into FFMA2 even for the _rn intrinsics, but cannot
+// fold a multiply by an unknown value, so the exact chain fl(acc + fl(s*P)) is
+// expressed as FMUL2 then FFMA2(t, one, acc).
 template <int kEpi>
 __device__ __forceinline__ void consume(const uint32_t (&v)[32], float2* acc, float s, float one) {
-  const float2 nb = make_float2(-kBiasF, -kBiasF);
   const float2 s2 = make_float2(s, s);
   const float2 one2 = make_float2(one, one);
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const float2 f = make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-    const float2 pf = __fadd2_rn(f, nb);  // exact: 1.5*2^23 + P - 1.5*2^23
+    const float2 pf = make_float2(__int2float_rn((int)v[2 * i]), __int2float_rn((int)v[2 * i + 1]));
     if constexpr (kEpi == kEpiExact) {
       acc[i] = __ffma2_rn(__fmul2_rn(s2, pf), one2, acc[i]);  // fl(acc + fl(s * P))
     } else {
@@ -162,6 +161,11 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             uint8_t* sa = smem + stage * kStageBytes;
             uint8_t* sr = sa + kTileA;
             uint8_t* sb = sa + 2 * kTileA;
+            if (p.diag & 2) {  // diagnostic: no operand traffic
+              mbar_arrive(full + stage);
+              if (++stage == kStages) { stage = 0; phase ^= 1; }
+              continue;
+            }
             mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
             const int k0 = bk * kBK, m0 = bm * kBM, n0 = bn2 * kBN;
             if (p.a_major == 0) {
@@ -183,48 +187,64 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    const uint32_t idesc = idesc_i8(kBM, kBN, p.a_major, p.b_major);
-    int stage = 0;
-    uint32_t phase = 0, item = 0, pc = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
-        const ScalePage& sp = pages[pc & 1];
-        mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
-        const int nk = min(kPage, p.KB - pg);
-        for (int j = 0; j < nk; ++j) {
-          const bool masked = sp.flag[j];
-          mbar_wait(full + stage, phase);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-          const uint32_t sr = sa + kTileA;
-          const uint32_t sb = sa + 2 * kTileA;
-          for (int r = 0; r < (masked ? 2 : 1); ++r) {
-            const uint32_t slot = item & 1;
-            mbar_wait(tempty + slot, (item >> 1) & 1);  // slot restored to the bias
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8(kBM, kBN, p.a_major, p.b_major);
+      // Descriptor templates: per stage only the 14-bit start address changes,
+      // per 32-deep k step the address advances by 32 B (K-major: inside the
+      // 128 B swizzle row) or 4 KiB (MN-major: 32 k-rows of 128 B).
+      const uint32_t a_step = p.a_major == 0 ? (32 >> 4) : (4096 >> 4);
+      const uint32_t b_step = p.b_major == 0 ? (32 >> 4) : (4096 >> 4);
+      const uint64_t a_tmpl = smem_desc_sw128(0, 16, 1024);
+      const uint64_t b_tmpl = smem_desc_sw128(0, p.b_major == 0 ? 16 : kTileA, 1024);
+      const uint32_t smem0 = smem_u32(smem);
+      int stage = 0;
+      uint32_t phase = 0, item = 0, pc = 0;
+      long long t_full = 0, t_tempty = 0, t_page = 0, t_issue = 0;
+      const long long t_start = clock64();
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
+          const ScalePage& sp = pages[pc & 1];
+          long long t0 = clock64();
+          mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
+          t_page += clock64() - t0;
+          const int nk = min(kPage, p.KB - pg);
+          for (int j = 0; j < nk; ++j) {
+            const int n_items = sp.flag[j] ? 2 : 1;
+            t0 = clock64();
+            if (!(p.diag & 16)) mbar_wait(full + stage, phase);
+            t_full += clock64() - t0;
             tc_fence_after();
-            if (lane == 0) {
-              const uint32_t a_base = r ? sr : sa;
+            const uint32_t sa = smem0 + stage * kStageBytes;
+            const uint64_t bd0 = b_tmpl | ((sa + 2 * kTileA) >> 4);
+            for (int r = 0; r < n_items; ++r) {
+              const uint32_t slot = item & 1;
+              t0 = clock64();
+              if (!(p.diag & 8)) mbar_wait(tempty + slot, ((item >> 1) & 1) ^ 1);
+              t_tempty += clock64() - t0;
+              tc_fence_after();
+              t0 = clock64();
+              const uint64_t ad0 = a_tmpl | ((sa + (r ? kTileA : 0)) >> 4);
+              const uint32_t d = tmem_base + slot * 256;
 #pragma unroll
-              for (int kk = 0; kk < kBK / 32; ++kk) {
-                // K-major: advance 32 B inside the 128 B swizzle row;
-                // MN-major: advance 32 k-rows = 4 x (8-row core groups of 1 KiB).
-                const uint32_t a_off = p.a_major == 0 ? kk * 32 : kk * 4096;
-                const uint32_t b_off = p.b_major == 0 ? kk * 32 : kk * 4096;
-                const uint64_t ad = smem_desc_sw128(a_base + a_off, 16, 1024);
-                const uint64_t bd = p.b_major == 0 ? smem_desc_sw128(sb + b_off, 16, 1024)
-                                                   : smem_desc_sw128(sb + b_off, kTileA, 1024);
-                mma_i8(tmem_base + slot * 256, ad, bd, idesc, 1u);  // accumulate onto the bias
-              }
+              for (int kk = 0; kk < kBK / 32; ++kk)
+                mma_i8(d, ad0 + kk * a_step, bd0 + kk * b_step, idesc, kk > 0 ? 1u : 0u);
               mma_commit(tfull + slot);
+              t_issue += clock64() - t0;
+              ++item;
             }
-            __syncwarp();
-            ++item;
+            mma_commit(empty + stage);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          if (lane == 0) mma_commit(empty + stage);
-          __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+      }
+      if (p.prof) {
+        long long* o = p.prof + blockIdx.x * 5;
+        o[0] = clock64() - t_start;
+        o[1] = t_full;
+        o[2] = t_tempty;
+        o[3] = t_page;
+        o[4] = t_issue;
       }
     }
   } else if (warp == 2) {
@@ -267,20 +287,6 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
 
-    // Pre-bias both TMEM slots, then hand them to the MMA warp.
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tmem_st32_const(tmem_base + lane_addr + s * 256 + h * 128 + c * 32, kBias);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(tempty + 0);
-      mbar_arrive(tempty + 1);
-    }
-
     uint32_t item = 0, pc = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int bm = tile / NT, bn2 = tile % NT;
@@ -308,37 +314,36 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 uint32_t v[32];
                 tmem_ld32(tb + c * 32, v);
                 tmem_ld_wait();
-                tmem_st32_const(tb + c * 32, kBias);
                 if (bn < p.NB) {
 #pragma unroll
                   for (int i = 0; i < 32; i += 4)
                     *reinterpret_cast<int4*>(d + c * 32 + i) =
-                        make_int4((int)(v[i] - kBias), (int)(v[i + 1] - kBias),
-                                  (int)(v[i + 2] - kBias), (int)(v[i + 3] - kBias));
+                        make_int4((int)v[i], (int)v[i + 1], (int)v[i + 2], (int)v[i + 3]);
                 }
               }
-              tmem_st_wait();
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(tempty + slot);
             } else {
+              if (p.diag & 1) {  // diagnostic: release the slot without epilogue math
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + slot);
+                ++item;
+                continue;
+              }
               uint32_t va[32], vb[32];
               tmem_ld32(tb + 0, va);
               tmem_ld_wait();
-              tmem_st32_const(tb + 0, kBias);
               tmem_ld32(tb + 32, vb);
               consume<kEpi>(va, acc + 0, s, p.one);
               tmem_ld_wait();
-              tmem_st32_const(tb + 32, kBias);
               tmem_ld32(tb + 64, va);
               consume<kEpi>(vb, acc + 16, s, p.one);
               tmem_ld_wait();
-              tmem_st32_const(tb + 64, kBias);
               tmem_ld32(tb + 96, vb);
               consume<kEpi>(va, acc + 32, s, p.one);
               tmem_ld_wait();
-              tmem_st32_const(tb + 96, kBias);
-              tmem_st_wait();
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(tempty + slot);
@@ -350,7 +355,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         __syncwarp();
         if (lane == 0) mbar_arrive(sempty + (pc & 1));
       }
-      if constexpr (kEpi != kEpiDump) {
+      if (kEpi != kEpiDump && !(p.diag & 4)) {
         const int64_t grow = (int64_t)bm * kBM + row_in_tile;
         const int64_t gcol0 = (int64_t)bn * 128;
         if (bn < p.NB && grow < p.M) {

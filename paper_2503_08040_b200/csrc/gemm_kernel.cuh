@@ -31,6 +31,8 @@ struct GemmParams {
   int64_t dump_res_offset;  // element offset of the residual products
   int num_tiles;
   float one;  // 1.0f (runtime constant for the exact epilogue)
+  int diag;   // perf diagnostics: 1 = skip epilogue math, 2 = skip TMA loads
+  long long* prof;  // perf diagnostics: per-CTA MMA-warp wait cycles (or null)
 };
 
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s);
