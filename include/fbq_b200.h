@@ -82,6 +82,54 @@ int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t c
                                int32_t* masked_count, float* amax_out, int8_t* sr_codes,
                                uint64_t sr_seed, int64_t sr_row_offset, fbq_stream_t stream);
 
+/* Linear-layer input quantizer (QuantLinearLayer::forward, trainsim.cpp:80-102):
+ * as fbq_cuda_quantize_fallback, plus a SECOND stochastic context plane with its
+ * own seed -- layers that share an input (gate/up of a GLU block) each keep the
+ * reference's own context stream -- and an optional device-resident threshold
+ * (theta_dev != NULL overrides theta; see fbq_cuda_controller_update). */
+int fbq_cuda_quantize_linear_input(const void* x, int dtype, int64_t rows, int64_t cols,
+                                   int64_t ldx, int mask_mode, double theta,
+                                   const double* theta_dev, uint32_t* mask_bits,
+                                   int8_t* codes, int64_t ldq, float* scales, int8_t* res_codes,
+                                   float* res_scales, int32_t* masked_count, int8_t* ctx_codes,
+                                   uint64_t ctx_seed, int8_t* ctx_codes2, uint64_t ctx_seed2,
+                                   int64_t row_offset, fbq_stream_t stream);
+
+/* GluCombine::forward (trainsim.cpp:224-246) fused with the down projection's
+ * input quantizer: ab = [a | b] (rows x 2*cols, the gate/up GEMM output, fp32
+ * or bf16); writes the ctx_bits-bit 1x128 RTN contexts of a and b (int16 codes,
+ * trainsim.cpp:240-243) and quantizes h = silu(a)*b exactly like
+ * fbq_cuda_quantize_linear_input (threshold mode) with one context plane.
+ * h itself is not written unless h_out != NULL (fp32, parity/debug).  silu is
+ * evaluated like silu_scalar (trainsim.cpp:38-41): double exp, one rounding. */
+int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, int64_t ld_ab,
+                         int16_t* ctx_a, int16_t* ctx_b, int64_t ld_ctx, float* ctx_a_scales,
+                         float* ctx_b_scales, int ctx_bits, double theta,
+                         const double* theta_dev, uint32_t* mask_bits, int8_t* codes,
+                         int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
+                         int32_t* masked_count, int8_t* ctx_codes, uint64_t ctx_seed,
+                         int64_t row_offset, float* h_out, int64_t ld_h, fbq_stream_t stream);
+
+/* GluCombine::backward (trainsim.cpp:248-263) fused with the gate and up
+ * layers' dY quantizers (trainsim.cpp:117-119): from dH and the dequantized
+ * contexts, ga = dH*b*silu'(a) and gb = dH*silu(a), stochastically rounded
+ * (seeds seed_a / seed_b, RNG index over each rows x cols matrix) into
+ * gq = [q(ga) | q(gb)] (int8 rows x ldq, ldq >= 2*cols) with scale grid
+ * gq_scales [ceil(rows/128)][2*ceil(cols/128)].  g_out (optional fp32
+ * [2][rows][cols]) receives ga, gb for parity checks. */
+int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols, int64_t ld_gh,
+                          const int16_t* ctx_a, const int16_t* ctx_b, int64_t ld_ctx,
+                          const float* ctx_a_scales, const float* ctx_b_scales, int8_t* gq,
+                          int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
+                          int64_t row_offset, float* g_out, fbq_stream_t stream);
+
+/* controller_update (policy.cpp:97-109) on device: rate = *masked_count /
+ * n_blocks; *theta_dev /= alpha if rate < r_min, *= alpha if rate > r_max;
+ * *last_rate_dev = rate (may be NULL). */
+int fbq_cuda_controller_update(double* theta_dev, const int32_t* masked_count, int64_t n_blocks,
+                               double r_min, double r_max, double alpha, double* last_rate_dev,
+                               fbq_stream_t stream);
+
 /* quantize_rtn -- quant.cpp:36-53 / quant.hpp:61 */
 int fbq_cuda_quantize_rtn(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
                           int8_t* codes, int64_t ldq, float* scales, fbq_stream_t stream);
@@ -111,6 +159,17 @@ int fbq_cuda_gemm(const int8_t* a_codes, int64_t lda, const float* a_scales, int
                   const uint32_t* mask_bits, const int8_t* res_codes, const float* res_scales,
                   int64_t M, int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo,
                   int accumulate, int epilogue, fbq_stream_t stream);
+
+/* fbq_cuda_gemm with explicit row strides of the stored scale grids (0 =
+ * natural), so a column slice of a concatenated code plane (e.g. the gate half
+ * of [q(ga) | q(gb)]) can be used as an operand with its parent's scale grid.
+ * Fallback (mask_bits != NULL) needs the natural A grid. */
+int fbq_cuda_gemm_ex(const int8_t* a_codes, int64_t lda, const float* a_scales, int64_t lds_a,
+                     int a_major, const int8_t* b_codes, int64_t ldb, const float* b_scales,
+                     int64_t lds_b, int b_major, const uint32_t* mask_bits,
+                     const int8_t* res_codes, const float* res_scales, int64_t M, int64_t N,
+                     int64_t K, void* out, int out_dtype, int64_t ldo, int accumulate,
+                     int epilogue, fbq_stream_t stream);
 
 /* Debug/parity: the raw per-block int32 products of the same tcgen05 path
  * (gemm.cpp:140-145 pbuf), out[((bi*NB+bj)*KB+bk)*16384 + r*128 + c]; the

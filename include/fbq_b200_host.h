@@ -1,0 +1,78 @@
+/* fbq_b200_host.h -- host-side drivers above the C ABI (include/fbq_b200.h).
+ *
+ * A fallback-quantized SwiGLU MLP (gate/up -> GluCombine -> down) that mirrors
+ * the reference's QuantLinearLayer::forward/backward (trainsim.cpp:61-127) and
+ * GluCombine (trainsim.cpp:224-263) data flow with 128 x 128 blocks, 8-bit
+ * linear operands, 10-bit 1 x 128 non-linear contexts and the delay-threshold
+ * controller (policy.cpp:97-109).  It is the e2e entry point the reference's
+ * callers would bind: fbq_mlp_step_host takes HOST fp32 buffers exactly like
+ * the reference value API (DenseMatrix in, DenseMatrix out) and performs the
+ * host<->device copies itself.
+ *
+ * Per-layer RNG streams follow layer_seed (trainsim.cpp:16-19): gate = layer
+ * layer_id_base, up = +1, down = +2; tag 0 = X context, tag 1 = dY.
+ * gate and up see the same input and start from the same threshold, so the
+ * reference's two controllers evolve identically; the driver keeps one.
+ */
+#ifndef FBQ_B200_HOST_H
+#define FBQ_B200_HOST_H
+
+#include <stdint.h>
+
+#include "fbq_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fbq_mlp_config {
+  int64_t d_model;        /* K of gate/up, N of down */
+  int64_t d_ff;           /* N of gate/up, K of down */
+  int64_t max_tokens;     /* capacity of the device workspaces */
+  int act_dtype;          /* FBQ_F32 / FBQ_BF16: x, dY, y, dX in the device API */
+  int mid_dtype;          /* dtype of the [a|b] and dH intermediates (FBQ_F32 = parity) */
+  int epilogue;           /* FBQ_EPI_EXACT (bit-exact) or FBQ_EPI_FMA */
+  int nonlinear_bits;     /* 10 (QuantConfig::nonlinear_bits, trainsim.hpp:26) */
+  int layer_id_base;      /* 0 */
+  uint64_t seed;          /* 0x5eed (QuantConfig::seed) */
+  double threshold_init;  /* 1.0 (QuantConfig::threshold_init) */
+  double r_min, r_max, alpha; /* 0.1, 0.3, 1.3 (ControllerConfig) */
+} fbq_mlp_config;
+
+void fbq_mlp_default_config(fbq_mlp_config* cfg);
+
+/* w_gate, w_up: d_ff x d_model; w_down: d_model x d_ff (host fp32, row-major,
+ * as QuantLinearLayer's weight, out x in).  Returns NULL on failure. */
+void* fbq_mlp_create(const fbq_mlp_config* cfg, const float* w_gate, const float* w_up,
+                     const float* w_down);
+void fbq_mlp_destroy(void* mlp);
+
+/* Device API (stream-ordered, no host synchronisation).  x, gy, y, gx are
+ * device buffers of `tokens` rows in act_dtype.  `row_offset` is the global
+ * row of this shard's row 0 (token sharding across ranks; 0 = whole batch). */
+int fbq_mlp_forward_device(void* mlp, const void* x, int64_t tokens, int64_t row_offset, int step,
+                           void* y, fbq_stream_t stream);
+int fbq_mlp_backward_device(void* mlp, const void* gy, int64_t tokens, int64_t row_offset,
+                            int step, void* gx, fbq_stream_t stream);
+/* controller_step of every layer (trainsim.cpp:129-133) from the last forward */
+int fbq_mlp_controller_step(void* mlp, fbq_stream_t stream);
+int fbq_mlp_zero_grad(void* mlp, fbq_stream_t stream);
+
+/* Host API: one fwd+bwd step over host fp32 buffers (synchronous, like the
+ * reference).  Pinned buffers make the copies asynchronous and overlapped. */
+int fbq_mlp_step_host(void* mlp, const float* x, const float* gy, int64_t tokens, int step,
+                      float* y, float* gx);
+
+/* Device pointers of the fp32 gradient accumulators (for the data-parallel
+ * all-reduce): which = 0 gate (d_ff x d_model), 1 up, 2 down (d_model x d_ff).
+ * gate and up are contiguous ([gate; up]). */
+void* fbq_mlp_grad_ptr(void* mlp, int which);
+/* Copy gradients / fallback statistics to the host (synchronises). */
+int fbq_mlp_get_grads(void* mlp, float* g_gate, float* g_up, float* g_down);
+/* rates[2] = last fallback rate of gate/up and down; thresholds[2] likewise */
+int fbq_mlp_get_controller(void* mlp, double* rates, double* thresholds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBQ_B200_HOST_H */

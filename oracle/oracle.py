@@ -369,3 +369,57 @@ def REF_oracle() -> Oracle | None:
     if _REF is None and os.path.exists(REF_SO):
         _REF = Oracle(REF_SO, "ref_")
     return _REF
+
+
+class RefMlp:
+    """The reference's own gate/up -> GluCombine -> down (QuantLinearLayer x 3,
+    trainsim.hpp:38-118) with 128 x 128 blocks, through oracle/_ref."""
+
+    def __init__(self, w_gate, w_up, w_down, threshold=1.0, g=128):
+        r = REF_oracle()
+        if r is None:
+            raise FileNotFoundError("oracle/_ref not built")
+        lib = r._l.lib
+        self.lib = lib
+        lib.ref_mlp_create.restype = C.c_void_p
+        lib.ref_mlp_create.argtypes = [F32, F32, F32, i64, i64, i64, dbl]
+        lib.ref_mlp_destroy.argtypes = [C.c_void_p]
+        lib.ref_mlp_step.argtypes = [C.c_void_p, F32, F32, i64, i64, cint, F32, F32]
+        lib.ref_mlp_grads.argtypes = [C.c_void_p, F32, F32, F32]
+        lib.ref_mlp_controller.argtypes = [C.c_void_p, F64, F64]
+        self.wg = np.ascontiguousarray(w_gate, np.float32)
+        self.wu = np.ascontiguousarray(w_up, np.float32)
+        self.wd = np.ascontiguousarray(w_down, np.float32)
+        self.d_ff, self.d_model = self.wg.shape
+        self.h = lib.ref_mlp_create(self.wg, self.wu, self.wd, self.d_model, self.d_ff, g, threshold)
+        if not self.h:
+            raise RuntimeError(r._err().decode())
+        self._err = r._err
+
+    def step(self, x, gy, step):
+        x = np.ascontiguousarray(x, np.float32)
+        gy = np.ascontiguousarray(gy, np.float32)
+        y = np.zeros_like(x)
+        gx = np.zeros_like(x)
+        rc = self.lib.ref_mlp_step(self.h, x, gy, x.shape[0], self.d_model, step, y, gx)
+        if rc:
+            raise RuntimeError(self._err().decode())
+        return y, gx
+
+    def grads(self):
+        gg = np.zeros((self.d_ff, self.d_model), np.float32)
+        gu = np.zeros_like(gg)
+        gd = np.zeros((self.d_model, self.d_ff), np.float32)
+        self.lib.ref_mlp_grads(self.h, gg, gu, gd)
+        return gg, gu, gd
+
+    def controller(self):
+        rates = np.zeros(3)
+        th = np.zeros(3)
+        self.lib.ref_mlp_controller(self.h, rates, th)
+        return rates, th
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_mlp_destroy(self.h)
+            self.h = None

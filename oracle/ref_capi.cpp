@@ -337,4 +337,27 @@ int ref_mlp_step(void* h, const float* x, const float* grad_out, int64_t tokens,
     });
 }
 
+int ref_mlp_grads(void* h, float* g_gate, float* g_up, float* g_down) {
+    return guarded([&] {
+        auto* m = static_cast<RefMlp*>(h);
+        std::memcpy(g_gate, m->gate->grad_weight().data(), m->gate->grad_weight().size() * 4);
+        std::memcpy(g_up, m->up->grad_weight().data(), m->up->grad_weight().size() * 4);
+        std::memcpy(g_down, m->down->grad_weight().data(), m->down->grad_weight().size() * 4);
+    });
+}
+
+// controller_step of every layer (trainsim.cpp:129-133); rates/thresholds of
+// gate, up, down after the update.
+int ref_mlp_controller(void* h, double* rates3, double* thresholds3) {
+    return guarded([&] {
+        auto* m = static_cast<RefMlp*>(h);
+        QuantLinearLayer* ls[3] = {m->gate.get(), m->up.get(), m->down.get()};
+        for (int i = 0; i < 3; ++i) {
+            rates3[i] = ls[i]->last_fallback_rate();
+            ls[i]->controller_step();
+            thresholds3[i] = ls[i]->threshold();
+        }
+    });
+}
+
 } // extern "C"

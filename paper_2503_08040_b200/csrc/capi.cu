@@ -54,19 +54,20 @@ const char* fbq_status_string(int s) {
   }
 }
 
-int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
-                               int mask_mode, double theta, uint32_t* mask_bits, int8_t* codes,
-                               int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
-                               int32_t* masked_count, float* amax_out, int8_t* sr_codes,
-                               uint64_t sr_seed, int64_t sr_row_offset, fbq_stream_t stream) {
-  if (int st = check_x(x, dtype, rows, cols, ldx)) return st;
+static int fill_quant_params(fbq::QuantParams& p, const void* x, int64_t rows, int64_t cols,
+                             int64_t ldx, int mask_mode, double theta, uint32_t* mask_bits,
+                             int8_t* codes, int64_t ldq, float* scales, int8_t* res_codes,
+                             float* res_scales, int32_t* masked_count, float* amax_out,
+                             int8_t* sr_codes, uint64_t sr_seed, int8_t* sr_codes2,
+                             uint64_t sr_seed2, int64_t sr_row_offset, cudaStream_t s,
+                             const double* theta_dev = nullptr) {
   if (mask_mode < FBQ_MASK_NONE || mask_mode > FBQ_MASK_GIVEN) return FBQ_ERR_ARG;
   if (mask_mode != FBQ_MASK_NONE && mask_bits == nullptr) return FBQ_ERR_ARG;
-  if (mask_mode == FBQ_MASK_THRESHOLD && !(theta > 0.0)) return FBQ_ERR_ARG;  // policy.cpp:74
+  if (mask_mode == FBQ_MASK_THRESHOLD && !theta_dev && !(theta > 0.0))
+    return FBQ_ERR_ARG;  // policy.cpp:74
   if ((res_codes == nullptr) != (res_scales == nullptr)) return FBQ_ERR_ARG;
-  if ((codes || res_codes || sr_codes) && ldq < cols) return FBQ_ERR_ARG;
+  if ((codes || res_codes || sr_codes || sr_codes2) && ldq < cols) return FBQ_ERR_ARG;
   if (sr_row_offset < 0) return FBQ_ERR_ARG;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t grid = cdiv(rows, 128) * cdiv(cols, 128);
   if (mask_mode == FBQ_MASK_THRESHOLD && grid > 0) {
     if (int st = cuda_status(cudaMemsetAsync(mask_bits, 0, (size_t)cdiv(grid, 32) * 4, s)))
@@ -75,8 +76,7 @@ int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t c
   if (masked_count) {
     if (int st = cuda_status(cudaMemsetAsync(masked_count, 0, sizeof(int32_t), s))) return st;
   }
-  if (grid == 0) return FBQ_OK;
-  fbq::QuantParams p{};
+  p = fbq::QuantParams{};
   p.x = x;
   p.rows = rows;
   p.cols = cols;
@@ -84,6 +84,7 @@ int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t c
   p.ldq = ldq;
   p.mask_mode = mask_mode;
   p.theta = theta;
+  p.theta_dev = theta_dev;
   p.mask_bits = mask_bits;
   p.codes = codes;
   p.scales = scales;
@@ -93,7 +94,97 @@ int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t c
   p.amax_out = amax_out;
   p.sr_codes = sr_codes;
   p.sr_seed = sr_seed;
+  p.sr_codes2 = sr_codes2;
+  p.sr_seed2 = sr_seed2;
   p.row_offset = sr_row_offset;
+  return FBQ_OK;
+}
+
+int fbq_cuda_quantize_linear_input(const void* x, int dtype, int64_t rows, int64_t cols,
+                                   int64_t ldx, int mask_mode, double theta,
+                                   const double* theta_dev, uint32_t* mask_bits,
+                                   int8_t* codes, int64_t ldq, float* scales, int8_t* res_codes,
+                                   float* res_scales, int32_t* masked_count, int8_t* ctx_codes,
+                                   uint64_t ctx_seed, int8_t* ctx_codes2, uint64_t ctx_seed2,
+                                   int64_t row_offset, fbq_stream_t stream) {
+  if (int st = check_x(x, dtype, rows, cols, ldx)) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  fbq::QuantParams p;
+  if (int st = fill_quant_params(p, x, rows, cols, ldx, mask_mode, theta, mask_bits, codes, ldq,
+                                 scales, res_codes, res_scales, masked_count, nullptr, ctx_codes,
+                                 ctx_seed, ctx_codes2, ctx_seed2, row_offset, s, theta_dev))
+    return st;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  return cuda_status(fbq::launch_quantize(p, dtype == FBQ_BF16, s));
+}
+
+int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, int64_t ld_ab,
+                         int16_t* ctx_a, int16_t* ctx_b, int64_t ld_ctx, float* ctx_a_scales,
+                         float* ctx_b_scales, int ctx_bits, double theta,
+                         const double* theta_dev, uint32_t* mask_bits,
+                         int8_t* codes, int64_t ldq, float* scales, int8_t* res_codes,
+                         float* res_scales, int32_t* masked_count, int8_t* ctx_codes,
+                         uint64_t ctx_seed, int64_t row_offset, float* h_out, int64_t ld_h,
+                         fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  const size_t esz = dtype == FBQ_F32 ? 4 : 2;
+  if (!ab || ld_ab < 2 * cols || (h_out && ld_h < cols)) return FBQ_ERR_ARG;
+  if ((ctx_a || ctx_b) && ld_ctx < cols) return FBQ_ERR_ARG;
+  if (ctx_bits < 2 || ctx_bits > 16) return FBQ_ERR_ARG;
+  // vectorised 16-byte loads of a and b, 16-byte context stores
+  if (cols % 8 || (ld_ab * esz) % 16 || !aligned16(ab) || (cols * esz) % 16 ||
+      ((ctx_a || ctx_b) && (ld_ctx % 8 || (ctx_a && !aligned16(ctx_a)) || (ctx_b && !aligned16(ctx_b)))))
+    return FBQ_ERR_UNSUPPORTED;
+  if (cdiv(rows, 128) > 65535) return FBQ_ERR_UNSUPPORTED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  fbq::QuantParams p;
+  if (int st = fill_quant_params(p, nullptr, rows, cols, cols, FBQ_MASK_THRESHOLD, theta,
+                                 mask_bits, codes, ldq, scales, res_codes, res_scales,
+                                 masked_count, nullptr, ctx_codes, ctx_seed, nullptr, 0,
+                                 row_offset, s, theta_dev))
+    return st;
+  if (ldq % 16) return FBQ_ERR_UNSUPPORTED;
+  fbq::GluParams g{ab, rows, cols, ld_ab, ctx_a, ctx_b, ld_ctx, ctx_a_scales, ctx_b_scales,
+                   (float)((1 << (ctx_bits - 1)) - 1), h_out, ld_h};
+  return cuda_status(fbq::launch_glu_forward(g, p, dtype == FBQ_BF16, s));
+}
+
+int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols, int64_t ld_gh,
+                          const int16_t* ctx_a, const int16_t* ctx_b, int64_t ld_ctx,
+                          const float* ctx_a_scales, const float* ctx_b_scales, int8_t* gq,
+                          int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
+                          int64_t row_offset, float* g_out, fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  const size_t esz = dtype == FBQ_F32 ? 4 : 2;
+  if (!gh || !ctx_a || !ctx_b || !ctx_a_scales || !ctx_b_scales || !gq || !gq_scales)
+    return FBQ_ERR_ARG;
+  if (ld_gh < cols || ld_ctx < cols || ldq < 2 * cols || row_offset < 0) return FBQ_ERR_ARG;
+  if (cols % 8 || (ld_gh * esz) % 16 || !aligned16(gh) || ldq % 16 || cols % 16)
+    return FBQ_ERR_UNSUPPORTED;
+  if (cdiv(rows, 128) > 65535) return FBQ_ERR_UNSUPPORTED;
+  fbq::GluBwdParams g{gh,    rows,   cols,   ld_gh,      ctx_a,     ctx_b,    ld_ctx,
+                      ctx_a_scales, ctx_b_scales, gq, ldq, gq_scales, seed_a, seed_b,
+                      row_offset, g_out};
+  return cuda_status(fbq::launch_glu_backward(g, dtype == FBQ_BF16, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                               int mask_mode, double theta, uint32_t* mask_bits, int8_t* codes,
+                               int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
+                               int32_t* masked_count, float* amax_out, int8_t* sr_codes,
+                               uint64_t sr_seed, int64_t sr_row_offset, fbq_stream_t stream) {
+  if (int st = check_x(x, dtype, rows, cols, ldx)) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  fbq::QuantParams p;
+  if (int st = fill_quant_params(p, x, rows, cols, ldx, mask_mode, theta, mask_bits, codes, ldq,
+                                 scales, res_codes, res_scales, masked_count, amax_out, sr_codes,
+                                 sr_seed, nullptr, 0, sr_row_offset, s))
+    return st;
+  if (rows == 0 || cols == 0) return FBQ_OK;
   return cuda_status(fbq::launch_quantize(p, dtype == FBQ_BF16, s));
 }
 
@@ -122,8 +213,9 @@ int fbq_cuda_quantize_stochastic(const void* x, int dtype, int64_t rows, int64_t
                                     codes, seed, row_offset, stream);
 }
 
-static int gemm_common(const int8_t* a_codes, int64_t lda, const float* a_scales, int a_major,
-                       const int8_t* b_codes, int64_t ldb, const float* b_scales, int b_major,
+static int gemm_common(const int8_t* a_codes, int64_t lda, const float* a_scales,
+                       int64_t lds_a, int a_major, const int8_t* b_codes, int64_t ldb,
+                       const float* b_scales, int64_t lds_b, int b_major,
                        const uint32_t* mask_bits, const int8_t* res_codes,
                        const float* res_scales, int64_t M, int64_t N, int64_t K, void* out,
                        int out_dtype, int64_t ldo, int accumulate, int epi, int32_t* dump,
@@ -156,6 +248,13 @@ static int gemm_common(const int8_t* a_codes, int64_t lda, const float* a_scales
   p.KB = (int)cdiv(K, 128);
   p.a_major = a_major;
   p.b_major = b_major;
+  // natural grid strides unless given: K-major stored grids are [.][KB], MN-major [KB][.]
+  const int64_t nat_a = a_major == 0 ? p.KB : p.MB;
+  const int64_t nat_b = b_major == 0 ? p.KB : p.NB;
+  if ((lds_a && lds_a < nat_a) || (lds_b && lds_b < nat_b)) return FBQ_ERR_SHAPE;
+  if (mask_bits && lds_a && lds_a != nat_a) return FBQ_ERR_UNSUPPORTED;  // mask = natural A grid
+  p.lds_a = lds_a ? lds_a : nat_a;
+  p.lds_b = lds_b ? lds_b : nat_b;
   p.a_scales = a_scales;
   p.b_scales = b_scales;
   p.mask_bits = mask_bits;
@@ -179,9 +278,22 @@ int fbq_cuda_gemm(const int8_t* a_codes, int64_t lda, const float* a_scales, int
                   int64_t M, int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo,
                   int accumulate, int epilogue, fbq_stream_t stream) {
   if (epilogue != FBQ_EPI_EXACT && epilogue != FBQ_EPI_FMA) return FBQ_ERR_ARG;
-  return gemm_common(a_codes, lda, a_scales, a_major, b_codes, ldb, b_scales, b_major, mask_bits,
-                     res_codes, res_scales, M, N, K, out, out_dtype, ldo, accumulate, epilogue,
-                     nullptr, reinterpret_cast<cudaStream_t>(stream));
+  return gemm_common(a_codes, lda, a_scales, 0, a_major, b_codes, ldb, b_scales, 0, b_major,
+                     mask_bits, res_codes, res_scales, M, N, K, out, out_dtype, ldo, accumulate,
+                     epilogue, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fbq_cuda_gemm_ex(const int8_t* a_codes, int64_t lda, const float* a_scales, int64_t lds_a,
+                     int a_major, const int8_t* b_codes, int64_t ldb, const float* b_scales,
+                     int64_t lds_b, int b_major, const uint32_t* mask_bits,
+                     const int8_t* res_codes, const float* res_scales, int64_t M, int64_t N,
+                     int64_t K, void* out, int out_dtype, int64_t ldo, int accumulate,
+                     int epilogue, fbq_stream_t stream) {
+  if (epilogue != FBQ_EPI_EXACT && epilogue != FBQ_EPI_FMA) return FBQ_ERR_ARG;
+  if (lds_a < 0 || lds_b < 0) return FBQ_ERR_ARG;
+  return gemm_common(a_codes, lda, a_scales, lds_a, a_major, b_codes, ldb, b_scales, lds_b,
+                     b_major, mask_bits, res_codes, res_scales, M, N, K, out, out_dtype, ldo,
+                     accumulate, epilogue, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int fbq_cuda_gemm_block_products(const int8_t* a_codes, int64_t lda, int a_major,
@@ -189,9 +301,19 @@ int fbq_cuda_gemm_block_products(const int8_t* a_codes, int64_t lda, int a_major
                                  const uint32_t* mask_bits, const int8_t* res_codes, int64_t M,
                                  int64_t N, int64_t K, int32_t* out, fbq_stream_t stream) {
   if (out == nullptr) return FBQ_ERR_ARG;
-  return gemm_common(a_codes, lda, nullptr, a_major, b_codes, ldb, nullptr, b_major, mask_bits,
-                     res_codes, nullptr, M, N, K, nullptr, FBQ_F32, 0, 0, FBQ_EPI_EXACT, out,
-                     reinterpret_cast<cudaStream_t>(stream));
+  return gemm_common(a_codes, lda, nullptr, 0, a_major, b_codes, ldb, nullptr, 0, b_major,
+                     mask_bits, res_codes, nullptr, M, N, K, nullptr, FBQ_F32, 0, 0,
+                     FBQ_EPI_EXACT, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fbq_cuda_controller_update(double* theta_dev, const int32_t* masked_count, int64_t n_blocks,
+                               double r_min, double r_max, double alpha, double* last_rate_dev,
+                               fbq_stream_t stream) {
+  if (!theta_dev || !masked_count || n_blocks < 0) return FBQ_ERR_ARG;
+  if (!(0.0 <= r_min && r_min < r_max && r_max <= 1.0) || !(alpha > 1.0)) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_controller(theta_dev, masked_count, n_blocks, r_min, r_max,
+                                            alpha, last_rate_dev,
+                                            reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,

@@ -32,8 +32,9 @@ __device__ __forceinline__ float block_scale(float amax) {
   return amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
 }
 
-// clamp(round_half_even(x / a), -127, 127); a > 0.   kernels.cpp:24-40
-__device__ __forceinline__ int rtn_code(float x, float a, float inv_a) {
+// clamp(round_half_even(x / a), -L, L); a > 0.   kernels.cpp:24-40
+// (L = 127 for the 8-bit GEMM operands, 511 for the 10-bit non-linear contexts)
+__device__ __forceinline__ int rtn_code(float x, float a, float inv_a, float level = 127.0f) {
   float n;
   if (a >= kTinyScale) {
     n = rintf(__fmul_rn(x, inv_a));
@@ -49,7 +50,7 @@ __device__ __forceinline__ int rtn_code(float x, float a, float inv_a) {
   } else {
     n = (float)rint(__ddiv_rn((double)x, (double)a));
   }
-  n = fminf(fmaxf(n, -127.0f), 127.0f);
+  n = fminf(fmaxf(n, -level), level);
   return (int)n;
 }
 

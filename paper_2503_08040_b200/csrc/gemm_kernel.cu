@@ -130,11 +130,12 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // scale-grid indices of the stored operands (row stride lds_a / lds_b)
   auto a_blk = [&](int bm, int bk) -> int64_t {
-    return p.a_major == 0 ? (int64_t)bm * p.KB + bk : (int64_t)bk * p.MB + bm;
+    return p.a_major == 0 ? (int64_t)bm * p.lds_a + bk : (int64_t)bk * p.lds_a + bm;
   };
   auto b_blk = [&](int bk, int bn) -> int64_t {
-    return p.b_major == 0 ? (int64_t)bn * p.KB + bk : (int64_t)bk * p.NB + bn;
+    return p.b_major == 0 ? (int64_t)bn * p.lds_b + bk : (int64_t)bk * p.lds_b + bn;
   };
 
   if (warp < 4) setmaxnreg_dec<56>();

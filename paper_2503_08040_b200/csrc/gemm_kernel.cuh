@@ -18,6 +18,7 @@ struct GemmParams {
   int64_t M, N, K;
   int MB, NB, KB;  // ceil(M/128), ceil(N/128), ceil(K/128)
   int a_major, b_major;  // 0 = K-major, 1 = MN-major
+  int64_t lds_a, lds_b;  // row strides of the stored scale grids (elements)
   const float* a_scales;
   const float* b_scales;
   const uint32_t* mask_bits;  // over A's stored block grid; null = block_quant_gemm

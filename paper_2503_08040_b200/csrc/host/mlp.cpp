@@ -1,0 +1,436 @@
+// Fallback-quantized SwiGLU MLP driver (include/fbq_b200_host.h).
+//
+// Mirrors the reference composition of QuantLinearLayer (trainsim.cpp:61-127)
+// and GluCombine (trainsim.cpp:224-263) for gate/up/down, re-planned for B200:
+//   forward   RTN(W_gu), RTN(W_d)                         2 x K1
+//             K1(X): fallback codes + 2 SR contexts       1 read of X
+//             [a|b] = fallback_gemm(X, W_gu^T)            K3, one GEMM for gate+up
+//             GLU fwd fused with K1(h)                    h never materialised
+//             y = fallback_gemm(h, W_d^T)                 K3
+//   backward  K2(dY) -> dH = bqg(dY, W_d) ; dW_d += bqg(dY^T, ctx_h)
+//             GLU bwd fused with K2(ga), K2(gb)
+//             dX = bqg(ga, W_g) + bqg(gb, W_u)            (accumulate = the reference's add)
+//             dW_g += bqg(ga^T, ctx_g) ; dW_u += bqg(gb^T, ctx_u)
+// Every operand is consumed in the layout it was produced in: the backward
+// GEMMs read the forward code planes MN-major instead of transposing them.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "../../../include/fbq_b200_host.h"
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  int status;
+  CudaError(int st, const std::string& w) : std::runtime_error(w), status(st) {}
+};
+
+#define FBQ_TRY(expr)                                                     \
+  do {                                                                    \
+    int _st = (expr);                                                     \
+    if (_st != FBQ_OK) throw CudaError(_st, #expr);                       \
+  } while (0)
+#define CU_TRY(expr)                                                      \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) throw CudaError(FBQ_ERR_CUDA, cudaGetErrorString(_e)); \
+  } while (0)
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t ld16(int64_t n) { return (n + 15) / 16 * 16; }
+
+// rng.hpp:11-58 / trainsim.cpp:16-19
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t bits_at(uint64_t seed, uint64_t n) { return mix64(seed + (n + 1) * 0x9E3779B97F4A7C15ull); }
+uint64_t layer_seed(uint64_t base, int layer, uint64_t tag, int step) {
+  return bits_at(bits_at(base, (uint64_t)layer * 4 + tag), (uint64_t)step);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) {
+    if (bytes) CU_TRY(cudaMalloc(&p, bytes));
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    return *this;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+size_t esize(int dt) { return dt == FBQ_F32 ? 4 : 2; }
+
+struct Mlp {
+  fbq_mlp_config c;
+  int64_t D, F, T;            // d_model, d_ff, max tokens
+  int64_t ldD, ldF, ldF2;     // int8 plane strides
+  int64_t gD, gF, gT;         // grid extents (blocks)
+  // weights (fp32 master) and gradients
+  DevBuf w_gu, w_d, g_gu, g_d;
+  // quantized weights
+  DevBuf wgu_codes, wgu_scales, wd_codes, wd_scales;
+  // forward X quantization
+  DevBuf x_codes, x_scales, x_res, x_res_scales, x_mask, ctx_g, ctx_u;
+  // [a|b], GLU contexts, h quantization
+  DevBuf ab, ctx_a, ctx_b, ctx_a_s, ctx_b_s, h_codes, h_scales, h_res, h_res_scales, h_mask, ctx_h;
+  // backward
+  DevBuf gy_codes, gy_scales, gh, gq, gq_scales;
+  // controller state on device: theta[2], count[2], rate[2]
+  DevBuf theta, counts, rates;
+  // host e2e staging
+  DevBuf hx, hgy, hy, hgx;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_gy = nullptr, ev_fwd = nullptr, ev_bwd = nullptr;
+
+  Mlp(const fbq_mlp_config& cfg, const float* wg, const float* wu, const float* wd) : c(cfg) {
+    D = c.d_model;
+    F = c.d_ff;
+    T = c.max_tokens;
+    if (D <= 0 || F <= 0 || T <= 0) throw CudaError(FBQ_ERR_SHAPE, "bad MLP shape");
+    // d_ff % 128: the concatenated [gate; up] planes must not share a block
+    if (D % 16 || F % 128) throw CudaError(FBQ_ERR_UNSUPPORTED, "need d_model % 16 == 0 and d_ff % 128 == 0");
+    ldD = ld16(D);
+    ldF = ld16(F);
+    ldF2 = ld16(2 * F);
+    gD = cdiv(D, 128);
+    gF = cdiv(F, 128);
+    gT = cdiv(T, 128);
+    const size_t f4 = 4;
+    w_gu = DevBuf(2 * F * D * f4);
+    w_d = DevBuf(D * F * f4);
+    g_gu = DevBuf(2 * F * D * f4);
+    g_d = DevBuf(D * F * f4);
+    CU_TRY(cudaMemcpy(w_gu.p, wg, F * D * f4, cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemcpy(w_gu.as<float>() + F * D, wu, F * D * f4, cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemcpy(w_d.p, wd, D * F * f4, cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemset(g_gu.p, 0, 2 * F * D * f4));
+    CU_TRY(cudaMemset(g_d.p, 0, D * F * f4));
+    wgu_codes = DevBuf(2 * F * ldD);
+    wgu_scales = DevBuf(cdiv(2 * F, 128) * gD * f4);
+    wd_codes = DevBuf(D * ldF);
+    wd_scales = DevBuf(gD * gF * f4);
+    x_codes = DevBuf(T * ldD);
+    x_res = DevBuf(T * ldD);
+    ctx_g = DevBuf(T * ldD);
+    ctx_u = DevBuf(T * ldD);
+    x_scales = DevBuf(gT * gD * f4);
+    x_res_scales = DevBuf(gT * gD * f4);
+    x_mask = DevBuf(cdiv(gT * gD, 32) * 4);
+    ab = DevBuf(T * 2 * F * esize(c.mid_dtype));
+    ctx_a = DevBuf(T * ldF * 2);
+    ctx_b = DevBuf(T * ldF * 2);
+    ctx_a_s = DevBuf(T * gF * f4);
+    ctx_b_s = DevBuf(T * gF * f4);
+    h_codes = DevBuf(T * ldF);
+    h_res = DevBuf(T * ldF);
+    ctx_h = DevBuf(T * ldF);
+    h_scales = DevBuf(gT * gF * f4);
+    h_res_scales = DevBuf(gT * gF * f4);
+    h_mask = DevBuf(cdiv(gT * gF, 32) * 4);
+    gy_codes = DevBuf(T * ldD);
+    gy_scales = DevBuf(gT * gD * f4);
+    gh = DevBuf(T * F * esize(c.mid_dtype));
+    gq = DevBuf(T * ldF2);
+    gq_scales = DevBuf(gT * 2 * gF * f4);
+    theta = DevBuf(2 * sizeof(double));
+    counts = DevBuf(2 * sizeof(int32_t));
+    rates = DevBuf(2 * sizeof(double));
+    const double th[2] = {c.threshold_init, c.threshold_init};
+    CU_TRY(cudaMemcpy(theta.p, th, sizeof(th), cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemset(counts.p, 0, 2 * sizeof(int32_t)));
+    CU_TRY(cudaMemset(rates.p, 0, 2 * sizeof(double)));
+    CU_TRY(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    CU_TRY(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
+    CU_TRY(cudaEventCreateWithFlags(&ev_gy, cudaEventDisableTiming));
+    CU_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
+    CU_TRY(cudaEventCreateWithFlags(&ev_bwd, cudaEventDisableTiming));
+  }
+
+  ~Mlp() {
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd})
+      if (e) cudaEventDestroy(e);
+  }
+
+  int layer(int i) const { return c.layer_id_base + i; }  // 0 gate, 1 up, 2 down
+
+  void forward(const void* x, int64_t tok, int64_t row_off, int step, void* y, cudaStream_t s) {
+    if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
+    if (tok == 0) return;
+    const int64_t gTt = cdiv(tok, 128);
+    int32_t* cnt = counts.as<int32_t>();
+    double* th = theta.as<double>();
+    // weights: one RTN quantization serves forward (K-major) and dgrad (MN-major);
+    // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97, 121)
+    FBQ_TRY(fbq_cuda_quantize_rtn(w_gu.p, FBQ_F32, 2 * F, D, D, wgu_codes.as<int8_t>(), ldD,
+                                  wgu_scales.as<float>(), s));
+    FBQ_TRY(fbq_cuda_quantize_rtn(w_d.p, FBQ_F32, D, F, F, wd_codes.as<int8_t>(), ldF,
+                                  wd_scales.as<float>(), s));
+    // X: score + threshold mask + fallback codes + gate/up contexts (trainsim.cpp:80-102)
+    FBQ_TRY(fbq_cuda_quantize_linear_input(
+        x, c.act_dtype, tok, D, D, FBQ_MASK_THRESHOLD, c.threshold_init, th,
+        x_mask.as<uint32_t>(), x_codes.as<int8_t>(), ldD, x_scales.as<float>(),
+        x_res.as<int8_t>(), x_res_scales.as<float>(), cnt, ctx_g.as<int8_t>(),
+        layer_seed(c.seed, layer(0), 0, step), ctx_u.as<int8_t>(),
+        layer_seed(c.seed, layer(1), 0, step), row_off, s));
+    // [a | b] = fallback_gemm(X, [W_g; W_u]^T)
+    FBQ_TRY(fbq_cuda_gemm(x_codes.as<int8_t>(), ldD, x_scales.as<float>(), FBQ_K_MAJOR,
+                          wgu_codes.as<int8_t>(), ldD, wgu_scales.as<float>(), FBQ_K_MAJOR,
+                          x_mask.as<uint32_t>(), x_res.as<int8_t>(), x_res_scales.as<float>(),
+                          tok, 2 * F, D, ab.p, c.mid_dtype, 2 * F, 0, c.epilogue, s));
+    // GLU + contexts + quantization of h for the down projection
+    FBQ_TRY(fbq_cuda_glu_forward(
+        ab.p, c.mid_dtype, tok, F, 2 * F, ctx_a.as<int16_t>(), ctx_b.as<int16_t>(), ldF,
+        ctx_a_s.as<float>(), ctx_b_s.as<float>(), c.nonlinear_bits, c.threshold_init, th + 1,
+        h_mask.as<uint32_t>(), h_codes.as<int8_t>(), ldF, h_scales.as<float>(),
+        h_res.as<int8_t>(), h_res_scales.as<float>(), cnt + 1, ctx_h.as<int8_t>(),
+        layer_seed(c.seed, layer(2), 0, step), row_off, nullptr, 0, s));
+    // y = fallback_gemm(h, W_d^T)
+    FBQ_TRY(fbq_cuda_gemm(h_codes.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_K_MAJOR,
+                          wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_K_MAJOR,
+                          h_mask.as<uint32_t>(), h_res.as<int8_t>(), h_res_scales.as<float>(),
+                          tok, D, F, y, c.act_dtype, D, 0, c.epilogue, s));
+    (void)gTt;
+  }
+
+  void backward(const void* gy, int64_t tok, int64_t row_off, int step, void* gx,
+                cudaStream_t s) {
+    if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
+    if (tok == 0) return;
+    // down: SR(dY) (trainsim.cpp:117-119)
+    FBQ_TRY(fbq_cuda_quantize_stochastic(gy, c.act_dtype, tok, D, D,
+                                         layer_seed(c.seed, layer(2), 1, step), row_off,
+                                         gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), s));
+    // dH = bqg(dY, W_d): B = W_d codes (D x F) read MN-major (trainsim.cpp:121-122)
+    FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_K_MAJOR,
+                          wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_MN_MAJOR,
+                          nullptr, nullptr, nullptr, tok, F, D, gh.p, c.mid_dtype, F, 0,
+                          c.epilogue, s));
+    // dW_d += bqg(dY^T, ctx_h) (trainsim.cpp:124-125)
+    FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_MN_MAJOR,
+                          ctx_h.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
+                          nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, 1, c.epilogue, s));
+    // GLU backward fused with SR(ga), SR(gb)
+    FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.as<int16_t>(),
+                                  ctx_b.as<int16_t>(), ldF, ctx_a_s.as<float>(),
+                                  ctx_b_s.as<float>(), gq.as<int8_t>(), ldF2,
+                                  gq_scales.as<float>(), layer_seed(c.seed, layer(0), 1, step),
+                                  layer_seed(c.seed, layer(1), 1, step), row_off, nullptr, s));
+    // dX = bqg(ga, W_g) + bqg(gb, W_u)   (the reference adds the two layers' dX)
+    const int64_t lds_gq = 2 * gF;
+    int8_t* gqc = gq.as<int8_t>();
+    float* gqs = gq_scales.as<float>();
+    FBQ_TRY(fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_K_MAJOR, wgu_codes.as<int8_t>(), ldD,
+                             wgu_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr,
+                             tok, D, F, gx, c.act_dtype, D, 0,
+                             c.epilogue, s));
+    FBQ_TRY(fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_K_MAJOR,
+                             wgu_codes.as<int8_t>() + F * ldD, ldD,
+                             wgu_scales.as<float>() + gF * gD, gD, FBQ_MN_MAJOR, nullptr, nullptr,
+                             nullptr, tok, D, F, gx, c.act_dtype, D, 1, c.epilogue, s));
+    // dW_g += bqg(ga^T, ctx_g) ; dW_u += bqg(gb^T, ctx_u)
+    FBQ_TRY(fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_MN_MAJOR, ctx_g.as<int8_t>(), ldD,
+                             x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr, F,
+                             D, tok, g_gu.p, FBQ_F32, D, 1, c.epilogue, s));
+    FBQ_TRY(fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_MN_MAJOR, ctx_u.as<int8_t>(),
+                             ldD, x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr,
+                             nullptr, F, D, tok, g_gu.as<float>() + F * D, FBQ_F32, D, 1,
+                             c.epilogue, s));
+  }
+
+  void controller(cudaStream_t s) {
+    // observed rate = masked blocks / blocks of the last forward (policy.cpp:82-87)
+    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), counts.as<int32_t>(), last_blocks[0],
+                                       c.r_min, c.r_max, c.alpha, rates.as<double>(), s));
+    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>() + 1, counts.as<int32_t>() + 1,
+                                       last_blocks[1], c.r_min, c.r_max, c.alpha,
+                                       rates.as<double>() + 1, s));
+  }
+  int64_t last_blocks[2] = {1, 1};
+
+  void step_host(const float* x, const float* gy, int64_t tok, int step, float* y, float* gx) {
+    if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
+    if (!hx.p) {
+      hx = DevBuf(T * D * 4);
+      hgy = DevBuf(T * D * 4);
+      hy = DevBuf(T * D * 4);
+      hgx = DevBuf(T * D * 4);
+    }
+    if (tok == 0) return;
+    const size_t bytes = tok * D * 4;
+    cudaStream_t s = nullptr;  // legacy default stream for compute
+    CU_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct Guard { cudaStream_t s; ~Guard() { cudaStreamDestroy(s); } } guard{s};
+    CU_TRY(cudaMemcpyAsync(hx.p, x, bytes, cudaMemcpyHostToDevice, s));
+    CU_TRY(cudaMemcpyAsync(hgy.p, gy, bytes, cudaMemcpyHostToDevice, copy_stream));
+    CU_TRY(cudaEventRecord(ev_gy, copy_stream));
+    const int saved = c.act_dtype;
+    c.act_dtype = FBQ_F32;  // the host API is fp32 like the reference
+    try {
+      forward(hx.p, tok, 0, step, hy.p, s);
+      CU_TRY(cudaEventRecord(ev_fwd, s));
+      CU_TRY(cudaStreamWaitEvent(copy_stream, ev_fwd, 0));
+      CU_TRY(cudaMemcpyAsync(y, hy.p, bytes, cudaMemcpyDeviceToHost, copy_stream));
+      CU_TRY(cudaStreamWaitEvent(s, ev_gy, 0));
+      backward(hgy.p, tok, 0, step, hgx.p, s);
+      CU_TRY(cudaMemcpyAsync(gx, hgx.p, bytes, cudaMemcpyDeviceToHost, s));
+    } catch (...) {
+      c.act_dtype = saved;
+      throw;
+    }
+    c.act_dtype = saved;
+    CU_TRY(cudaStreamSynchronize(s));
+    CU_TRY(cudaStreamSynchronize(copy_stream));
+  }
+};
+
+thread_local std::string g_host_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FBQ_OK;
+  } catch (const CudaError& e) {
+    g_host_err = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return FBQ_ERR_ARG;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fbq_host_last_error(void) { return g_host_err.c_str(); }
+
+void fbq_mlp_default_config(fbq_mlp_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->act_dtype = FBQ_BF16;
+  c->mid_dtype = FBQ_BF16;
+  c->epilogue = FBQ_EPI_FMA;
+  c->nonlinear_bits = 10;
+  c->layer_id_base = 0;
+  c->seed = 0x5eedull;
+  c->threshold_init = 1.0;
+  c->r_min = 0.1;
+  c->r_max = 0.3;
+  c->alpha = 1.3;
+}
+
+void* fbq_mlp_create(const fbq_mlp_config* cfg, const float* w_gate, const float* w_up,
+                     const float* w_down) {
+  if (!cfg || !w_gate || !w_up || !w_down) return nullptr;
+  try {
+    return new Mlp(*cfg, w_gate, w_up, w_down);
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return nullptr;
+  }
+}
+
+void fbq_mlp_destroy(void* m) { delete static_cast<Mlp*>(m); }
+
+int fbq_mlp_forward_device(void* m, const void* x, int64_t tokens, int64_t row_offset, int step,
+                           void* y, fbq_stream_t stream) {
+  if (!m || (tokens > 0 && (!x || !y))) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    mlp->forward(x, tokens, row_offset, step, y, reinterpret_cast<cudaStream_t>(stream));
+    mlp->last_blocks[0] = cdiv(tokens, 128) * mlp->gD;
+    mlp->last_blocks[1] = cdiv(tokens, 128) * mlp->gF;
+  });
+}
+
+int fbq_mlp_backward_device(void* m, const void* gy, int64_t tokens, int64_t row_offset, int step,
+                            void* gx, fbq_stream_t stream) {
+  if (!m || (tokens > 0 && (!gy || !gx))) return FBQ_ERR_ARG;
+  return guarded([&] {
+    static_cast<Mlp*>(m)->backward(gy, tokens, row_offset, step, gx,
+                                   reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int fbq_mlp_controller_step(void* m, fbq_stream_t stream) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<Mlp*>(m)->controller(reinterpret_cast<cudaStream_t>(stream)); });
+}
+
+int fbq_mlp_zero_grad(void* m, fbq_stream_t stream) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    CU_TRY(cudaMemsetAsync(mlp->g_gu.p, 0, 2 * mlp->F * mlp->D * 4, s));
+    CU_TRY(cudaMemsetAsync(mlp->g_d.p, 0, mlp->D * mlp->F * 4, s));
+  });
+}
+
+int fbq_mlp_step_host(void* m, const float* x, const float* gy, int64_t tokens, int step,
+                      float* y, float* gx) {
+  if (!m || (tokens > 0 && (!x || !gy || !y || !gx))) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    mlp->step_host(x, gy, tokens, step, y, gx);
+    mlp->last_blocks[0] = cdiv(tokens, 128) * mlp->gD;
+    mlp->last_blocks[1] = cdiv(tokens, 128) * mlp->gF;
+  });
+}
+
+void* fbq_mlp_grad_ptr(void* m, int which) {
+  if (!m) return nullptr;
+  auto* mlp = static_cast<Mlp*>(m);
+  if (which == 0) return mlp->g_gu.p;
+  if (which == 1) return mlp->g_gu.as<float>() + mlp->F * mlp->D;
+  if (which == 2) return mlp->g_d.p;
+  return nullptr;
+}
+
+int fbq_mlp_get_grads(void* m, float* g_gate, float* g_up, float* g_down) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    CU_TRY(cudaDeviceSynchronize());
+    const size_t n = mlp->F * mlp->D * 4;
+    if (g_gate) CU_TRY(cudaMemcpy(g_gate, mlp->g_gu.p, n, cudaMemcpyDeviceToHost));
+    if (g_up) CU_TRY(cudaMemcpy(g_up, mlp->g_gu.as<float>() + mlp->F * mlp->D, n, cudaMemcpyDeviceToHost));
+    if (g_down) CU_TRY(cudaMemcpy(g_down, mlp->g_d.p, n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int fbq_mlp_get_controller(void* m, double* rates, double* thresholds) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    CU_TRY(cudaDeviceSynchronize());
+    if (thresholds) CU_TRY(cudaMemcpy(thresholds, mlp->theta.p, 16, cudaMemcpyDeviceToHost));
+    if (rates) {
+      // last observed rate of the most recent forward (masked / blocks)
+      int32_t cnt[2];
+      CU_TRY(cudaMemcpy(cnt, mlp->counts.p, 8, cudaMemcpyDeviceToHost));
+      rates[0] = (double)cnt[0] / (double)mlp->last_blocks[0];
+      rates[1] = (double)cnt[1] / (double)mlp->last_blocks[1];
+    }
+  });
+}
+
+}  // extern "C"

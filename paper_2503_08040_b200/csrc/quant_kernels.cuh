@@ -13,6 +13,7 @@ struct QuantParams {
   int64_t ldq;         // leading dim of every int8 code plane
   int mask_mode;
   double theta;
+  const double* theta_dev;  // if non-null, the threshold is read on device (controller state)
   uint32_t* mask_bits;     // in (given) / out (threshold, pre-zeroed)
   int8_t* codes;           // may be null (SR-only launch)
   float* scales;           // may be null
@@ -22,7 +23,40 @@ struct QuantParams {
   float* amax_out;         // may be null
   int8_t* sr_codes;        // may be null
   uint64_t sr_seed;
+  int8_t* sr_codes2;       // optional second stochastic plane (own seed), may be null
+  uint64_t sr_seed2;
   int64_t row_offset;      // global row of this shard's row 0 (RNG index)
+};
+
+// GluCombine forward fused with the next linear's input quantizer.
+struct GluParams {
+  const void* ab;          // rows x ld_ab: a in cols [0, cols), b in [cols, 2 cols)
+  int64_t rows, cols, ld_ab;
+  int16_t* ctx_a;          // 1 x 128 RTN contexts (rows x ld_ctx), may be null
+  int16_t* ctx_b;
+  int64_t ld_ctx;
+  float* ctx_a_scales;     // rows x ceil(cols/128)
+  float* ctx_b_scales;
+  float ctx_level;         // 2^(bits-1) - 1 (511 for 10 bits)
+  float* h_out;            // optional fp32 h (rows x ld_h), parity/debug
+  int64_t ld_h;
+};
+
+// GluCombine backward fused with the gate/up dY stochastic quantizers.
+struct GluBwdParams {
+  const void* gh;          // dH, rows x ld_gh
+  int64_t rows, cols, ld_gh;
+  const int16_t* ctx_a;
+  const int16_t* ctx_b;
+  int64_t ld_ctx;
+  const float* ctx_a_scales;
+  const float* ctx_b_scales;
+  int8_t* gq;              // rows x ldq int8: [SR(ga) | SR(gb)]
+  int64_t ldq;
+  float* gq_scales;        // ceil(rows/128) x 2*ceil(cols/128)
+  uint64_t seed_a, seed_b; // DeterministicRng seeds of the gate / up dY streams
+  int64_t row_offset;
+  float* g_out;            // optional fp32 [2][rows][cols] (ga, gb), parity/debug
 };
 
 struct DequantParams {
@@ -37,6 +71,11 @@ struct DequantParams {
 
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
+cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s);
+cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s);
+cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,
+                              double r_min, double r_max, double alpha, double* last_rate,
+                              cudaStream_t s);
 cudaError_t launch_round_probe(const float* x, const float* a, const uint64_t* bits,
                                int8_t* out_rtn, int8_t* out_sr, int64_t n, cudaStream_t s);
 

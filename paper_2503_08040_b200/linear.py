@@ -1,0 +1,163 @@
+"""SwiGLU MLP driver (include/fbq_b200_host.h) from Python.
+
+``GluMlp`` mirrors the reference's gate/up -> GluCombine -> down composition
+(QuantLinearLayer::forward/backward, trainsim.cpp:61-127; GluCombine,
+trainsim.cpp:224-263).  The C++ driver owns its device workspaces; PyTorch
+tensors are only used to hand it device pointers and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _capi as K
+
+lib = K.lib
+
+
+class MlpConfig(C.Structure):
+    _fields_ = [
+        ("d_model", C.c_int64), ("d_ff", C.c_int64), ("max_tokens", C.c_int64),
+        ("act_dtype", C.c_int), ("mid_dtype", C.c_int), ("epilogue", C.c_int),
+        ("nonlinear_bits", C.c_int), ("layer_id_base", C.c_int), ("seed", C.c_uint64),
+        ("threshold_init", C.c_double), ("r_min", C.c_double), ("r_max", C.c_double),
+        ("alpha", C.c_double),
+    ]
+
+
+_F32P = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_sigs = {
+    "fbq_mlp_default_config": (None, [C.POINTER(MlpConfig)]),
+    "fbq_mlp_create": (C.c_void_p, [C.POINTER(MlpConfig), _F32P, _F32P, _F32P]),
+    "fbq_mlp_destroy": (None, [C.c_void_p]),
+    "fbq_mlp_forward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                         C.c_void_p, C.c_void_p]),
+    "fbq_mlp_backward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                          C.c_void_p, C.c_void_p]),
+    "fbq_mlp_controller_step": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_mlp_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_mlp_step_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                    C.c_void_p, C.c_void_p]),
+    "fbq_mlp_grad_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "fbq_mlp_get_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fbq_mlp_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "fbq_host_last_error": (C.c_char_p, []),
+}
+for _n, (_r, _a) in _sigs.items():
+    _f = getattr(lib, _n)
+    _f.restype = _r
+    _f.argtypes = _a
+
+
+def _check(st, what):
+    if st != K.FBQ_OK:
+        raise K.FbqError(st, f"{what} ({lib.fbq_host_last_error().decode()})")
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of a driver-owned fp32 buffer."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False), "version": 3,
+            "strides": None,
+        }
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class GluMlp:
+    """Fallback-quantized SwiGLU MLP (d_model -> d_ff -> d_model) on B200."""
+
+    def __init__(self, w_gate, w_up, w_down, max_tokens, *, act_dtype=torch.bfloat16,
+                 mid_dtype=torch.bfloat16, exact=False, threshold_init=1.0, seed=0x5EED,
+                 layer_id_base=0, nonlinear_bits=10, r_min=0.1, r_max=0.3, alpha=1.3):
+        wg = np.ascontiguousarray(np.asarray(w_gate, np.float32))
+        wu = np.ascontiguousarray(np.asarray(w_up, np.float32))
+        wd = np.ascontiguousarray(np.asarray(w_down, np.float32))
+        self.d_ff, self.d_model = wg.shape
+        assert wu.shape == wg.shape and wd.shape == (self.d_model, self.d_ff)
+        cfg = MlpConfig()
+        lib.fbq_mlp_default_config(C.byref(cfg))
+        cfg.d_model, cfg.d_ff, cfg.max_tokens = self.d_model, self.d_ff, max_tokens
+        dt = {torch.float32: K.FBQ_F32, torch.bfloat16: K.FBQ_BF16}
+        cfg.act_dtype, cfg.mid_dtype = dt[act_dtype], dt[mid_dtype]
+        cfg.epilogue = K.FBQ_EPI_EXACT if exact else K.FBQ_EPI_FMA
+        cfg.threshold_init, cfg.seed, cfg.layer_id_base = threshold_init, seed, layer_id_base
+        cfg.nonlinear_bits, cfg.r_min, cfg.r_max, cfg.alpha = nonlinear_bits, r_min, r_max, alpha
+        self.cfg = cfg
+        self.act_dtype = act_dtype
+        self.max_tokens = max_tokens
+        h = lib.fbq_mlp_create(C.byref(cfg), wg, wu, wd)
+        if not h:
+            raise K.FbqError(K.FBQ_ERR_ARG, f"fbq_mlp_create ({lib.fbq_host_last_error().decode()})")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.fbq_mlp_destroy(h)
+            self._h = None
+
+    # -- device API ----------------------------------------------------------
+    def forward(self, x: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        assert x.is_cuda and x.dtype == self.act_dtype and x.shape[1] == self.d_model
+        x = x.contiguous()
+        y = out if out is not None else torch.empty_like(x)
+        _check(lib.fbq_mlp_forward_device(self._h, x.data_ptr(), x.shape[0], row_offset, step,
+                                          y.data_ptr(), _stream()), "forward")
+        return y
+
+    def backward(self, gy: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        assert gy.is_cuda and gy.dtype == self.act_dtype and gy.shape[1] == self.d_model
+        gy = gy.contiguous()
+        gx = out if out is not None else torch.empty_like(gy)
+        _check(lib.fbq_mlp_backward_device(self._h, gy.data_ptr(), gy.shape[0], row_offset, step,
+                                           gx.data_ptr(), _stream()), "backward")
+        return gx
+
+    def controller_step(self):
+        _check(lib.fbq_mlp_controller_step(self._h, _stream()), "controller_step")
+
+    def zero_grad(self):
+        _check(lib.fbq_mlp_zero_grad(self._h, _stream()), "zero_grad")
+
+    def grad_tensors(self):
+        """Device fp32 views (gate+up contiguous, down) for the DP all-reduce."""
+        gu = torch.as_tensor(_DevArray(lib.fbq_mlp_grad_ptr(self._h, 0),
+                                       (2 * self.d_ff, self.d_model)), device="cuda")
+        gd = torch.as_tensor(_DevArray(lib.fbq_mlp_grad_ptr(self._h, 2),
+                                       (self.d_model, self.d_ff)), device="cuda")
+        return gu, gd
+
+    # -- host API (reference value semantics) --------------------------------
+    def step_host(self, x: np.ndarray, gy: np.ndarray, step: int, y=None, gx=None):
+        """fwd+bwd over host fp32 buffers (pinned numpy/torch CPU tensors welcome)."""
+        t = x.shape[0]
+        y = np.empty_like(x) if y is None else y
+        gx = np.empty_like(x) if gx is None else gx
+
+        def ptr(a):
+            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+        _check(lib.fbq_mlp_step_host(self._h, ptr(x), ptr(gy), t, step, ptr(y), ptr(gx)),
+               "step_host")
+        return y, gx
+
+    def grads_host(self):
+        gg = np.empty((self.d_ff, self.d_model), np.float32)
+        gu = np.empty_like(gg)
+        gd = np.empty((self.d_model, self.d_ff), np.float32)
+        _check(lib.fbq_mlp_get_grads(self._h, gg.ctypes.data, gu.ctypes.data, gd.ctypes.data),
+               "get_grads")
+        return gg, gu, gd
+
+    def controller_state(self):
+        r = (C.c_double * 2)()
+        t = (C.c_double * 2)()
+        _check(lib.fbq_mlp_get_controller(self._h, r, t), "get_controller")
+        return list(r), list(t)

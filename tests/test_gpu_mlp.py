@@ -1,0 +1,144 @@
+"""GPU: the fused SwiGLU-MLP driver vs the reference's own QuantLinearLayer x3
++ GluCombine composition (oracle/_ref, trainsim.cpp:61-127, 224-263)."""
+import numpy as np
+import pytest
+
+from tests.helpers import outlier_matrix, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+D, F, T = 256, 384, 384
+
+
+def weights(seed=0, d=D, f=F):
+    rng = np.random.default_rng(seed)
+    wg = (rng.standard_normal((f, d)) * 0.05).astype(np.float32)
+    wu = (rng.standard_normal((f, d)) * 0.05).astype(np.float32)
+    wd = (rng.standard_normal((d, f)) * 0.05).astype(np.float32)
+    return wg, wu, wd
+
+
+def inputs(seed=1, t=T, d=D):
+    x = outlier_matrix(t, d, seed=seed, body=0.3, channels=[5], tokens=[t // 3], mag_c=20.0,
+                       mag_t=40.0)
+    gy = outlier_matrix(t, d, seed=seed + 7, body=1e-3)
+    return x, gy
+
+
+@pytest.fixture(scope="module")
+def mods():
+    import torch  # noqa: F401
+    from oracle.oracle import REF_oracle, RefMlp
+    from paper_2503_08040_b200 import linear
+    if REF_oracle() is None:
+        pytest.skip("oracle/_ref not present")
+    return linear, RefMlp
+
+
+def _dev(a, dtype=None):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+@pytest.mark.parametrize("threshold", [1.0, 8.0])
+def test_mlp_step_bit_exact_vs_reference(mods, threshold):
+    """fp32 intermediates + exact epilogue reproduce the reference bit for bit."""
+    import torch
+    linear, RefMlp = mods
+    wg, wu, wd = weights()
+    x, gy = inputs()
+    ref = RefMlp(wg, wu, wd, threshold=threshold)
+    y_r, gx_r = ref.step(x, gy, 0)
+    m = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.float32,
+                      exact=True, threshold_init=threshold)
+    y = m.forward(_dev(x), 0)
+    gx = m.backward(_dev(gy), 0)
+    torch.cuda.synchronize()
+    y, gx = y.cpu().numpy(), gx.cpu().numpy()
+    assert np.array_equal(y.view(np.int32), y_r.view(np.int32)), rel_fro(y, y_r)
+    assert np.array_equal(gx.view(np.int32), gx_r.view(np.int32)), rel_fro(gx, gx_r)
+    for g, g_r in zip(m.grads_host(), ref.grads()):
+        assert np.array_equal(g.view(np.int32), g_r.view(np.int32)), rel_fro(g, g_r)
+    # controller (trainsim.cpp:129-133) fed with the same observed rates
+    m.controller_step()
+    rates, th = m.controller_state()
+    r_rates, r_th = ref.controller()
+    assert rates[0] == r_rates[0] == r_rates[1] and rates[1] == r_rates[2]
+    assert th[0] == r_th[0] == r_th[1] and th[1] == r_th[2]
+
+
+def test_mlp_multi_step_with_controller(mods):
+    import torch
+    linear, RefMlp = mods
+    wg, wu, wd = weights(3)
+    ref = RefMlp(wg, wu, wd, threshold=1.0)
+    m = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.float32,
+                      exact=True, threshold_init=1.0)
+    for step in range(4):
+        x, gy = inputs(10 + step)
+        y_r, gx_r = ref.step(x, gy, step)
+        y = m.forward(_dev(x), step).cpu().numpy()
+        gx = m.backward(_dev(gy), step).cpu().numpy()
+        assert np.array_equal(y.view(np.int32), y_r.view(np.int32)), (step, rel_fro(y, y_r))
+        assert np.array_equal(gx.view(np.int32), gx_r.view(np.int32)), (step, rel_fro(gx, gx_r))
+        m.controller_step()
+        _, th = m.controller_state()
+        _, r_th = ref.controller()
+        assert th[0] == r_th[0] and th[1] == r_th[2], (step, th, r_th)
+    for g, g_r in zip(m.grads_host(), ref.grads()):
+        assert np.array_equal(g.view(np.int32), g_r.view(np.int32))
+
+
+def test_mlp_bf16_fast_path_within_tolerance(mods):
+    """bf16 activations/intermediates + FMA epilogue: tolerance vs the fp32 reference."""
+    import torch
+    linear, RefMlp = mods
+    wg, wu, wd = weights(5)
+    x, gy = inputs(6)
+    ref = RefMlp(wg, wu, wd, threshold=4.0)
+    y_r, gx_r = ref.step(x, gy, 0)
+    m = linear.GluMlp(wg, wu, wd, T, threshold_init=4.0)  # bf16 / FMA defaults
+    y = m.forward(_dev(x, torch.bfloat16), 0).float().cpu().numpy()
+    gx = m.backward(_dev(gy, torch.bfloat16), 0).float().cpu().numpy()
+    assert rel_fro(y, y_r) < 3e-2
+    assert rel_fro(gx, gx_r) < 5e-2
+    for g, g_r in zip(m.grads_host(), ref.grads()):
+        assert rel_fro(g, g_r) < 5e-2
+
+
+def test_mlp_host_api_matches_device_api(mods):
+    import torch
+    linear, _ = mods
+    wg, wu, wd = weights(7)
+    x, gy = inputs(8)
+    kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True)
+    m1 = linear.GluMlp(wg, wu, wd, T, **kw)
+    m2 = linear.GluMlp(wg, wu, wd, T, **kw)
+    y1, gx1 = m1.step_host(x, gy, 2)
+    y2 = m2.forward(_dev(x), 2).cpu().numpy()
+    gx2 = m2.backward(_dev(gy), 2).cpu().numpy()
+    assert np.array_equal(y1, y2) and np.array_equal(gx1, gx2)
+    for a, b in zip(m1.grads_host(), m2.grads_host()):
+        assert np.array_equal(a, b)
+
+
+def test_mlp_token_shards_match_full_batch(mods):
+    """Token sharding (row_offset): per-row outputs bit-identical, dW sums within tolerance."""
+    import torch
+    linear, _ = mods
+    wg, wu, wd = weights(9)
+    x, gy = inputs(11, t=512)
+    kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True)
+    full = linear.GluMlp(wg, wu, wd, 512, **kw)
+    y = full.forward(_dev(x), 1).cpu().numpy()
+    gx = full.backward(_dev(gy), 1).cpu().numpy()
+    parts = []
+    for r0 in (0, 256):
+        m = linear.GluMlp(wg, wu, wd, 256, **kw)
+        ys = m.forward(_dev(x[r0:r0 + 256]), 1, row_offset=r0).cpu().numpy()
+        gxs = m.backward(_dev(gy[r0:r0 + 256]), 1, row_offset=r0).cpu().numpy()
+        assert np.array_equal(ys, y[r0:r0 + 256]) and np.array_equal(gxs, gx[r0:r0 + 256])
+        parts.append(m.grads_host())
+    for i, g in enumerate(full.grads_host()):
+        assert rel_fro(parts[0][i] + parts[1][i], g) < 1e-6
