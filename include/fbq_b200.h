@@ -100,11 +100,12 @@ int fbq_cuda_quantize_linear_input(const void* x, int dtype, int64_t rows, int64
  * or bf16); writes the ctx_bits-bit 1x128 RTN contexts of a and b (int16 codes,
  * trainsim.cpp:240-243) and quantizes h = silu(a)*b exactly like
  * fbq_cuda_quantize_linear_input (threshold mode) with one context plane.
- * h itself is not written unless h_out != NULL (fp32, parity/debug).  silu is
- * evaluated like silu_scalar (trainsim.cpp:38-41): double exp, one rounding. */
+ * h itself is not written unless h_out != NULL (fp32, parity/debug).  With
+ * exact_math != 0 silu is evaluated like silu_scalar (trainsim.cpp:38-41):
+ * double exp, one rounding; otherwise a fast fp32 form (a few ulp away). */
 int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, int64_t ld_ab,
                          int16_t* ctx_a, int16_t* ctx_b, int64_t ld_ctx, float* ctx_a_scales,
-                         float* ctx_b_scales, int ctx_bits, double theta,
+                         float* ctx_b_scales, int ctx_bits, int exact_math, double theta,
                          const double* theta_dev, uint32_t* mask_bits, int8_t* codes,
                          int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
                          int32_t* masked_count, int8_t* ctx_codes, uint64_t ctx_seed,
@@ -116,12 +117,13 @@ int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, 
  * (seeds seed_a / seed_b, RNG index over each rows x cols matrix) into
  * gq = [q(ga) | q(gb)] (int8 rows x ldq, ldq >= 2*cols) with scale grid
  * gq_scales [ceil(rows/128)][2*ceil(cols/128)].  g_out (optional fp32
- * [2][rows][cols]) receives ga, gb for parity checks. */
+ * [2][rows][cols]) receives ga, gb for parity checks.  exact_math as in
+ * fbq_cuda_glu_forward (silu / silu_grad_scalar, trainsim.cpp:38-46). */
 int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols, int64_t ld_gh,
                           const int16_t* ctx_a, const int16_t* ctx_b, int64_t ld_ctx,
                           const float* ctx_a_scales, const float* ctx_b_scales, int8_t* gq,
                           int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
-                          int64_t row_offset, float* g_out, fbq_stream_t stream);
+                          int64_t row_offset, float* g_out, int exact_math, fbq_stream_t stream);
 
 /* controller_update (policy.cpp:97-109) on device: rate = *masked_count /
  * n_blocks; *theta_dev /= alpha if rate < r_min, *= alpha if rate > r_max;

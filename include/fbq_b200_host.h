@@ -40,6 +40,8 @@ typedef struct fbq_mlp_config {
 } fbq_mlp_config;
 
 void fbq_mlp_default_config(fbq_mlp_config* cfg);
+/* Message of the last failing host-API call on this thread. */
+const char* fbq_host_last_error(void);
 
 /* w_gate, w_up: d_ff x d_model; w_down: d_model x d_ff (host fp32, row-major,
  * as QuantLinearLayer's weight, out x in).  Returns NULL on failure. */
@@ -62,6 +64,16 @@ int fbq_mlp_zero_grad(void* mlp, fbq_stream_t stream);
  * reference).  Pinned buffers make the copies asynchronous and overlapped. */
 int fbq_mlp_step_host(void* mlp, const float* x, const float* gy, int64_t tokens, int step,
                       float* y, float* gx);
+
+/* Set the device-resident thresholds (gate/up share one, down has its own). */
+int fbq_mlp_set_thresholds(void* mlp, double theta_gate_up, double theta_down);
+/* Optional CUDA-event timing of every GEMM launch (on the launching stream);
+ * fbq_mlp_gemm_time returns the summed GEMM time since profiling was enabled
+ * or last read (synchronise first) and resets. */
+int fbq_mlp_set_profiling(void* mlp, int on);
+int fbq_mlp_gemm_time(void* mlp, double* total_ms, int64_t* n_gemms);
+/* Number of our kernels launched by this driver so far. */
+int64_t fbq_mlp_launch_count(void* mlp);
 
 /* Device pointers of the fp32 gradient accumulators (for the data-parallel
  * all-reduce): which = 0 gate (d_ff x d_model), 1 up, 2 down (d_model x d_ff).

@@ -97,6 +97,8 @@ static int fill_quant_params(fbq::QuantParams& p, const void* x, int64_t rows, i
   p.sr_codes2 = sr_codes2;
   p.sr_seed2 = sr_seed2;
   p.row_offset = sr_row_offset;
+  p.vec_store = (ldq % 16 == 0) && aligned16(codes) && aligned16(res_codes) &&
+                aligned16(sr_codes) && aligned16(sr_codes2);
   return FBQ_OK;
 }
 
@@ -120,7 +122,7 @@ int fbq_cuda_quantize_linear_input(const void* x, int dtype, int64_t rows, int64
 
 int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, int64_t ld_ab,
                          int16_t* ctx_a, int16_t* ctx_b, int64_t ld_ctx, float* ctx_a_scales,
-                         float* ctx_b_scales, int ctx_bits, double theta,
+                         float* ctx_b_scales, int ctx_bits, int exact_math, double theta,
                          const double* theta_dev, uint32_t* mask_bits,
                          int8_t* codes, int64_t ldq, float* scales, int8_t* res_codes,
                          float* res_scales, int32_t* masked_count, int8_t* ctx_codes,
@@ -147,7 +149,7 @@ int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, 
     return st;
   if (ldq % 16) return FBQ_ERR_UNSUPPORTED;
   fbq::GluParams g{ab, rows, cols, ld_ab, ctx_a, ctx_b, ld_ctx, ctx_a_scales, ctx_b_scales,
-                   (float)((1 << (ctx_bits - 1)) - 1), h_out, ld_h};
+                   (float)((1 << (ctx_bits - 1)) - 1), h_out, ld_h, exact_math ? 1 : 0};
   return cuda_status(fbq::launch_glu_forward(g, p, dtype == FBQ_BF16, s));
 }
 
@@ -155,7 +157,7 @@ int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols,
                           const int16_t* ctx_a, const int16_t* ctx_b, int64_t ld_ctx,
                           const float* ctx_a_scales, const float* ctx_b_scales, int8_t* gq,
                           int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
-                          int64_t row_offset, float* g_out, fbq_stream_t stream) {
+                          int64_t row_offset, float* g_out, int exact_math, fbq_stream_t stream) {
   if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
   if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
   if (rows == 0 || cols == 0) return FBQ_OK;
@@ -168,7 +170,7 @@ int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols,
   if (cdiv(rows, 128) > 65535) return FBQ_ERR_UNSUPPORTED;
   fbq::GluBwdParams g{gh,    rows,   cols,   ld_gh,      ctx_a,     ctx_b,    ld_ctx,
                       ctx_a_scales, ctx_b_scales, gq, ldq, gq_scales, seed_a, seed_b,
-                      row_offset, g_out};
+                      row_offset, g_out, exact_math ? 1 : 0};
   return cuda_status(fbq::launch_glu_backward(g, dtype == FBQ_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 

@@ -34,24 +34,23 @@ __device__ __forceinline__ float block_scale(float amax) {
 
 // clamp(round_half_even(x / a), -L, L); a > 0.   kernels.cpp:24-40
 // (L = 127 for the 8-bit GEMM operands, 511 for the 10-bit non-linear contexts)
+// Slow path for scales so small that 1/a could overflow: the reference formula.
+__device__ __noinline__ int rtn_code_slow(float x, float a, float level) {
+  const float n = (float)rint(__ddiv_rn((double)x, (double)a));
+  return (int)fminf(fmaxf(n, -level), level);
+}
+// Branch-free fast path (callers guarantee a >= kTinyScale, block-uniformly).
+__device__ __forceinline__ int rtn_code_fast(float x, float a, float inv_a, float level) {
+  float n = rintf(__fmul_rn(x, inv_a));
+  const float rem = __fmaf_rn(-n, a, x);
+  const float two = __fmul_rn(2.0f, fabsf(rem));
+  // off by one, or an exact tie x/a = n +- 1/2 with n odd: step toward x
+  const bool step = (two > a) | ((two == a) & (((int)n & 1) != 0));
+  n = step ? (rem > 0.0f ? n + 1.0f : n - 1.0f) : n;
+  return (int)fminf(fmaxf(n, -level), level);
+}
 __device__ __forceinline__ int rtn_code(float x, float a, float inv_a, float level = 127.0f) {
-  float n;
-  if (a >= kTinyScale) {
-    n = rintf(__fmul_rn(x, inv_a));
-    const float rem = __fmaf_rn(-n, a, x);
-    const float two = __fmul_rn(2.0f, fabsf(rem));
-    if (two > a) {
-      n = rem > 0.0f ? n + 1.0f : n - 1.0f;
-    } else if (two == a) {
-      // exact tie between n and n + sign(rem): keep the even one
-      const float alt = rem > 0.0f ? n + 1.0f : n - 1.0f;
-      if (fmodf(n, 2.0f) != 0.0f) n = alt;
-    }
-  } else {
-    n = (float)rint(__ddiv_rn((double)x, (double)a));
-  }
-  n = fminf(fmaxf(n, -level), level);
-  return (int)n;
+  return a >= kTinyScale ? rtn_code_fast(x, a, inv_a, level) : rtn_code_slow(x, a, level);
 }
 
 // splitmix64 finalizer (rng.hpp:11-15)
@@ -68,40 +67,30 @@ constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;  // rng.hpp:29
 //   if (frac > 0 && uniform(lin) < frac) f += 1; clamp(+-127)
 // Fast path decides u < frac with an fp32 estimate whenever the two are more
 // than 2^-20 apart (the estimate's error is < 2^-21); otherwise (probability
-// ~2^-19 per element) it recomputes the reference's double formula exactly.
+// ~2^-19 per element) it recomputes the reference's double formula exactly,
+// out of line so the unrolled fast path stays small.
+__device__ __noinline__ int sr_code_slow(float x, float a, uint64_t bits) {
+  const double t = __ddiv_rn((double)x, (double)a);
+  double fd = floor(t);
+  const double frac = t - fd;
+  const double u = (double)(bits >> 11) * 0x1.0p-53;
+  if (frac > 0.0 && u < frac) fd += 1.0;
+  return (int)fmin(fmax(fd, -127.0), 127.0);
+}
 __device__ __forceinline__ int sr_code(float x, float a, float inv_a, uint64_t bits) {
-  float f;
-  bool slow = a < kTinyScale;
-  if (!slow) {
-    float n0 = floorf(__fmul_rn(x, inv_a));
-    float rem = __fmaf_rn(-n0, a, x);
-    if (rem < 0.0f) {
-      n0 -= 1.0f;
-      rem = __fmaf_rn(-n0, a, x);
-    } else if (rem >= a) {
-      n0 += 1.0f;
-      rem = __fmaf_rn(-n0, a, x);
-    }
-    // now n0 = floor(x/a) exactly, 0 <= rem < a, frac = rem / a
-    const float frac = __fmul_rn(rem, inv_a);
-    const float u = (float)(uint32_t)(bits >> 32) * 0x1p-32f;  // top bits of (bits>>11)*2^-53
-    const float d = u - frac;
-    if (fabsf(d) > 0x1p-20f) {
-      f = (rem > 0.0f && d < 0.0f) ? n0 + 1.0f : n0;
-    } else {
-      slow = true;
-    }
-  }
-  if (slow) {
-    const double t = __ddiv_rn((double)x, (double)a);
-    double fd = floor(t);
-    const double frac = t - fd;
-    const double u = (double)(bits >> 11) * 0x1.0p-53;
-    if (frac > 0.0 && u < frac) fd += 1.0;
-    f = (float)fd;
-  }
-  f = fminf(fmaxf(f, -127.0f), 127.0f);
-  return (int)f;
+  if (a < kTinyScale) return sr_code_slow(x, a, bits);
+  float n0 = floorf(__fmul_rn(x, inv_a));
+  float rem = __fmaf_rn(-n0, a, x);
+  // one correction step makes n0 = floor(x/a) exactly, 0 <= rem < a
+  const float adj = rem < 0.0f ? -1.0f : (rem >= a ? 1.0f : 0.0f);
+  n0 += adj;
+  rem = adj != 0.0f ? __fmaf_rn(-n0, a, x) : rem;
+  const float frac = __fmul_rn(rem, inv_a);
+  const float u = (float)(uint32_t)(bits >> 32) * 0x1p-32f;  // top bits of (bits>>11)*2^-53
+  const float d = u - frac;
+  if (fabsf(d) <= 0x1p-20f) return sr_code_slow(x, a, bits);
+  const float f = (rem > 0.0f && d < 0.0f) ? n0 + 1.0f : n0;
+  return (int)fminf(fmaxf(f, -127.0f), 127.0f);
 }
 
 }  // namespace fbq

@@ -20,6 +20,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../../include/fbq_b200_host.h"
 
@@ -164,12 +165,46 @@ struct Mlp {
   }
 
   ~Mlp() {
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd})
       if (e) cudaEventDestroy(e);
   }
 
   int layer(int i) const { return c.layer_id_base + i; }  // 0 gate, 1 up, 2 down
+  // reference-exact non-linear math in parity mode (fp32 intermediates)
+  int exact_math() const { return c.mid_dtype == FBQ_F32 ? 1 : 0; }
+
+  // ---- launch accounting and optional per-GEMM CUDA-event timing ----
+  int64_t launches = 0;        // our kernels launched (K1/K2/K3/GLU/controller)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t next_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      CU_TRY(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  template <class Fn>
+  void gemm(Fn&& launch, cudaStream_t s) {
+    if (profiling) CU_TRY(cudaEventRecord(next_event(), s));
+    FBQ_TRY(launch());
+    if (profiling) CU_TRY(cudaEventRecord(next_event(), s));
+    ++launches;
+  }
+  double gemm_ms_and_reset() {
+    double total = 0.0;
+    for (size_t i = 0; i + 1 < ev_used; i += 2) {
+      float ms = 0.f;
+      CU_TRY(cudaEventElapsedTime(&ms, ev_pool[i], ev_pool[i + 1]));
+      total += ms;
+    }
+    ev_used = 0;
+    return total;
+  }
 
   void forward(const void* x, int64_t tok, int64_t row_off, int step, void* y, cudaStream_t s) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
@@ -179,6 +214,7 @@ struct Mlp {
     double* th = theta.as<double>();
     // weights: one RTN quantization serves forward (K-major) and dgrad (MN-major);
     // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97, 121)
+    launches += 5;  // 2 x RTN(W), K1(X), GLU forward (+ the 2 GEMMs counted in gemm())
     FBQ_TRY(fbq_cuda_quantize_rtn(w_gu.p, FBQ_F32, 2 * F, D, D, wgu_codes.as<int8_t>(), ldD,
                                   wgu_scales.as<float>(), s));
     FBQ_TRY(fbq_cuda_quantize_rtn(w_d.p, FBQ_F32, D, F, F, wd_codes.as<int8_t>(), ldF,
@@ -191,22 +227,22 @@ struct Mlp {
         layer_seed(c.seed, layer(0), 0, step), ctx_u.as<int8_t>(),
         layer_seed(c.seed, layer(1), 0, step), row_off, s));
     // [a | b] = fallback_gemm(X, [W_g; W_u]^T)
-    FBQ_TRY(fbq_cuda_gemm(x_codes.as<int8_t>(), ldD, x_scales.as<float>(), FBQ_K_MAJOR,
+    gemm([&] { return fbq_cuda_gemm(x_codes.as<int8_t>(), ldD, x_scales.as<float>(), FBQ_K_MAJOR,
                           wgu_codes.as<int8_t>(), ldD, wgu_scales.as<float>(), FBQ_K_MAJOR,
                           x_mask.as<uint32_t>(), x_res.as<int8_t>(), x_res_scales.as<float>(),
-                          tok, 2 * F, D, ab.p, c.mid_dtype, 2 * F, 0, c.epilogue, s));
+                          tok, 2 * F, D, ab.p, c.mid_dtype, 2 * F, 0, c.epilogue, s); }, s);
     // GLU + contexts + quantization of h for the down projection
     FBQ_TRY(fbq_cuda_glu_forward(
         ab.p, c.mid_dtype, tok, F, 2 * F, ctx_a.as<int16_t>(), ctx_b.as<int16_t>(), ldF,
-        ctx_a_s.as<float>(), ctx_b_s.as<float>(), c.nonlinear_bits, c.threshold_init, th + 1,
+        ctx_a_s.as<float>(), ctx_b_s.as<float>(), c.nonlinear_bits, exact_math(), c.threshold_init, th + 1,
         h_mask.as<uint32_t>(), h_codes.as<int8_t>(), ldF, h_scales.as<float>(),
         h_res.as<int8_t>(), h_res_scales.as<float>(), cnt + 1, ctx_h.as<int8_t>(),
         layer_seed(c.seed, layer(2), 0, step), row_off, nullptr, 0, s));
     // y = fallback_gemm(h, W_d^T)
-    FBQ_TRY(fbq_cuda_gemm(h_codes.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_K_MAJOR,
+    gemm([&] { return fbq_cuda_gemm(h_codes.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_K_MAJOR,
                           wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_K_MAJOR,
                           h_mask.as<uint32_t>(), h_res.as<int8_t>(), h_res_scales.as<float>(),
-                          tok, D, F, y, c.act_dtype, D, 0, c.epilogue, s));
+                          tok, D, F, y, c.act_dtype, D, 0, c.epilogue, s); }, s);
     (void)gTt;
   }
 
@@ -214,48 +250,51 @@ struct Mlp {
                 cudaStream_t s) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
     if (tok == 0) return;
+    launches += 2;  // K2(dY), GLU backward (+ 6 GEMMs counted in gemm())
     // down: SR(dY) (trainsim.cpp:117-119)
     FBQ_TRY(fbq_cuda_quantize_stochastic(gy, c.act_dtype, tok, D, D,
                                          layer_seed(c.seed, layer(2), 1, step), row_off,
                                          gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), s));
     // dH = bqg(dY, W_d): B = W_d codes (D x F) read MN-major (trainsim.cpp:121-122)
-    FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_K_MAJOR,
+    gemm([&] { return fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_K_MAJOR,
                           wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_MN_MAJOR,
                           nullptr, nullptr, nullptr, tok, F, D, gh.p, c.mid_dtype, F, 0,
-                          c.epilogue, s));
+                          c.epilogue, s); }, s);
     // dW_d += bqg(dY^T, ctx_h) (trainsim.cpp:124-125)
-    FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_MN_MAJOR,
+    gemm([&] { return fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_MN_MAJOR,
                           ctx_h.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
-                          nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, 1, c.epilogue, s));
+                          nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, 1, c.epilogue, s); }, s);
     // GLU backward fused with SR(ga), SR(gb)
     FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.as<int16_t>(),
                                   ctx_b.as<int16_t>(), ldF, ctx_a_s.as<float>(),
                                   ctx_b_s.as<float>(), gq.as<int8_t>(), ldF2,
                                   gq_scales.as<float>(), layer_seed(c.seed, layer(0), 1, step),
-                                  layer_seed(c.seed, layer(1), 1, step), row_off, nullptr, s));
+                                  layer_seed(c.seed, layer(1), 1, step), row_off, nullptr,
+                                  exact_math(), s));
     // dX = bqg(ga, W_g) + bqg(gb, W_u)   (the reference adds the two layers' dX)
     const int64_t lds_gq = 2 * gF;
     int8_t* gqc = gq.as<int8_t>();
     float* gqs = gq_scales.as<float>();
-    FBQ_TRY(fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_K_MAJOR, wgu_codes.as<int8_t>(), ldD,
+    gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_K_MAJOR, wgu_codes.as<int8_t>(), ldD,
                              wgu_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr,
                              tok, D, F, gx, c.act_dtype, D, 0,
-                             c.epilogue, s));
-    FBQ_TRY(fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_K_MAJOR,
+                             c.epilogue, s); }, s);
+    gemm([&] { return fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_K_MAJOR,
                              wgu_codes.as<int8_t>() + F * ldD, ldD,
                              wgu_scales.as<float>() + gF * gD, gD, FBQ_MN_MAJOR, nullptr, nullptr,
-                             nullptr, tok, D, F, gx, c.act_dtype, D, 1, c.epilogue, s));
+                             nullptr, tok, D, F, gx, c.act_dtype, D, 1, c.epilogue, s); }, s);
     // dW_g += bqg(ga^T, ctx_g) ; dW_u += bqg(gb^T, ctx_u)
-    FBQ_TRY(fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_MN_MAJOR, ctx_g.as<int8_t>(), ldD,
+    gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_MN_MAJOR, ctx_g.as<int8_t>(), ldD,
                              x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr, F,
-                             D, tok, g_gu.p, FBQ_F32, D, 1, c.epilogue, s));
-    FBQ_TRY(fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_MN_MAJOR, ctx_u.as<int8_t>(),
+                             D, tok, g_gu.p, FBQ_F32, D, 1, c.epilogue, s); }, s);
+    gemm([&] { return fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_MN_MAJOR, ctx_u.as<int8_t>(),
                              ldD, x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr,
                              nullptr, F, D, tok, g_gu.as<float>() + F * D, FBQ_F32, D, 1,
-                             c.epilogue, s));
+                             c.epilogue, s); }, s);
   }
 
   void controller(cudaStream_t s) {
+    launches += 2;
     // observed rate = masked blocks / blocks of the last forward (policy.cpp:82-87)
     FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), counts.as<int32_t>(), last_blocks[0],
                                        c.r_min, c.r_max, c.alpha, rates.as<double>(), s));
@@ -395,6 +434,33 @@ int fbq_mlp_step_host(void* m, const float* x, const float* gy, int64_t tokens, 
     mlp->last_blocks[1] = cdiv(tokens, 128) * mlp->gF;
   });
 }
+
+int fbq_mlp_set_thresholds(void* m, double theta_gate_up, double theta_down) {
+  if (!m || !(theta_gate_up > 0.0) || !(theta_down > 0.0)) return FBQ_ERR_ARG;
+  return guarded([&] {
+    const double th[2] = {theta_gate_up, theta_down};
+    CU_TRY(cudaMemcpy(static_cast<Mlp*>(m)->theta.p, th, sizeof(th), cudaMemcpyHostToDevice));
+  });
+}
+
+int fbq_mlp_set_profiling(void* m, int on) {
+  if (!m) return FBQ_ERR_ARG;
+  auto* mlp = static_cast<Mlp*>(m);
+  mlp->profiling = on != 0;
+  mlp->ev_used = 0;
+  return FBQ_OK;
+}
+
+int fbq_mlp_gemm_time(void* m, double* total_ms, int64_t* n_gemms) {
+  if (!m || !total_ms) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    if (n_gemms) *n_gemms = (int64_t)(mlp->ev_used / 2);
+    *total_ms = mlp->gemm_ms_and_reset();
+  });
+}
+
+int64_t fbq_mlp_launch_count(void* m) { return m ? static_cast<Mlp*>(m)->launches : 0; }
 
 void* fbq_mlp_grad_ptr(void* m, int which) {
   if (!m) return nullptr;

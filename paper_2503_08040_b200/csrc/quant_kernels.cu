@@ -10,18 +10,20 @@
 //      (quantize_stochastic, quant.cpp:55-84).
 //  K4  dequantize / dequantize_fallback (quant.cpp:86-104, 178-202), parity/debug.
 //  GLU forward  (GluCombine::forward, trainsim.cpp:224-246, fused with the next
-//      linear's K1): h = silu(a) * b computed in registers from the gate/up GEMM
-//      output, 10-bit 1x128 RTN contexts of a and b, then K1 on h -- h itself
-//      never goes to HBM.
+//      linear's K1): h = silu(a) * b from the gate/up GEMM output, 10-bit 1x128
+//      RTN contexts of a and b, then K1 on h -- h itself never goes to HBM.
 //  GLU backward (GluCombine::backward, trainsim.cpp:248-263, fused with the
 //      gate/up linears' dY quantizer, trainsim.cpp:117-119): ga, gb from dH and
 //      the dequantized contexts, stochastic-rounded straight into the int8 code
 //      plane of [ga | gb].
 //
-// Work split: one 256-thread CTA per 128x128 block.  Each thread keeps its 64
-// elements in registers (16x 128-bit loads for fp32, 8 for bf16), so the
-// residual pass of a flagged block (fallback) re-uses registers and never
-// re-reads HBM.  Block absmax: warp shuffles + one smem exchange.
+// Work split: one 256-thread CTA per 128x128 block.  The raw block is staged
+// in shared memory with one coalesced, vectorised HBM read (all loads issued
+// before the first use); every later pass (absmax, RTN, stochastic planes,
+// the fallback residual) streams it from smem in a compact per-row loop, so
+// the kernels stay small (fully unrolling 64 values per thread through the
+// rounding/RNG code produced ~15-30K-instruction kernels that thrashed the
+// instruction cache).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -39,15 +41,27 @@ template <>
 __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) {
   return __bfloat162float(v);
 }
+template <>
+__device__ __forceinline__ float to_f32<int16_t>(int16_t v) { return (float)v; }
 
-template <typename T, bool kVec>
+template <typename T>
+__device__ __forceinline__ T zero_of();
+template <>
+__device__ __forceinline__ float zero_of<float>() { return 0.0f; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 zero_of<__nv_bfloat16>() { return __float2bfloat16(0.0f); }
+template <>
+__device__ __forceinline__ int16_t zero_of<int16_t>() { return 0; }
+
+// Thread <-> element map of a 128 x 128 block for 16-byte vectors of T.
+template <typename T>
 struct Tiling {
-  static constexpr int V = kVec ? int(16 / sizeof(T)) : 1;  // elements per load
-  static constexpr int VPR = kBlock / V;                    // loads per block row
-  static constexpr int RPP = kQuantThreads / VPR;           // rows per pass
-  static constexpr int NP = kBlock / RPP;                   // passes
-  static_assert(NP * V == 64, "64 elements per thread");
+  static constexpr int V = int(16 / sizeof(T));       // elements per vector
+  static constexpr int VPR = kBlock / V;              // vectors per block row
+  static constexpr int RPP = kQuantThreads / VPR;     // rows per pass
+  static constexpr int NP = kBlock / RPP;             // passes
 };
+constexpr int kTileElems = kBlock * kBlock;
 
 __device__ __forceinline__ float block_max(float v, float* red) {
 #pragma unroll
@@ -70,53 +84,104 @@ __device__ __forceinline__ float row_max(float v) {
   return v;
 }
 
+// Store V int8 codes: one vector store when the plane is 16-byte aligned and the
+// vector is whole, else element stores (ragged right edge / odd strides).
 template <int V>
-__device__ __forceinline__ void store_codes(int8_t* p, const int* c) {
-  if constexpr (V == 1) {
-    *p = (int8_t)c[0];
-  } else if constexpr (V == 4) {
-    uint32_t w = 0;
+__device__ __forceinline__ void store_codes(int8_t* p, const int* c, int n, bool vec) {
+  if (vec && n == V) {
+    if constexpr (V == 4) {
+      uint32_t w = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) w |= (uint32_t)(uint8_t)(int8_t)c[i] << (8 * i);
-    *reinterpret_cast<uint32_t*>(p) = w;
-  } else {
-    uint32_t w0 = 0, w1 = 0;
+      for (int i = 0; i < 4; ++i) w |= (uint32_t)(uint8_t)(int8_t)c[i] << (8 * i);
+      *reinterpret_cast<uint32_t*>(p) = w;
+    } else {
+      uint32_t w0 = 0, w1 = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      w0 |= (uint32_t)(uint8_t)(int8_t)c[i] << (8 * i);
-      w1 |= (uint32_t)(uint8_t)(int8_t)c[i + 4] << (8 * i);
+      for (int i = 0; i < 4; ++i) {
+        w0 |= (uint32_t)(uint8_t)(int8_t)c[i] << (8 * i);
+        w1 |= (uint32_t)(uint8_t)(int8_t)c[i + 4] << (8 * i);
+      }
+      *reinterpret_cast<uint2*>(p) = make_uint2(w0, w1);
     }
-    *reinterpret_cast<uint2*>(p) = make_uint2(w0, w1);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (i < n) p[i] = (int8_t)c[i];
   }
 }
 
 template <int V>
 __device__ __forceinline__ void store_codes16(int16_t* p, const int* c) {
-  if constexpr (V == 1) {
-    *p = (int16_t)c[0];
-  } else {
-    uint32_t w[V / 2];
+  uint32_t w[V / 2];
 #pragma unroll
-    for (int i = 0; i < V / 2; ++i)
-      w[i] = (uint32_t)(uint16_t)(int16_t)c[2 * i] | ((uint32_t)(uint16_t)(int16_t)c[2 * i + 1] << 16);
-    if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
-    else *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  for (int i = 0; i < V / 2; ++i)
+    w[i] = (uint32_t)(uint16_t)(int16_t)c[2 * i] | ((uint32_t)(uint16_t)(int16_t)c[2 * i + 1] << 16);
+  if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  else *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ------------------------------------------------------------------ staging
+// Copy a 128 x 128 block of T (row stride ld) into smem (row stride 128),
+// zero-filling outside [rows) x [cols).  All vector loads are issued before the
+// smem stores.  kVec requires 16-byte aligned rows and cols % V == 0.
+template <typename T, bool kVec>
+__device__ __forceinline__ void stage_tile(T* __restrict__ s, const T* __restrict__ g, int64_t ld,
+                                           int64_t rows, int64_t cols, int64_t r0, int64_t c0) {
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  if constexpr (kVec) {
+    uint4 raw[NP];
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {
+      const int64_t r = r0 + lr + ps * RPP, c = c0 + lc;
+      raw[ps] = (r < rows && c < cols) ? __ldcs(reinterpret_cast<const uint4*>(g + r * ld + c))
+                                       : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps)
+      *reinterpret_cast<uint4*>(s + (lr + ps * RPP) * kBlock + lc) = raw[ps];
+  } else {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < kTileElems; i += kQuantThreads) {
+      const int rr = i / kBlock, cc = i % kBlock;
+      const int64_t r = r0 + rr, c = c0 + cc;
+      s[i] = (r < rows && c < cols) ? g[r * ld + c] : zero_of<T>();
+    }
   }
 }
 
-// Everything K1 does once the block's 64 values per thread are in registers:
-// scale, fallback flag, RTN codes, stochastic context codes, residual.
-template <int V, int NP, int RPP>
-__device__ __forceinline__ void quantize_fragment(float (&v)[NP][V], const QuantParams& p,
-                                                  int64_t blk, int64_t r0, int64_t c0, int lr,
-                                                  int lc, float* red) {
-  const int t = threadIdx.x;
+template <typename T, int V>
+__device__ __forceinline__ void load_vec(const T* s, float (&v)[V]) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(s);
+  const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+  for (int i = 0; i < V; ++i) v[i] = to_f32(e[i]);
+}
+
+// ------------------------------------------------------------------ K1 core
+// Quantize one 128 x 128 block whose values are produced on demand by
+// `val(row_in_block, col_in_block, float (&v)[V])` (V consecutive columns).
+// Fused outputs per QuantParams: scale, fallback flag, RTN codes, up to two
+// stochastic context planes and the fallback residual of flagged blocks.
+// Entered by all threads of the CTA (it contains CTA barriers).
+template <int V, class Val>
+__device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk, int64_t r0,
+                                               int64_t c0, float* red, Val&& val) {
+  constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t cc = c0 + lc;
+  const bool lane_ok = cc < p.cols;
+  const int nvalid = (int)(p.cols - cc < V ? p.cols - cc : V);
   // ---- block absmax -> scale (quant.cpp:27-32) ----
   float m = 0.0f;
+#pragma unroll 1
+  for (int ps = 0; ps < NP; ++ps) {
+    float v[V];
+    val(lr + ps * RPP, lc, v);
 #pragma unroll
-  for (int ps = 0; ps < NP; ++ps)
-#pragma unroll
-    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[ps][i]));
+    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+  }
   const float amax = block_max(m, red);
   const float a = block_scale(amax);
   const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
@@ -128,133 +193,117 @@ __device__ __forceinline__ void quantize_fragment(float (&v)[NP][V], const Quant
   } else if (p.mask_mode == kMaskGiven) {
     flagged = (p.mask_bits[blk >> 5] >> (blk & 31)) & 1u;
   }
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     if (p.scales) p.scales[blk] = a;
     if (p.amax_out) p.amax_out[blk] = amax;
-    if (p.mask_mode == kMaskThreshold && flagged) {
-      atomicOr(p.mask_bits + (blk >> 5), 1u << (blk & 31));
-    }
+    if (p.mask_mode == kMaskThreshold && flagged) atomicOr(p.mask_bits + (blk >> 5), 1u << (blk & 31));
     if (flagged && p.masked_count) atomicAdd(p.masked_count, 1);
     if (p.res_scales && !flagged) p.res_scales[blk] = 0.0f;
   }
 
-  // ---- primary RTN codes (kernels.cpp:24-40); zero-scale block -> 0 ----
-  // Codes are produced and stored pass by pass (never held as arrays) to keep
-  // the register footprint low enough for 2 CTAs/SM.
-  const int64_t cc = c0 + lc;
-  if (p.codes) {
-#pragma unroll
+  // ---- RTN codes + stochastic context planes (kernels.cpp:24-40, quant.cpp:66-80) ----
+  if (lane_ok) {
+#pragma unroll 1
     for (int ps = 0; ps < NP; ++ps) {
+      const int rb = lr + ps * RPP;
+      const int64_t r = r0 + rb;
+      if (r >= p.rows) break;
+      float v[V];
+      val(rb, lc, v);
       int code[V];
+      if (p.codes) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) code[i] = a > 0.0f ? rtn_code(v[ps][i], a, inv_a) : 0;
-      const int64_t r = r0 + lr + ps * RPP;
-      if (r < p.rows && cc < p.cols) store_codes<V>(p.codes + r * p.ldq + cc, code);
-    }
-  }
-
-  // ---- stochastic codes at global element index (quant.cpp:66-80) ----
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    int8_t* dst = k ? p.sr_codes2 : p.sr_codes;
-    if (!dst) continue;
-    const uint64_t seed = k ? p.sr_seed2 : p.sr_seed;
-#pragma unroll
-    for (int ps = 0; ps < NP; ++ps) {
-      const int64_t r = r0 + lr + ps * RPP;
-      uint64_t z = seed + (uint64_t)((p.row_offset + r) * p.cols + cc + 1) * kGolden;
-      int sc[V];
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        sc[i] = a > 0.0f ? sr_code(v[ps][i], a, inv_a, mix64(z)) : 0;
-        z += kGolden;
+        for (int i = 0; i < V; ++i) code[i] = a > 0.0f ? rtn_code(v[i], a, inv_a) : 0;
+        store_codes<V>(p.codes + r * p.ldq + cc, code, nvalid, p.vec_store);
       }
-      if (r < p.rows && cc < p.cols) store_codes<V>(dst + r * p.ldq + cc, sc);
-    }
-  }
-
-  // ---- fallback residual for flagged blocks, from registers (quant.cpp:146-172) ----
-  if (flagged) {  // block-uniform branch
-    float m2 = 0.0f;
+#pragma unroll 1
+      for (int k = 0; k < 2; ++k) {
+        int8_t* dst = k ? p.sr_codes2 : p.sr_codes;
+        if (!dst) continue;
+        uint64_t z = (k ? p.sr_seed2 : p.sr_seed) +
+                     (uint64_t)((p.row_offset + r) * p.cols + cc + 1) * kGolden;
 #pragma unroll
-    for (int ps = 0; ps < NP; ++ps)
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const int c = a > 0.0f ? rtn_code(v[ps][i], a, inv_a) : 0;
-        const float rec = __fmul_rn((float)c, a);
-        v[ps][i] = __fsub_rn(v[ps][i], rec);  // out-of-range lanes stay 0 - 0
-        m2 = fmaxf(m2, fabsf(v[ps][i]));
-      }
-    const float ramax = block_max(m2, red);
-    const float ra = block_scale(ramax);
-    const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
-    if (p.res_codes) {
-#pragma unroll
-      for (int ps = 0; ps < NP; ++ps) {
-        int code[V];
-#pragma unroll
-        for (int i = 0; i < V; ++i) code[i] = ra > 0.0f ? rtn_code(v[ps][i], ra, inv_ra) : 0;
-        const int64_t r = r0 + lr + ps * RPP;
-        if (r < p.rows && cc < p.cols) store_codes<V>(p.res_codes + r * p.ldq + cc, code);
+        for (int i = 0; i < V; ++i) {
+          code[i] = a > 0.0f ? sr_code(v[i], a, inv_a, mix64(z)) : 0;
+          z += kGolden;
+        }
+        store_codes<V>(dst + r * p.ldq + cc, code, nvalid, p.vec_store);
       }
     }
-    if (t == 0 && p.res_scales) p.res_scales[blk] = ra;
   }
-}
+  if (!flagged) return;  // block-uniform
 
-template <typename T, int V, int NP, int RPP, bool kVec>
-__device__ __forceinline__ void load_tile(float (&v)[NP][V], const T* __restrict__ x, int64_t ldx,
-                                          int64_t rows, int64_t cols, int64_t r0, int64_t c0,
-                                          int lr, int lc) {
+  // ---- fallback residual (quant.cpp:146-172): res = fl(x - fl(c*a)), recomputed
+  //      from the staged values (no fp32 residual tile) ----
+  auto res = [&](int rb, float (&v)[V]) {
+    val(rb, lc, v);
 #pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = a > 0.0f ? rtn_code(v[i], a, inv_a) : 0;
+      v[i] = __fsub_rn(v[i], __fmul_rn((float)c, a));  // zero-filled lanes stay 0
+    }
+  };
+  m = 0.0f;
+#pragma unroll 1
   for (int ps = 0; ps < NP; ++ps) {
-    const int64_t r = r0 + lr + ps * RPP;
-    const int64_t c = c0 + lc;
-    if constexpr (kVec) {
-      if (r < rows && c < cols) {
-        const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(x + r * ldx + c));
-        const T* e = reinterpret_cast<const T*>(&raw);
+    float v[V];
+    res(lr + ps * RPP, v);
 #pragma unroll
-        for (int i = 0; i < V; ++i) v[ps][i] = to_f32(e[i]);
-      } else {
+    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+  }
+  const float ra = block_scale(block_max(m, red));
+  const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
+  if (threadIdx.x == 0 && p.res_scales) p.res_scales[blk] = ra;
+  if (!p.res_codes || !lane_ok) return;
+#pragma unroll 1
+  for (int ps = 0; ps < NP; ++ps) {
+    const int rb = lr + ps * RPP;
+    const int64_t r = r0 + rb;
+    if (r >= p.rows) break;
+    float v[V];
+    res(rb, v);
+    int code[V];
 #pragma unroll
-        for (int i = 0; i < V; ++i) v[ps][i] = 0.0f;
-      }
-    } else {
-      v[ps][0] = (r < rows && c < cols) ? to_f32(x[r * ldx + c]) : 0.0f;
-    }
+    for (int i = 0; i < V; ++i) code[i] = ra > 0.0f ? rtn_code(v[i], ra, inv_ra) : 0;
+    store_codes<V>(p.res_codes + r * p.ldq + cc, code, nvalid, p.vec_store);
   }
 }
 
 template <typename T, bool kVec>
-__global__ void __launch_bounds__(kQuantThreads, 2)
+__global__ void __launch_bounds__(kQuantThreads)
 fbq_quantize_block_kernel(QuantParams p) {
-  using Tl = Tiling<T, kVec>;
-  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  T* tile = reinterpret_cast<T*>(dsm);
   __shared__ float red[kQuantThreads / 32];
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
-  const int lc = (threadIdx.x % VPR) * V;  // local column of this thread's first element
-  const int lr = threadIdx.x / VPR;        // local row of pass 0
-  float v[NP][V];  // one HBM read of X
-  load_tile<T, V, NP, RPP, kVec>(v, reinterpret_cast<const T*>(p.x), p.ldx, p.rows, p.cols, r0,
-                                 c0, lr, lc);
-  quantize_fragment<V, NP, RPP>(v, p, bi * gridDim.x + bj, r0, c0, lr, lc, red);
+  stage_tile<T, kVec>(tile, reinterpret_cast<const T*>(p.x), p.ldx, p.rows, p.cols, r0, c0);
+  __syncthreads();
+  constexpr int V = Tiling<T>::V;
+  quantize_block<V>(p, bi * gridDim.x + bj, r0, c0, red,
+                    [&](int rb, int cb, float (&v)[V]) { load_vec<T, V>(tile + rb * kBlock + cb, v); });
 }
 
 // ------------------------------------------------------------------ GLU
 // silu(x) = x / (1 + exp(-x)) evaluated like the reference (trainsim.cpp:38-46):
-// double-precision exp and divide, rounded to float once.
-__device__ __forceinline__ float silu_ref(float x) {
+// double-precision exp and divide, rounded to float once (out of line).
+__device__ __noinline__ float silu_ref(float x) {
   return (float)((double)x / (1.0 + exp(-(double)x)));
 }
-__device__ __forceinline__ float silu_grad_ref(float x) {
+__device__ __noinline__ float silu_grad_ref(float x) {
   const double s = 1.0 / (1.0 + exp(-(double)x));
   return (float)(s * (1.0 + (double)x * (1.0 - s)));
 }
+// Fast fp32 variants for the bf16 training path (a few ulp from the reference).
+__device__ __forceinline__ float sigmoid_fast(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu_fast(float x) { return x * sigmoid_fast(x); }
+__device__ __forceinline__ float silu_grad_fast(float x) {
+  const float s = sigmoid_fast(x);
+  return s * (1.0f + x * (1.0f - s));
+}
 
-// 10-bit (or any <= 16-bit) RTN of one 1 x 128 row group shared by VPR threads
-// (quantize_rtn with GroupGeometry(1, 128), quant.cpp:36-53).
+// 1 x 128 row-group RTN shared by the VPR threads of a row (quantize_rtn with
+// GroupGeometry(1, 128), quant.cpp:36-53).
 template <int V, int VPR>
 __device__ __forceinline__ float group_rtn(const float (&x)[V], int (&code)[V], float level) {
   float m = 0.0f;
@@ -269,121 +318,172 @@ __device__ __forceinline__ float group_rtn(const float (&x)[V], int (&code)[V], 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kQuantThreads, 1)
+__global__ void __launch_bounds__(kQuantThreads)
 fbq_glu_forward_kernel(GluParams g, QuantParams p) {
-  using Tl = Tiling<T, true>;
-  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  // raw a and b tiles; h = silu(a) * b is recomputed from them on every pass
+  extern __shared__ __align__(16) uint8_t dsm[];
+  T* ta = reinterpret_cast<T*>(dsm);
+  T* tb = ta + kTileElems;
   __shared__ float red[kQuantThreads / 32];
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
-  const int lc = (threadIdx.x % VPR) * V;
-  const int lr = threadIdx.x / VPR;
   const T* ab = reinterpret_cast<const T*>(g.ab);
-  float va[NP][V], vb[NP][V];
-  load_tile<T, V, NP, RPP, true>(va, ab, g.ld_ab, g.rows, g.cols, r0, c0, lr, lc);
-  load_tile<T, V, NP, RPP, true>(vb, ab + g.cols, g.ld_ab, g.rows, g.cols, r0, c0, lr, lc);
+  stage_tile<T, true>(ta, ab, g.ld_ab, g.rows, g.cols, r0, c0);
+  stage_tile<T, true>(tb, ab + g.cols, g.ld_ab, g.rows, g.cols, r0, c0);
+  __syncthreads();
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
   const int64_t cc = c0 + lc;
-#pragma unroll
+  // 10-bit contexts of a and b (trainsim.cpp:240-243) [+ optional h_out]
+#pragma unroll 1
   for (int ps = 0; ps < NP; ++ps) {
-    const int64_t r = r0 + lr + ps * RPP;
-    const bool ok = r < g.rows && cc < g.cols;
-    // 10-bit contexts of a and b (trainsim.cpp:240-243)
+    const int rb = lr + ps * RPP;
+    const int64_t r = r0 + rb;
+    const bool ok = r < g.rows && cc < g.cols;  // cols % 8 == 0: uniform per row group
+    float va[V], vb[V];
+    load_vec<T, V>(ta + rb * kBlock + lc, va);
+    load_vec<T, V>(tb + rb * kBlock + lc, vb);
     int code[V];
-    float s = group_rtn<V, VPR>(va[ps], code, g.ctx_level);
+    float s = group_rtn<V, VPR>(va, code, g.ctx_level);
     if (ok && g.ctx_a) store_codes16<V>(g.ctx_a + r * g.ld_ctx + cc, code);
     if (ok && g.ctx_a_scales && lc == 0) g.ctx_a_scales[r * gcols + bj] = s;
-    s = group_rtn<V, VPR>(vb[ps], code, g.ctx_level);
+    s = group_rtn<V, VPR>(vb, code, g.ctx_level);
     if (ok && g.ctx_b) store_codes16<V>(g.ctx_b + r * g.ld_ctx + cc, code);
     if (ok && g.ctx_b_scales && lc == 0) g.ctx_b_scales[r * gcols + bj] = s;
-    // h = fl(silu(a) * b)  (trainsim.cpp:230)
-#pragma unroll
-    for (int i = 0; i < V; ++i) va[ps][i] = ok ? __fmul_rn(silu_ref(va[ps][i]), vb[ps][i]) : 0.0f;
     if (ok && g.h_out) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) g.h_out[r * g.ld_h + cc + i] = va[ps][i];
+      for (int i = 0; i < V; ++i) {
+        const float sa = g.exact_math ? silu_ref(va[i]) : silu_fast(va[i]);
+        g.h_out[r * g.ld_h + cc + i] = __fmul_rn(sa, vb[i]);
+      }
     }
   }
-  quantize_fragment<V, NP, RPP>(va, p, bi * gridDim.x + bj, r0, c0, lr, lc, red);
+  // h = fl(silu(a) * b) (trainsim.cpp:230), quantized like a linear input
+  quantize_block<V>(p, bi * gridDim.x + bj, r0, c0, red, [&](int rb, int cb, float (&v)[V]) {
+    float vb[V];
+    load_vec<T, V>(ta + rb * kBlock + cb, v);
+    load_vec<T, V>(tb + rb * kBlock + cb, vb);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float sa = g.exact_math ? silu_ref(v[i]) : silu_fast(v[i]);
+      v[i] = __fmul_rn(sa, vb[i]);  // zero-filled lanes: silu(0) * 0 = 0
+    }
+  });
 }
 
-// SR-quantize one 128x128 block held in registers into `dst` with its own
-// RNG stream; returns nothing, writes the block scale.
-template <int V, int NP, int RPP>
-__device__ __forceinline__ void sr_fragment(const float (&v)[NP][V], int8_t* dst, int64_t ldq,
-                                            float* scale_out, uint64_t seed, int64_t row_offset,
-                                            int64_t rows, int64_t cols, int64_t r0, int64_t c0,
-                                            int lr, int lc, float* red) {
+// SR-quantize one block whose values come from `val` into `dst` with its own
+// RNG stream (quant.cpp:55-84); writes the block scale.
+template <int V, class Val>
+__device__ __forceinline__ void sr_block(int8_t* dst, int64_t ldq, float* scale_out, uint64_t seed,
+                                         int64_t row_offset, int64_t rows, int64_t cols,
+                                         int64_t r0, int64_t c0, float* red, Val&& val) {
+  constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t cc = c0 + lc;
   float m = 0.0f;
+#pragma unroll 1
+  for (int ps = 0; ps < NP; ++ps) {
+    float v[V];
+    val(lr + ps * RPP, lc, v);
 #pragma unroll
-  for (int ps = 0; ps < NP; ++ps)
-#pragma unroll
-    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[ps][i]));
+    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+  }
   const float amax = block_max(m, red);
   const float a = block_scale(amax);
   const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
   if (threadIdx.x == 0) *scale_out = a;
-  const int64_t cc = c0 + lc;
-#pragma unroll
+  if (cc >= cols) return;
+#pragma unroll 1
   for (int ps = 0; ps < NP; ++ps) {
-    const int64_t r = r0 + lr + ps * RPP;
+    const int rb = lr + ps * RPP;
+    const int64_t r = r0 + rb;
+    if (r >= rows) break;
+    float v[V];
+    val(rb, lc, v);
     uint64_t z = seed + (uint64_t)((row_offset + r) * cols + cc + 1) * kGolden;
-    int sc[V];
+    int code[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      sc[i] = a > 0.0f ? sr_code(v[ps][i], a, inv_a, mix64(z)) : 0;
+      code[i] = a > 0.0f ? sr_code(v[i], a, inv_a, mix64(z)) : 0;
       z += kGolden;
     }
-    if (r < rows && cc < cols) store_codes<V>(dst + r * ldq + cc, sc);
+    store_codes<V>(dst + r * ldq + cc, code, V, true);
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kQuantThreads, 2)
+__global__ void __launch_bounds__(kQuantThreads)
 fbq_glu_backward_kernel(GluBwdParams g) {
-  using Tl = Tiling<T, true>;
-  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  T* tg = reinterpret_cast<T*>(dsm);
+  int16_t* tca = reinterpret_cast<int16_t*>(tg + kTileElems);
+  int16_t* tcb = tca + kTileElems;
+  __shared__ float sa_row[kBlock], sb_row[kBlock];
   __shared__ float red[kQuantThreads / 32];
+  constexpr int V = Tiling<T>::V;
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
-  const int lc = (threadIdx.x % VPR) * V;
-  const int lr = threadIdx.x / VPR;
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
-  const int64_t cc = c0 + lc;
-  const T* gh = reinterpret_cast<const T*>(g.gh);
-  float v[NP][V];
-  // pass 0: ga = fl(fl(gy * b) * silu'(a)); pass 1: gb = fl(gy * silu(a))   (trainsim.cpp:256-259)
-#pragma unroll 1
-  for (int which = 0; which < 2; ++which) {
-    load_tile<T, V, NP, RPP, true>(v, gh, g.ld_gh, g.rows, g.cols, r0, c0, lr, lc);
+  stage_tile<T, true>(tg, reinterpret_cast<const T*>(g.gh), g.ld_gh, g.rows, g.cols, r0, c0);
+  stage_tile<int16_t, true>(tca, g.ctx_a, g.ld_ctx, g.rows, g.cols, r0, c0);
+  stage_tile<int16_t, true>(tcb, g.ctx_b, g.ld_ctx, g.rows, g.cols, r0, c0);
+  if (threadIdx.x < kBlock) {
+    const int64_t r = r0 + threadIdx.x;
+    sa_row[threadIdx.x] = r < g.rows ? g.ctx_a_scales[r * gcols + bj] : 0.0f;
+    sb_row[threadIdx.x] = r < g.rows ? g.ctx_b_scales[r * gcols + bj] : 0.0f;
+  }
+  __syncthreads();
+  // dequantized contexts: fl(code * scale) (quant.cpp:86-104); codes read as
+  // one 16-byte smem vector per 8 values
+  auto deq = [&](const int16_t* t, float s, int rb, int cb, float (&v)[V]) {
 #pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = s == 0.0f ? 0.0f : __fmul_rn((float)t[rb * kBlock + cb + i], s);
+  };
+  // ga = fl(fl(gy * b) * silu'(a)),  gb = fl(gy * silu(a))   (trainsim.cpp:256-259)
+  auto ga = [&](int rb, int cb, float (&v)[V]) {
+    float a[V], b[V];
+    load_vec<T, V>(tg + rb * kBlock + cb, v);
+    deq(tca, sa_row[rb], rb, cb, a);
+    deq(tcb, sb_row[rb], rb, cb, b);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float sg = g.exact_math ? silu_grad_ref(a[i]) : silu_grad_fast(a[i]);
+      v[i] = __fmul_rn(__fmul_rn(v[i], b[i]), sg);
+    }
+  };
+  auto gb = [&](int rb, int cb, float (&v)[V]) {
+    float a[V];
+    load_vec<T, V>(tg + rb * kBlock + cb, v);
+    deq(tca, sa_row[rb], rb, cb, a);
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      v[i] = __fmul_rn(v[i], g.exact_math ? silu_ref(a[i]) : silu_fast(a[i]));
+  };
+  if (g.g_out) {
+    constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
+    const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+#pragma unroll 1
     for (int ps = 0; ps < NP; ++ps) {
-      const int64_t r = r0 + lr + ps * RPP;
-      const bool ok = r < g.rows && cc < g.cols;
-      const float sa = ok ? g.ctx_a_scales[r * gcols + bj] : 0.0f;
-      const float sb = ok ? g.ctx_b_scales[r * gcols + bj] : 0.0f;
+      const int rb = lr + ps * RPP;
+      const int64_t r = r0 + rb;
+      if (r >= g.rows || c0 + lc >= g.cols) continue;
+      float v[V], w[V];
+      ga(rb, lc, v);
+      gb(rb, lc, w);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        if (!ok) {
-          v[ps][i] = 0.0f;
-          continue;
-        }
-        // dequantize the contexts: fl(code * scale) (quant.cpp:86-104)
-        const float a = sa == 0.0f ? 0.0f : __fmul_rn((float)g.ctx_a[r * g.ld_ctx + cc + i], sa);
-        if (which == 0) {
-          const float b = sb == 0.0f ? 0.0f : __fmul_rn((float)g.ctx_b[r * g.ld_ctx + cc + i], sb);
-          v[ps][i] = __fmul_rn(__fmul_rn(v[ps][i], b), silu_grad_ref(a));
-        } else {
-          v[ps][i] = __fmul_rn(v[ps][i], silu_ref(a));
-        }
-        if (g.g_out) g.g_out[which * g.rows * g.cols + r * g.cols + cc + i] = v[ps][i];
+        g.g_out[r * g.cols + c0 + lc + i] = v[i];
+        g.g_out[g.rows * g.cols + r * g.cols + c0 + lc + i] = w[i];
       }
     }
-    const int64_t gq_bj = which * gcols + bj;
-    sr_fragment<V, NP, RPP>(v, g.gq + which * g.cols, g.ldq, g.gq_scales + bi * (2 * gcols) + gq_bj,
-                            which ? g.seed_b : g.seed_a, g.row_offset, g.rows, g.cols, r0, c0, lr,
-                            lc, red);
   }
+  sr_block<V>(g.gq, g.ldq, g.gq_scales + bi * (2 * gcols) + bj, g.seed_a, g.row_offset, g.rows,
+              g.cols, r0, c0, red, ga);
+  __syncthreads();
+  sr_block<V>(g.gq + g.cols, g.ldq, g.gq_scales + bi * (2 * gcols) + gcols + bj, g.seed_b,
+              g.row_offset, g.rows, g.cols, r0, c0, red, gb);
 }
 
 // Delay-threshold controller on device (policy.cpp:97-109, Algorithm 2):
@@ -396,14 +496,6 @@ __global__ void fbq_controller_kernel(double* theta, const int* masked_count, in
   if (rate < r_min) *theta /= alpha;
   else if (rate > r_max) *theta *= alpha;
   if (last_rate) *last_rate = rate;
-}
-
-cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,
-                              double r_min, double r_max, double alpha, double* last_rate,
-                              cudaStream_t s) {
-  fbq_controller_kernel<<<1, 1, 0, s>>>(theta, masked_count, n_blocks, r_min, r_max, alpha,
-                                        last_rate);
-  return cudaGetLastError();
 }
 
 // dequantize[_fallback]: y = fl(c*a) [+ fl(rc*ra)]  (quant.cpp:86-104, 178-202)
@@ -436,36 +528,71 @@ __global__ void fbq_round_probe_kernel(const float* x, const float* a, const uin
   }
 }
 
+// ------------------------------------------------------------------ launchers
+template <class K>
+static cudaError_t opt_in_smem(K kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <typename T, bool kVec>
+static cudaError_t launch_k1(const QuantParams& p, dim3 grid, cudaStream_t s) {
+  const size_t smem = sizeof(T) * kTileElems;
+  static bool ready = false;
+  if (!ready) {
+    if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec>, smem)) return e;
+    ready = true;
+  }
+  fbq_quantize_block_kernel<T, kVec><<<grid, kQuantThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
   const dim3 grid((unsigned)((p.cols + kBlock - 1) / kBlock),
                   (unsigned)((p.rows + kBlock - 1) / kBlock));
   const size_t esz = bf16 ? 2 : 4;
   const bool vec = (reinterpret_cast<uintptr_t>(p.x) % 16 == 0) && ((p.ldx * esz) % 16 == 0) &&
-                   (p.cols % 8 == 0) && (p.ldq % 16 == 0);
-  if (bf16) {
-    if (vec) fbq_quantize_block_kernel<__nv_bfloat16, true><<<grid, kQuantThreads, 0, s>>>(p);
-    else fbq_quantize_block_kernel<__nv_bfloat16, false><<<grid, kQuantThreads, 0, s>>>(p);
-  } else {
-    if (vec) fbq_quantize_block_kernel<float, true><<<grid, kQuantThreads, 0, s>>>(p);
-    else fbq_quantize_block_kernel<float, false><<<grid, kQuantThreads, 0, s>>>(p);
-  }
-  return cudaGetLastError();
+                   (p.cols % (16 / esz) == 0);
+  if (bf16) return vec ? launch_k1<__nv_bfloat16, true>(p, grid, s)
+                       : launch_k1<__nv_bfloat16, false>(p, grid, s);
+  return vec ? launch_k1<float, true>(p, grid, s) : launch_k1<float, false>(p, grid, s);
 }
 
 cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16,
                                cudaStream_t s) {
   const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
                   (unsigned)((g.rows + kBlock - 1) / kBlock));
-  if (bf16) fbq_glu_forward_kernel<__nv_bfloat16><<<grid, kQuantThreads, 0, s>>>(g, p);
-  else fbq_glu_forward_kernel<float><<<grid, kQuantThreads, 0, s>>>(g, p);
+  if (bf16) {
+    const size_t smem = 2 * sizeof(__nv_bfloat16) * kTileElems;
+    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16>, smem)) return e;
+    fbq_glu_forward_kernel<__nv_bfloat16><<<grid, kQuantThreads, smem, s>>>(g, p);
+  } else {
+    const size_t smem = 2 * sizeof(float) * kTileElems;
+    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<float>, smem)) return e;
+    fbq_glu_forward_kernel<float><<<grid, kQuantThreads, smem, s>>>(g, p);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s) {
   const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
                   (unsigned)((g.rows + kBlock - 1) / kBlock));
-  if (bf16) fbq_glu_backward_kernel<__nv_bfloat16><<<grid, kQuantThreads, 0, s>>>(g);
-  else fbq_glu_backward_kernel<float><<<grid, kQuantThreads, 0, s>>>(g);
+  if (bf16) {
+    const size_t smem = (sizeof(__nv_bfloat16) + 2 * sizeof(int16_t)) * kTileElems;
+    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<__nv_bfloat16>, smem)) return e;
+    fbq_glu_backward_kernel<__nv_bfloat16><<<grid, kQuantThreads, smem, s>>>(g);
+  } else {
+    const size_t smem = (sizeof(float) + 2 * sizeof(int16_t)) * kTileElems;
+    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<float>, smem)) return e;
+    fbq_glu_backward_kernel<float><<<grid, kQuantThreads, smem, s>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,
+                              double r_min, double r_max, double alpha, double* last_rate,
+                              cudaStream_t s) {
+  fbq_controller_kernel<<<1, 1, 0, s>>>(theta, masked_count, n_blocks, r_min, r_max, alpha,
+                                        last_rate);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@ struct QuantParams {
   const void* x;       // rows x ldx, fp32 or bf16
   int64_t rows, cols, ldx;
   int64_t ldq;         // leading dim of every int8 code plane
+  int vec_store;       // 1: all code planes 16-byte aligned with ldq % 16 == 0
   int mask_mode;
   double theta;
   const double* theta_dev;  // if non-null, the threshold is read on device (controller state)
@@ -40,6 +41,7 @@ struct GluParams {
   float ctx_level;         // 2^(bits-1) - 1 (511 for 10 bits)
   float* h_out;            // optional fp32 h (rows x ld_h), parity/debug
   int64_t ld_h;
+  int exact_math;          // 1: silu like the reference (double); 0: fast fp32
 };
 
 // GluCombine backward fused with the gate/up dY stochastic quantizers.
@@ -57,6 +59,7 @@ struct GluBwdParams {
   uint64_t seed_a, seed_b; // DeterministicRng seeds of the gate / up dY streams
   int64_t row_offset;
   float* g_out;            // optional fp32 [2][rows][cols] (ga, gb), parity/debug
+  int exact_math;          // 1: silu / silu' like the reference (double); 0: fast fp32
 };
 
 struct DequantParams {

@@ -44,6 +44,10 @@ _sigs = {
     "fbq_mlp_get_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fbq_mlp_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "fbq_host_last_error": (C.c_char_p, []),
+    "fbq_mlp_set_thresholds": (C.c_int, [C.c_void_p, C.c_double, C.c_double]),
+    "fbq_mlp_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "fbq_mlp_gemm_time": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "fbq_mlp_launch_count": (C.c_int64, [C.c_void_p]),
 }
 for _n, (_r, _a) in _sigs.items():
     _f = getattr(lib, _n)
@@ -155,6 +159,21 @@ class GluMlp:
         _check(lib.fbq_mlp_get_grads(self._h, gg.ctypes.data, gu.ctypes.data, gd.ctypes.data),
                "get_grads")
         return gg, gu, gd
+
+    def set_thresholds(self, theta_gate_up: float, theta_down: float):
+        _check(lib.fbq_mlp_set_thresholds(self._h, theta_gate_up, theta_down), "set_thresholds")
+
+    def set_profiling(self, on: bool):
+        _check(lib.fbq_mlp_set_profiling(self._h, int(on)), "set_profiling")
+
+    def gemm_time(self):
+        """(summed GEMM milliseconds, number of GEMM launches) since the last call."""
+        ms, n = C.c_double(), C.c_int64()
+        _check(lib.fbq_mlp_gemm_time(self._h, C.byref(ms), C.byref(n)), "gemm_time")
+        return ms.value, n.value
+
+    def launch_count(self) -> int:
+        return lib.fbq_mlp_launch_count(self._h)
 
     def controller_state(self):
         r = (C.c_double * 2)()
