@@ -61,6 +61,16 @@ const char* fbq_status_string(int status);
 int fbq_last_cuda_error(void); /* cudaError_t of the last FBQ_ERR_CUDA on this thread */
 int fbq_block_side(void);      /* 128 */
 
+/* Device memory helpers (synchronous; default stream) so that bindings -- the
+ * reference-typed C++ adapter, cgo/ctypes stubs -- need no CUDA runtime of
+ * their own. */
+int fbq_malloc(void** ptr, size_t bytes);
+int fbq_free(void* ptr);
+int fbq_memcpy_h2d(void* dst, const void* src, size_t bytes);
+int fbq_memcpy_d2h(void* dst, const void* src, size_t bytes);
+int fbq_memset(void* dst, int value, size_t bytes);
+int fbq_synchronize(void);
+
 /* score_blocks(AbsMax) -- policy.cpp:12-28 / policy.hpp:18-19.
  * amax[blk] = max |x| over the block (float; the reference widens to double). */
 int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,

@@ -44,6 +44,9 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir(REF_SRC)
     if ref:
         subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+        lib = os.path.join(os.path.dirname(HERE), "paper_2503_08040_b200", "lib", "libfbq_b200.so")
+        if os.path.exists(lib):  # the reference-typed adapter test links the B200 library
+            subprocess.run(["make", "-s", "-C", HERE, "adapter_test"], check=True)
 
 
 def cdiv(a: int, b: int) -> int:

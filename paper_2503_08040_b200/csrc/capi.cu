@@ -41,6 +41,24 @@ void fbq_debug_set_gemm_diag(int flags) { g_gemm_diag = flags; }
 /* device buffer of 5 x num_SMs int64: MMA-warp total / full-wait / tmem-wait / page-wait / issue cycles */
 void fbq_debug_set_gemm_prof(long long* dev_buf) { g_gemm_prof = dev_buf; }
 int fbq_block_side(void) { return 128; }
+
+int fbq_malloc(void** ptr, size_t bytes) {
+  if (!ptr) return FBQ_ERR_ARG;
+  *ptr = nullptr;
+  if (bytes == 0) return FBQ_OK;
+  return cuda_status(cudaMalloc(ptr, bytes));
+}
+int fbq_free(void* ptr) { return ptr ? cuda_status(cudaFree(ptr)) : FBQ_OK; }
+int fbq_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  return bytes ? cuda_status(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)) : FBQ_OK;
+}
+int fbq_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  return bytes ? cuda_status(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)) : FBQ_OK;
+}
+int fbq_memset(void* dst, int value, size_t bytes) {
+  return bytes ? cuda_status(cudaMemset(dst, value, bytes)) : FBQ_OK;
+}
+int fbq_synchronize(void) { return cuda_status(cudaDeviceSynchronize()); }
 int fbq_last_cuda_error(void) { return g_last_cuda; }
 
 const char* fbq_status_string(int s) {

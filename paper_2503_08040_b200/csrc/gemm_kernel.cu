@@ -65,6 +65,21 @@ struct ScalePage {
 constexpr size_t kSmemBytes =
     1024 + (size_t)kStages * kStageBytes + 2 * sizeof(ScalePage) + 256;
 
+// Grouped rasterisation: tiles walk kGroupM block-rows at a time (bm fastest),
+// so the ~148 CTAs resident at once share kGroupM A row-panels and ~148/kGroupM
+// B column-panels in L2 instead of re-streaming all of B for every block-row
+// (row-major order read the gate/up B operand ~30x from DRAM).
+constexpr int kGroupM = 8;
+__device__ __forceinline__ void tile_coords(int tile, int MB, int NT, int& bm, int& bn2) {
+  const int per_group = kGroupM * NT;
+  const int group = tile / per_group;
+  const int first = group * kGroupM;
+  const int rows = min(kGroupM, MB - first);
+  const int in = tile - group * per_group;
+  bm = first + in % rows;
+  bn2 = in / rows;
+}
+
 __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t blk) {
   return (bits[blk >> 5] >> (blk & 31)) & 1u;
 }
@@ -149,8 +164,9 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint64_t pol = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0, pc = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int bm = tile / NT, bn2 = tile % NT;
+      for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        int bm, bn2;
+        tile_coords(tile, p.MB, NT, bm, bn2);
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
           mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
@@ -202,36 +218,37 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       int stage = 0;
       uint32_t phase = 0, item = 0, pc = 0;
       long long t_full = 0, t_tempty = 0, t_page = 0, t_issue = 0;
-      const long long t_start = clock64();
+      const bool prof = p.prof != nullptr;
+      const long long t_start = prof ? clock64() : 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
-          long long t0 = clock64();
-          mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
-          t_page += clock64() - t0;
+          long long t0 = prof ? clock64() : 0;
+          if (!(p.diag & 512)) mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
+          if (prof) t_page += clock64() - t0;
           const int nk = min(kPage, p.KB - pg);
           for (int j = 0; j < nk; ++j) {
-            const int n_items = sp.flag[j] ? 2 : 1;
-            t0 = clock64();
+            const int n_items = (!(p.diag & 512) && sp.flag[j]) ? 2 : 1;
+            t0 = prof ? clock64() : 0;
             if (!(p.diag & 16)) mbar_wait(full + stage, phase);
-            t_full += clock64() - t0;
+            if (prof) t_full += clock64() - t0;
             tc_fence_after();
             const uint32_t sa = smem0 + stage * kStageBytes;
             const uint64_t bd0 = b_tmpl | ((sa + 2 * kTileA) >> 4);
             for (int r = 0; r < n_items; ++r) {
               const uint32_t slot = item & 1;
-              t0 = clock64();
+              t0 = prof ? clock64() : 0;
               if (!(p.diag & 8)) mbar_wait(tempty + slot, ((item >> 1) & 1) ^ 1);
-              t_tempty += clock64() - t0;
+              if (prof) t_tempty += clock64() - t0;
               tc_fence_after();
-              t0 = clock64();
+              t0 = prof ? clock64() : 0;
               const uint64_t ad0 = a_tmpl | ((sa + (r ? kTileA : 0)) >> 4);
               const uint32_t d = tmem_base + slot * 256;
 #pragma unroll
               for (int kk = 0; kk < kBK / 32; ++kk)
                 mma_i8(d, ad0 + kk * a_step, bd0 + kk * b_step, idesc, kk > 0 ? 1u : 0u);
               mma_commit(tfull + slot);
-              t_issue += clock64() - t0;
+              if (prof) t_issue += clock64() - t0;
               ++item;
             }
             mma_commit(empty + stage);
@@ -251,8 +268,9 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   } else if (warp == 2) {
     // ===================== scale loader =====================
     uint32_t pc = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int bm = tile / NT, bn2 = tile % NT;
+    for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int bm, bn2;
+      tile_coords(tile, p.MB, NT, bm, bn2);
       const int bn0 = 2 * bn2, bn1 = 2 * bn2 + 1;
       for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
         ScalePage& sp = pages[pc & 1];
@@ -289,8 +307,9 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
 
     uint32_t item = 0, pc = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int bm = tile / NT, bn2 = tile % NT;
+    for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int bm, bn2;
+      tile_coords(tile, p.MB, NT, bm, bn2);
       const int bn = bn2 * 2 + h;
       float2 acc[64];
 #pragma unroll
@@ -333,21 +352,23 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 ++item;
                 continue;
               }
+              // Two 32-column loads in flight; the slot is released right after
+              // the last load lands (two consumes in between), the remaining math
+              // overlaps the next item's MMA.  The release latency is what paces
+              // the tensor pipe with only two TMEM slots.
               uint32_t va[32], vb[32];
               tmem_ld32(tb + 0, va);
-              tmem_ld_wait();
               tmem_ld32(tb + 32, vb);
-              consume<kEpi>(va, acc + 0, s, p.one);
               tmem_ld_wait();
+              consume<kEpi>(va, acc + 0, s, p.one);
               tmem_ld32(tb + 64, va);
               consume<kEpi>(vb, acc + 16, s, p.one);
-              tmem_ld_wait();
               tmem_ld32(tb + 96, vb);
-              consume<kEpi>(va, acc + 32, s, p.one);
               tmem_ld_wait();
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(tempty + slot);
+              consume<kEpi>(va, acc + 32, s, p.one);
               consume<kEpi>(vb, acc + 48, s, p.one);
             }
             ++item;

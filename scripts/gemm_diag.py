@@ -41,7 +41,7 @@ for (M, N, K) in [(8192, 14336, 4096)]:
     wq = fbq.transpose(fbq.quantize_rtn(w))
     qa = fbq.quantize_rtn(x)
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    for d in [0]:
+    for d in [0, 31, 512 + 31]:
         lib.fbq_debug_set_gemm_diag(d)
         lib.fbq_debug_set_gemm_prof(prof.data_ptr())
         fbq.block_quant_gemm(qa, wq, out=out, exact=False)
@@ -52,3 +52,11 @@ for (M, N, K) in [(8192, 14336, 4096)]:
         print(f"diag={d} per-item cycles: total {pr[0]/items:.0f} full-wait {pr[1]/items:.0f} "
               f"tmem-wait {pr[2]/items:.0f} page-wait {pr[3]/items:.0f} issue {pr[4]/items:.0f} (MMA ideal 512)", flush=True)
     lib.fbq_debug_set_gemm_diag(0)
+
+# wall-clock TOPS without the per-item clock reads (prof disabled)
+lib.fbq_debug_set_gemm_prof(None)
+for d in [0, 31, 512 + 31]:
+    lib.fbq_debug_set_gemm_diag(d)
+    t = timeit(lambda: fbq.block_quant_gemm(qa, wq, out=out, exact=False))
+    print(f"no-prof diag={d}: {t*1e3:.3f} ms {2*M*N*K/t/1e12:.0f} TOPS", flush=True)
+lib.fbq_debug_set_gemm_diag(0)
