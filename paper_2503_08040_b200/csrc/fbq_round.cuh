@@ -39,15 +39,24 @@ __device__ __noinline__ int rtn_code_slow(float x, float a, float level) {
   const float n = (float)rint(__ddiv_rn((double)x, (double)a));
   return (int)fminf(fmaxf(n, -level), level);
 }
-// Branch-free fast path (callers guarantee a >= kTinyScale, block-uniformly).
+// Branch-free fast path (a >= kTinyScale).  Rounding goes through the
+// "magic" constant M = 1.5 * 2^23: fl(t + M) rounds t to the nearest integer
+// with ties to even (|t| < 2^22), as_int(fl(t + M)) - as_int(M) is that integer
+// and fl(fl(t + M) - M) is it as a float -- FADD/IADD only, no F2I/FRND
+// (conversion-pipe) instructions.
+constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
 __device__ __forceinline__ int rtn_code_fast(float x, float a, float inv_a, float level) {
-  float n = rintf(__fmul_rn(x, inv_a));
-  const float rem = __fmaf_rn(-n, a, x);
-  const float two = __fmul_rn(2.0f, fabsf(rem));
+  const float m = __fadd_rn(__fmul_rn(x, inv_a), kMagic);
+  const float n = __fsub_rn(m, kMagic);
+  int ni = __float_as_int(m) - kMagicBits;
+  const float rem = __fmaf_rn(-n, a, x);  // exact
+  const float two = __fadd_rn(fabsf(rem), fabsf(rem));
   // off by one, or an exact tie x/a = n +- 1/2 with n odd: step toward x
-  const bool step = (two > a) | ((two == a) & (((int)n & 1) != 0));
-  n = step ? (rem > 0.0f ? n + 1.0f : n - 1.0f) : n;
-  return (int)fminf(fmaxf(n, -level), level);
+  const bool step = (two > a) | ((two == a) & ((ni & 1) != 0));
+  ni += step ? (rem > 0.0f ? 1 : -1) : 0;
+  const int L = (int)level;
+  return min(max(ni, -L), L);
 }
 __device__ __forceinline__ int rtn_code(float x, float a, float inv_a, float level = 127.0f) {
   return a >= kTinyScale ? rtn_code_fast(x, a, inv_a, level) : rtn_code_slow(x, a, level);
@@ -79,18 +88,24 @@ __device__ __noinline__ int sr_code_slow(float x, float a, uint64_t bits) {
 }
 __device__ __forceinline__ int sr_code(float x, float a, float inv_a, uint64_t bits) {
   if (a < kTinyScale) return sr_code_slow(x, a, bits);
-  float n0 = floorf(__fmul_rn(x, inv_a));
+  // nearest integer via the magic constant, then one exact-remainder correction
+  // turns it into floor(x/a) with 0 <= rem < a
+  const float m = __fadd_rn(__fmul_rn(x, inv_a), kMagic);
+  float n0 = __fsub_rn(m, kMagic);
+  int ni = __float_as_int(m) - kMagicBits;
   float rem = __fmaf_rn(-n0, a, x);
-  // one correction step makes n0 = floor(x/a) exactly, 0 <= rem < a
-  const float adj = rem < 0.0f ? -1.0f : (rem >= a ? 1.0f : 0.0f);
-  n0 += adj;
-  rem = adj != 0.0f ? __fmaf_rn(-n0, a, x) : rem;
+  const bool neg = rem < 0.0f;
+  n0 = neg ? n0 - 1.0f : n0;
+  ni -= neg ? 1 : 0;
+  rem = neg ? __fmaf_rn(-n0, a, x) : rem;
   const float frac = __fmul_rn(rem, inv_a);
-  const float u = (float)(uint32_t)(bits >> 32) * 0x1p-32f;  // top bits of (bits>>11)*2^-53
+  // u ~ (bits >> 11) * 2^-53 to 2^-23 from the top mantissa bits (no I2F):
+  // as_float(0x3F800000 | top 23 bits) - 1 is in [0, 1)
+  const float u = __fsub_rn(__uint_as_float(0x3F800000u | (uint32_t)(bits >> 41)), 1.0f);
   const float d = u - frac;
   if (fabsf(d) <= 0x1p-20f) return sr_code_slow(x, a, bits);
-  const float f = (rem > 0.0f && d < 0.0f) ? n0 + 1.0f : n0;
-  return (int)fminf(fmaxf(f, -127.0f), 127.0f);
+  ni += (rem > 0.0f && d < 0.0f) ? 1 : 0;
+  return min(max(ni, -127), 127);
 }
 
 }  // namespace fbq

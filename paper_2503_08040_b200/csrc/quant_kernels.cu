@@ -160,12 +160,40 @@ __device__ __forceinline__ void load_vec(const T* s, float (&v)[V]) {
 }
 
 // ------------------------------------------------------------------ K1 core
+// Per-block rounding dispatch, decided once per block (block-uniform): zero
+// scale -> all codes 0; tiny scale -> the reference's double formula (out of
+// line); otherwise the branch-free fp32 path.
+template <int V>
+__device__ __forceinline__ void rtn_vec(const float (&v)[V], float a, float inv_a, int mode,
+                                        int (&code)[V]) {
+  if (mode == 2) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) code[i] = rtn_code_fast(v[i], a, inv_a, 127.0f);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) code[i] = mode == 0 ? 0 : rtn_code_slow(v[i], a, 127.0f);
+  }
+}
+template <int V>
+__device__ __forceinline__ void sr_vec(const float (&v)[V], float a, float inv_a, int mode,
+                                       uint64_t z, int (&code)[V]) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    code[i] = mode == 0 ? 0 : sr_code(v[i], a, inv_a, mix64(z));
+    z += kGolden;
+  }
+}
+__device__ __forceinline__ int round_mode(float a) {
+  return a == 0.0f ? 0 : (a < kTinyScale ? 1 : 2);
+}
+
 // Quantize one 128 x 128 block whose values are produced on demand by
 // `val(row_in_block, col_in_block, float (&v)[V])` (V consecutive columns).
-// Fused outputs per QuantParams: scale, fallback flag, RTN codes, up to two
+// Fused outputs per QuantParams: scale, fallback flag, RTN codes, kSR (0-2)
 // stochastic context planes and the fallback residual of flagged blocks.
+// kSR is a compile-time count so RTN-only launches carry no RNG code.
 // Entered by all threads of the CTA (it contains CTA barriers).
-template <int V, class Val>
+template <int V, int kSR, class Val>
 __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk, int64_t r0,
                                                int64_t c0, float* red, Val&& val) {
   constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
@@ -185,6 +213,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   const float amax = block_max(m, red);
   const float a = block_scale(amax);
   const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
+  const int mode = round_mode(a);
 
   bool flagged = false;
   if (p.mask_mode == kMaskThreshold) {
@@ -202,7 +231,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   }
 
   // ---- RTN codes + stochastic context planes (kernels.cpp:24-40, quant.cpp:66-80) ----
-  if (lane_ok) {
+  if (lane_ok && (p.codes || kSR > 0)) {
 #pragma unroll 1
     for (int ps = 0; ps < NP; ++ps) {
       const int rb = lr + ps * RPP;
@@ -212,22 +241,17 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
       val(rb, lc, v);
       int code[V];
       if (p.codes) {
-#pragma unroll
-        for (int i = 0; i < V; ++i) code[i] = a > 0.0f ? rtn_code(v[i], a, inv_a) : 0;
+        rtn_vec<V>(v, a, inv_a, mode, code);
         store_codes<V>(p.codes + r * p.ldq + cc, code, nvalid, p.vec_store);
       }
-#pragma unroll 1
-      for (int k = 0; k < 2; ++k) {
-        int8_t* dst = k ? p.sr_codes2 : p.sr_codes;
-        if (!dst) continue;
-        uint64_t z = (k ? p.sr_seed2 : p.sr_seed) +
-                     (uint64_t)((p.row_offset + r) * p.cols + cc + 1) * kGolden;
-#pragma unroll
-        for (int i = 0; i < V; ++i) {
-          code[i] = a > 0.0f ? sr_code(v[i], a, inv_a, mix64(z)) : 0;
-          z += kGolden;
+      if constexpr (kSR >= 1) {
+        const uint64_t lin1 = (uint64_t)((p.row_offset + r) * p.cols + cc + 1);
+        sr_vec<V>(v, a, inv_a, mode, p.sr_seed + lin1 * kGolden, code);
+        store_codes<V>(p.sr_codes + r * p.ldq + cc, code, nvalid, p.vec_store);
+        if constexpr (kSR >= 2) {
+          sr_vec<V>(v, a, inv_a, mode, p.sr_seed2 + lin1 * kGolden, code);
+          store_codes<V>(p.sr_codes2 + r * p.ldq + cc, code, nvalid, p.vec_store);
         }
-        store_codes<V>(dst + r * p.ldq + cc, code, nvalid, p.vec_store);
       }
     }
   }
@@ -237,11 +261,10 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   //      from the staged values (no fp32 residual tile) ----
   auto res = [&](int rb, float (&v)[V]) {
     val(rb, lc, v);
+    int c[V];
+    rtn_vec<V>(v, a, inv_a, mode, c);
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const int c = a > 0.0f ? rtn_code(v[i], a, inv_a) : 0;
-      v[i] = __fsub_rn(v[i], __fmul_rn((float)c, a));  // zero-filled lanes stay 0
-    }
+    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)c[i], a));
   };
   m = 0.0f;
 #pragma unroll 1
@@ -253,6 +276,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   }
   const float ra = block_scale(block_max(m, red));
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
+  const int rmode = round_mode(ra);
   if (threadIdx.x == 0 && p.res_scales) p.res_scales[blk] = ra;
   if (!p.res_codes || !lane_ok) return;
 #pragma unroll 1
@@ -263,13 +287,12 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
     float v[V];
     res(rb, v);
     int code[V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) code[i] = ra > 0.0f ? rtn_code(v[i], ra, inv_ra) : 0;
+    rtn_vec<V>(v, ra, inv_ra, rmode, code);
     store_codes<V>(p.res_codes + r * p.ldq + cc, code, nvalid, p.vec_store);
   }
 }
 
-template <typename T, bool kVec>
+template <typename T, bool kVec, int kSR>
 __global__ void __launch_bounds__(kQuantThreads)
 fbq_quantize_block_kernel(QuantParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -280,8 +303,8 @@ fbq_quantize_block_kernel(QuantParams p) {
   stage_tile<T, kVec>(tile, reinterpret_cast<const T*>(p.x), p.ldx, p.rows, p.cols, r0, c0);
   __syncthreads();
   constexpr int V = Tiling<T>::V;
-  quantize_block<V>(p, bi * gridDim.x + bj, r0, c0, red,
-                    [&](int rb, int cb, float (&v)[V]) { load_vec<T, V>(tile + rb * kBlock + cb, v); });
+  quantize_block<V, kSR>(p, bi * gridDim.x + bj, r0, c0, red,
+                         [&](int rb, int cb, float (&v)[V]) { load_vec<T, V>(tile + rb * kBlock + cb, v); });
 }
 
 // ------------------------------------------------------------------ GLU
@@ -295,7 +318,7 @@ __device__ __noinline__ float silu_grad_ref(float x) {
   return (float)(s * (1.0 + (double)x * (1.0 - s)));
 }
 // Fast fp32 variants for the bf16 training path (a few ulp from the reference).
-__device__ __forceinline__ float sigmoid_fast(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float silu_fast(float x) { return x * sigmoid_fast(x); }
 __device__ __forceinline__ float silu_grad_fast(float x) {
   const float s = sigmoid_fast(x);
@@ -361,7 +384,7 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
     }
   }
   // h = fl(silu(a) * b) (trainsim.cpp:230), quantized like a linear input
-  quantize_block<V>(p, bi * gridDim.x + bj, r0, c0, red, [&](int rb, int cb, float (&v)[V]) {
+  quantize_block<V, 1>(p, bi * gridDim.x + bj, r0, c0, red, [&](int rb, int cb, float (&v)[V]) {
     float vb[V];
     load_vec<T, V>(ta + rb * kBlock + cb, v);
     load_vec<T, V>(tb + rb * kBlock + cb, vb);
@@ -393,6 +416,7 @@ __device__ __forceinline__ void sr_block(int8_t* dst, int64_t ldq, float* scale_
   const float amax = block_max(m, red);
   const float a = block_scale(amax);
   const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
+  const int mode = round_mode(a);
   if (threadIdx.x == 0) *scale_out = a;
   if (cc >= cols) return;
 #pragma unroll 1
@@ -402,13 +426,8 @@ __device__ __forceinline__ void sr_block(int8_t* dst, int64_t ldq, float* scale_
     if (r >= rows) break;
     float v[V];
     val(rb, lc, v);
-    uint64_t z = seed + (uint64_t)((row_offset + r) * cols + cc + 1) * kGolden;
     int code[V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      code[i] = a > 0.0f ? sr_code(v[i], a, inv_a, mix64(z)) : 0;
-      z += kGolden;
-    }
+    sr_vec<V>(v, a, inv_a, mode, seed + (uint64_t)((row_offset + r) * cols + cc + 1) * kGolden, code);
     store_codes<V>(dst + r * ldq + cc, code, V, true);
   }
 }
@@ -534,16 +553,28 @@ static cudaError_t opt_in_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <typename T, bool kVec>
-static cudaError_t launch_k1(const QuantParams& p, dim3 grid, cudaStream_t s) {
+template <typename T, bool kVec, int kSR>
+static cudaError_t launch_k1_sr(const QuantParams& p, dim3 grid, cudaStream_t s) {
   const size_t smem = sizeof(T) * kTileElems;
   static bool ready = false;
   if (!ready) {
-    if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec>, smem)) return e;
+    if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec, kSR>, smem)) return e;
     ready = true;
   }
-  fbq_quantize_block_kernel<T, kVec><<<grid, kQuantThreads, smem, s>>>(p);
+  fbq_quantize_block_kernel<T, kVec, kSR><<<grid, kQuantThreads, smem, s>>>(p);
   return cudaGetLastError();
+}
+template <typename T, bool kVec>
+static cudaError_t launch_k1(QuantParams p, dim3 grid, cudaStream_t s) {
+  // compact the stochastic planes into kSR = 0, 1, 2
+  if (!p.sr_codes && p.sr_codes2) {
+    p.sr_codes = p.sr_codes2;
+    p.sr_seed = p.sr_seed2;
+    p.sr_codes2 = nullptr;
+  }
+  if (p.sr_codes2) return launch_k1_sr<T, kVec, 2>(p, grid, s);
+  if (p.sr_codes) return launch_k1_sr<T, kVec, 1>(p, grid, s);
+  return launch_k1_sr<T, kVec, 0>(p, grid, s);
 }
 
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {

@@ -15,6 +15,10 @@ if what == "gemm":
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     for _ in range(3):
         fbq.fallback_gemm(fa, wq, out=out, exact=False)
+elif what == "rtn32":
+    w = torch.randn(4096, 14336, device="cuda") * 0.02
+    for _ in range(3):
+        fbq.quantize_rtn(w)
 elif what == "quant":
     R, C = 8192, 14336
     x = torch.randn(R, C, device="cuda").to(torch.bfloat16)
