@@ -201,7 +201,7 @@ int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
 /* Rounding probes for exhaustive tests: out_rtn[i] = RTN code of x[i]/a[i]
  * (kernels.cpp:24-40), out_sr[i] = SR code with RNG bits[i] (quant.cpp:69-77). */
 int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
-                         int8_t* out_sr, int64_t n, fbq_stream_t stream);
+                         int8_t* out_sr, int64_t n, int path, fbq_stream_t stream);
 
 /* Performance diagnostics only (not part of the reference API): flags
  * 1 = GEMM epilogue skips its math, 2 = GEMM producer skips the TMA loads,

@@ -42,7 +42,7 @@ _SIGS = {
     "fbq_cuda_gemm_block_products": (cint, [vp, i64, cint, vp, i64, cint, vp, vp, i64, i64, i64,
                                             vp, vp]),
     "fbq_cuda_dequantize": (cint, [vp, i64, vp, vp, vp, vp, i64, i64, vp, i64, vp]),
-    "fbq_cuda_round_probe": (cint, [vp, vp, vp, vp, vp, i64, vp]),
+    "fbq_cuda_round_probe": (cint, [vp, vp, vp, vp, vp, i64, cint, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

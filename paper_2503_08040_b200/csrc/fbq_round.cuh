@@ -108,4 +108,83 @@ __device__ __forceinline__ int sr_code(float x, float a, float inv_a, uint64_t b
   return min(max(ni, -127), 127);
 }
 
+// ------------------------------------------------------------------ vectors
+// Vector fast paths for a block-uniform scale a >= kTinyScale.  Each returns
+// the biased magic words m = fl(t + M) (their low byte / halfword IS the code
+// in two's complement: M's low 22 bits are zero) and a "near" flag: true when
+// some element's fp32 estimate lies within `window` of a rounding boundary,
+// where the estimate cannot decide -- the caller then redoes that vector with
+// the exact scalar functions above (probability ~2^-12 per element).
+//
+// RTN: q = fl(x * inv_a) is within |x/a| * 2^-23 < level * 2^-23 of x/a
+// (|x| <= amax by construction, so |x/a| <= level * (1 + 2^-24) and the clamp
+// is a no-op); d = q - rint(q) is exact.  |d| <= 1/2 - level * 2^-21 proves
+// rint(q) == round_half_even(x/a) with no tie.
+__device__ __forceinline__ float rtn_window(float level) { return 0.5f - level * 0x1p-21f; }
+
+template <int V>
+__device__ __forceinline__ bool rtn_fast_vec(const float (&x)[V], float inv_a, float window,
+                                             uint32_t (&w)[V]) {
+  bool near = false;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const float q = __fmul_rn(x[i], inv_a);
+    const float m = __fadd_rn(q, kMagic);
+    const float d = __fsub_rn(q, __fsub_rn(m, kMagic));
+    near |= fabsf(d) > window;
+    w[i] = __float_as_uint(m);
+  }
+  return near;
+}
+template <int V>
+__device__ __forceinline__ void rtn_exact_vec(const float (&x)[V], float a, float inv_a,
+                                              float level, uint32_t (&w)[V]) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) w[i] = (uint32_t)rtn_code_fast(x[i], a, inv_a, level);
+}
+
+// Top 32 bits of mix64(z) (exact for bits 33..63, the only ones the fast SR
+// path uses): the final z ^ (z >> 31) leaves them unchanged, and only the
+// high word of the second 64-bit product is needed.
+__device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = z ^ (z >> 27);
+  const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+  return __umulhi(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu;
+}
+
+// Stochastic rounding (quant.cpp:69-77):  floor(t) + [frac > 0 && u < frac]
+// == rint(t + 1/2 - u) unless t + 1/2 - u is (within rounding error of) a
+// half-integer -- i.e. u == frac, or frac == 0 with u == 0.  The fp32
+// w = fl(fl(x * inv_a) + (1/2 - u23)) is within 2^-15 of t + 1/2 - u53 (u23:
+// the top 23 RNG bits, exactly 1/2 - u23 = 1.5 - as_float(0x3F800000 | bits));
+// near boundaries (window 2^-13) or |w| > 127.25 (a possible clamp) the vector
+// is redone exactly.  z: the element's splitmix64 counter (seed + lin * golden).
+template <int V>
+__device__ __forceinline__ bool sr_fast_vec(const float (&x)[V], float inv_a, uint64_t z,
+                                            uint32_t (&w)[V]) {
+  bool near = false;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const uint32_t h = mix64_hi(z);
+    const float half_u = __fsub_rn(1.5f, __uint_as_float(0x3F800000u | (h >> 9)));
+    const float t = __fadd_rn(__fmul_rn(x[i], inv_a), half_u);
+    const float m = __fadd_rn(t, kMagic);
+    const float d = __fsub_rn(t, __fsub_rn(m, kMagic));
+    near |= (fabsf(d) > 0.5f - 0x1p-13f) | (fabsf(t) > 127.25f);
+    w[i] = __float_as_uint(m);
+    z += kGolden;
+  }
+  return near;
+}
+template <int V>
+__device__ __forceinline__ void sr_exact_vec(const float (&x)[V], float a, float inv_a, uint64_t z,
+                                             uint32_t (&w)[V]) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    w[i] = (uint32_t)sr_code(x[i], a, inv_a, mix64(z));
+    z += kGolden;
+  }
+}
+
 }  // namespace fbq

@@ -84,40 +84,33 @@ __device__ __forceinline__ float row_max(float v) {
   return v;
 }
 
-// Store V int8 codes: one vector store when the plane is 16-byte aligned and the
-// vector is whole, else element stores (ragged right edge / odd strides).
+// Store V int8 codes given as 32-bit words whose low byte is the code (the
+// magic-biased rounding words or plain ints): PRMT-packed into one vector store
+// when the plane is 16-byte aligned and the vector is whole, else byte stores
+// (ragged right edge / odd strides).
+__device__ __forceinline__ uint32_t pack4_lo8(const uint32_t* w) {
+  return __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+}
 template <int V>
-__device__ __forceinline__ void store_codes(int8_t* p, const int* c, int n, bool vec) {
+__device__ __forceinline__ void store_codes(int8_t* p, const uint32_t* w, int n, bool vec) {
   if (vec && n == V) {
-    if constexpr (V == 4) {
-      uint32_t w = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) w |= (uint32_t)(uint8_t)(int8_t)c[i] << (8 * i);
-      *reinterpret_cast<uint32_t*>(p) = w;
-    } else {
-      uint32_t w0 = 0, w1 = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        w0 |= (uint32_t)(uint8_t)(int8_t)c[i] << (8 * i);
-        w1 |= (uint32_t)(uint8_t)(int8_t)c[i + 4] << (8 * i);
-      }
-      *reinterpret_cast<uint2*>(p) = make_uint2(w0, w1);
-    }
+    if constexpr (V == 4) *reinterpret_cast<uint32_t*>(p) = pack4_lo8(w);
+    else *reinterpret_cast<uint2*>(p) = make_uint2(pack4_lo8(w), pack4_lo8(w + 4));
   } else {
 #pragma unroll
     for (int i = 0; i < V; ++i)
-      if (i < n) p[i] = (int8_t)c[i];
+      if (i < n) p[i] = (int8_t)(uint8_t)w[i];
   }
 }
 
+// V int16 codes from words whose low halfword is the code
 template <int V>
-__device__ __forceinline__ void store_codes16(int16_t* p, const int* c) {
-  uint32_t w[V / 2];
+__device__ __forceinline__ void store_codes16(int16_t* p, const uint32_t* w) {
+  uint32_t o[V / 2];
 #pragma unroll
-  for (int i = 0; i < V / 2; ++i)
-    w[i] = (uint32_t)(uint16_t)(int16_t)c[2 * i] | ((uint32_t)(uint16_t)(int16_t)c[2 * i + 1] << 16);
-  if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
-  else *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  for (int i = 0; i < V / 2; ++i) o[i] = __byte_perm(w[2 * i], w[2 * i + 1], 0x5410);
+  if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = make_uint2(o[0], o[1]);
+  else *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 // ------------------------------------------------------------------ staging
@@ -126,7 +119,8 @@ __device__ __forceinline__ void store_codes16(int16_t* p, const int* c) {
 // smem stores.  kVec requires 16-byte aligned rows and cols % V == 0.
 template <typename T, bool kVec>
 __device__ __forceinline__ void stage_tile(T* __restrict__ s, const T* __restrict__ g, int64_t ld,
-                                           int64_t rows, int64_t cols, int64_t r0, int64_t c0) {
+                                           int64_t rows, int64_t cols, int64_t r0, int64_t c0,
+                                           int sld = kBlock) {
   using Tl = Tiling<T>;
   constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
@@ -140,47 +134,62 @@ __device__ __forceinline__ void stage_tile(T* __restrict__ s, const T* __restric
     }
 #pragma unroll
     for (int ps = 0; ps < NP; ++ps)
-      *reinterpret_cast<uint4*>(s + (lr + ps * RPP) * kBlock + lc) = raw[ps];
+      *reinterpret_cast<uint4*>(s + (lr + ps * RPP) * sld + lc) = raw[ps];
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < kTileElems; i += kQuantThreads) {
       const int rr = i / kBlock, cc = i % kBlock;
       const int64_t r = r0 + rr, c = c0 + cc;
-      s[i] = (r < rows && c < cols) ? g[r * ld + c] : zero_of<T>();
+      s[rr * sld + cc] = (r < rows && c < cols) ? g[r * ld + c] : zero_of<T>();
     }
   }
 }
 
 template <typename T, int V>
 __device__ __forceinline__ void load_vec(const T* s, float (&v)[V]) {
-  const uint4 raw = *reinterpret_cast<const uint4*>(s);
-  const T* e = reinterpret_cast<const T*>(&raw);
+  if constexpr (V * sizeof(T) == 32) {  // 8 floats: two 16-byte loads
+    const float4 x = reinterpret_cast<const float4*>(s)[0], y = reinterpret_cast<const float4*>(s)[1];
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+    const uint4 raw = *reinterpret_cast<const uint4*>(s);
+    const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-  for (int i = 0; i < V; ++i) v[i] = to_f32(e[i]);
+    for (int i = 0; i < V; ++i) v[i] = to_f32(e[i]);
+  }
+}
+template <int V>
+__device__ __forceinline__ void store_f32(float* s, const float (&v)[V]) {
+#pragma unroll
+  for (int j = 0; j < V / 4; ++j)
+    reinterpret_cast<float4*>(s)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
 
 // ------------------------------------------------------------------ K1 core
 // Per-block rounding dispatch, decided once per block (block-uniform): zero
 // scale -> all codes 0; tiny scale -> the reference's double formula (out of
-// line); otherwise the branch-free fp32 path.
+// line); otherwise the fp32 vector fast path with its exact fallback.
+// Outputs are words whose low byte is the code.
 template <int V>
 __device__ __forceinline__ void rtn_vec(const float (&v)[V], float a, float inv_a, int mode,
-                                        int (&code)[V]) {
+                                        uint32_t (&w)[V]) {
   if (mode == 2) {
-#pragma unroll
-    for (int i = 0; i < V; ++i) code[i] = rtn_code_fast(v[i], a, inv_a, 127.0f);
+    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) rtn_exact_vec<V>(v, a, inv_a, 127.0f, w);
   } else {
 #pragma unroll
-    for (int i = 0; i < V; ++i) code[i] = mode == 0 ? 0 : rtn_code_slow(v[i], a, 127.0f);
+    for (int i = 0; i < V; ++i) w[i] = mode == 0 ? 0u : (uint32_t)rtn_code_slow(v[i], a, 127.0f);
   }
 }
 template <int V>
 __device__ __forceinline__ void sr_vec(const float (&v)[V], float a, float inv_a, int mode,
-                                       uint64_t z, int (&code)[V]) {
+                                       uint64_t z, uint32_t (&w)[V]) {
+  if (mode == 2) {
+    if (sr_fast_vec<V>(v, inv_a, z, w)) sr_exact_vec<V>(v, a, inv_a, z, w);
+  } else {
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    code[i] = mode == 0 ? 0 : sr_code(v[i], a, inv_a, mix64(z));
-    z += kGolden;
+    for (int i = 0; i < V; ++i) {
+      w[i] = mode == 0 ? 0u : (uint32_t)sr_code_slow(v[i], a, mix64(z));
+      z += kGolden;
+    }
   }
 }
 __device__ __forceinline__ int round_mode(float a) {
@@ -193,22 +202,27 @@ __device__ __forceinline__ int round_mode(float a) {
 // stochastic context planes and the fallback residual of flagged blocks.
 // kSR is a compile-time count so RTN-only launches carry no RNG code.
 // Entered by all threads of the CTA (it contains CTA barriers).
+// have_m: the caller already holds this thread's partial absmax `m_in` (and
+// the block barrier in block_max publishes the values `val` reads).
 template <int V, int kSR, class Val>
 __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk, int64_t r0,
-                                               int64_t c0, float* red, Val&& val) {
+                                               int64_t c0, float* red, Val&& val,
+                                               bool have_m = false, float m_in = 0.0f) {
   constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
   const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
   const int64_t cc = c0 + lc;
   const bool lane_ok = cc < p.cols;
   const int nvalid = (int)(p.cols - cc < V ? p.cols - cc : V);
   // ---- block absmax -> scale (quant.cpp:27-32) ----
-  float m = 0.0f;
+  float m = m_in;
+  if (!have_m) {
 #pragma unroll 1
-  for (int ps = 0; ps < NP; ++ps) {
-    float v[V];
-    val(lr + ps * RPP, lc, v);
+    for (int ps = 0; ps < NP; ++ps) {
+      float v[V];
+      val(lr + ps * RPP, lc, v);
 #pragma unroll
-    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+      for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+    }
   }
   const float amax = block_max(m, red);
   const float a = block_scale(amax);
@@ -239,7 +253,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
       if (r >= p.rows) break;
       float v[V];
       val(rb, lc, v);
-      int code[V];
+      uint32_t code[V];
       if (p.codes) {
         rtn_vec<V>(v, a, inv_a, mode, code);
         store_codes<V>(p.codes + r * p.ldq + cc, code, nvalid, p.vec_store);
@@ -261,10 +275,10 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   //      from the staged values (no fp32 residual tile) ----
   auto res = [&](int rb, float (&v)[V]) {
     val(rb, lc, v);
-    int c[V];
+    uint32_t c[V];
     rtn_vec<V>(v, a, inv_a, mode, c);
 #pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)c[i], a));
+    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)(int8_t)(uint8_t)c[i], a));
   };
   m = 0.0f;
 #pragma unroll 1
@@ -286,7 +300,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
     if (r >= p.rows) break;
     float v[V];
     res(rb, v);
-    int code[V];
+    uint32_t code[V];
     rtn_vec<V>(v, ra, inv_ra, rmode, code);
     store_codes<V>(p.res_codes + r * p.ldq + cc, code, nvalid, p.vec_store);
   }
@@ -317,8 +331,15 @@ __device__ __noinline__ float silu_grad_ref(float x) {
   const double s = 1.0 / (1.0 + exp(-(double)x));
   return (float)(s * (1.0 + (double)x * (1.0 - s)));
 }
-// Fast fp32 variants for the bf16 training path (a few ulp from the reference).
-__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+// Fast fp32 variants for the bf16 training path (a few ulp from the
+// reference): sigmoid = 1 / (1 + 2^(-x log2 e)) with the MUFU ex2 / rcp
+// approximations (flush-to-zero ex2: for x > 87 the sigmoid is 1 either way).
+__device__ __forceinline__ float sigmoid_fast(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return r;
+}
 __device__ __forceinline__ float silu_fast(float x) { return x * sigmoid_fast(x); }
 __device__ __forceinline__ float silu_grad_fast(float x) {
   const float s = sigmoid_fast(x);
@@ -326,112 +347,91 @@ __device__ __forceinline__ float silu_grad_fast(float x) {
 }
 
 // 1 x 128 row-group RTN shared by the VPR threads of a row (quantize_rtn with
-// GroupGeometry(1, 128), quant.cpp:36-53).
+// GroupGeometry(1, 128), quant.cpp:36-53).  Words' low halfword = the code.
 template <int V, int VPR>
-__device__ __forceinline__ float group_rtn(const float (&x)[V], int (&code)[V], float level) {
+__device__ __forceinline__ float group_rtn(const float (&x)[V], uint32_t (&w)[V], float level) {
   float m = 0.0f;
 #pragma unroll
   for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(x[i]));
   m = row_max<VPR>(m);
   const float s = m > 0.0f ? __fdiv_rn(m, level) : 0.0f;
   const float inv = s > 0.0f ? __frcp_rn(s) : 0.0f;
+  if (s >= kTinyScale) {
+    if (rtn_fast_vec<V>(x, inv, rtn_window(level), w)) rtn_exact_vec<V>(x, s, inv, level, w);
+  } else {
 #pragma unroll
-  for (int i = 0; i < V; ++i) code[i] = s > 0.0f ? rtn_code(x[i], s, inv, level) : 0;
+    for (int i = 0; i < V; ++i) w[i] = s > 0.0f ? (uint32_t)rtn_code_slow(x[i], s, level) : 0u;
+  }
   return s;
 }
 
+// Shared-memory row of the forward tile: [a (128 T) | b (128 T)].  The context
+// pass turns row r into h = fl(silu(a) * b) as 128 fp32 IN PLACE (512 bytes fit
+// in the row; only the VPR threads of that row -- one warp or half-warp --
+// touch it, so a __syncwarp orders their reads before their writes).  h is
+// thus evaluated once and never reaches HBM.
 template <typename T>
 __global__ void __launch_bounds__(kQuantThreads)
 fbq_glu_forward_kernel(GluParams g, QuantParams p) {
-  // raw a and b tiles; h = silu(a) * b is recomputed from them on every pass
   extern __shared__ __align__(16) uint8_t dsm[];
-  T* ta = reinterpret_cast<T*>(dsm);
-  T* tb = ta + kTileElems;
+  constexpr int kRow = 2 * kBlock;                      // T per smem row
+  constexpr int kRowF = kRow * (int)sizeof(T) / 4;      // fp32 per smem row
+  T* tab = reinterpret_cast<T*>(dsm);
+  float* th = reinterpret_cast<float*>(dsm);
   __shared__ float red[kQuantThreads / 32];
   using Tl = Tiling<T>;
   constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
   const T* ab = reinterpret_cast<const T*>(g.ab);
-  stage_tile<T, true>(ta, ab, g.ld_ab, g.rows, g.cols, r0, c0);
-  stage_tile<T, true>(tb, ab + g.cols, g.ld_ab, g.rows, g.cols, r0, c0);
+  stage_tile<T, true>(tab, ab, g.ld_ab, g.rows, g.cols, r0, c0, kRow);
+  stage_tile<T, true>(tab + kBlock, ab + g.cols, g.ld_ab, g.rows, g.cols, r0, c0, kRow);
   __syncthreads();
   const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
   const int64_t cc = c0 + lc;
-  // 10-bit contexts of a and b (trainsim.cpp:240-243) [+ optional h_out]
+  // 10-bit contexts of a and b (trainsim.cpp:240-243), h and its absmax
+  float m = 0.0f;
 #pragma unroll 1
   for (int ps = 0; ps < NP; ++ps) {
     const int rb = lr + ps * RPP;
     const int64_t r = r0 + rb;
     const bool ok = r < g.rows && cc < g.cols;  // cols % 8 == 0: uniform per row group
     float va[V], vb[V];
-    load_vec<T, V>(ta + rb * kBlock + lc, va);
-    load_vec<T, V>(tb + rb * kBlock + lc, vb);
-    int code[V];
+    load_vec<T, V>(tab + rb * kRow + lc, va);
+    load_vec<T, V>(tab + rb * kRow + kBlock + lc, vb);
+    uint32_t code[V];
     float s = group_rtn<V, VPR>(va, code, g.ctx_level);
     if (ok && g.ctx_a) store_codes16<V>(g.ctx_a + r * g.ld_ctx + cc, code);
     if (ok && g.ctx_a_scales && lc == 0) g.ctx_a_scales[r * gcols + bj] = s;
     s = group_rtn<V, VPR>(vb, code, g.ctx_level);
     if (ok && g.ctx_b) store_codes16<V>(g.ctx_b + r * g.ld_ctx + cc, code);
     if (ok && g.ctx_b_scales && lc == 0) g.ctx_b_scales[r * gcols + bj] = s;
-    if (ok && g.h_out) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const float sa = g.exact_math ? silu_ref(va[i]) : silu_fast(va[i]);
-        g.h_out[r * g.ld_h + cc + i] = __fmul_rn(sa, vb[i]);
-      }
-    }
-  }
-  // h = fl(silu(a) * b) (trainsim.cpp:230), quantized like a linear input
-  quantize_block<V, 1>(p, bi * gridDim.x + bj, r0, c0, red, [&](int rb, int cb, float (&v)[V]) {
-    float vb[V];
-    load_vec<T, V>(ta + rb * kBlock + cb, v);
-    load_vec<T, V>(tb + rb * kBlock + cb, vb);
+    // h = fl(silu(a) * b) (trainsim.cpp:230); zero-filled lanes: silu(0) * 0 = 0
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const float sa = g.exact_math ? silu_ref(v[i]) : silu_fast(v[i]);
-      v[i] = __fmul_rn(sa, vb[i]);  // zero-filled lanes: silu(0) * 0 = 0
+      const float sa = g.exact_math ? silu_ref(va[i]) : silu_fast(va[i]);
+      va[i] = __fmul_rn(sa, vb[i]);
+      m = fmaxf(m, fabsf(va[i]));
     }
-  });
-}
-
-// SR-quantize one block whose values come from `val` into `dst` with its own
-// RNG stream (quant.cpp:55-84); writes the block scale.
-template <int V, class Val>
-__device__ __forceinline__ void sr_block(int8_t* dst, int64_t ldq, float* scale_out, uint64_t seed,
-                                         int64_t row_offset, int64_t rows, int64_t cols,
-                                         int64_t r0, int64_t c0, float* red, Val&& val) {
-  constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
-  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
-  const int64_t cc = c0 + lc;
-  float m = 0.0f;
-#pragma unroll 1
-  for (int ps = 0; ps < NP; ++ps) {
-    float v[V];
-    val(lr + ps * RPP, lc, v);
+    if (ok && g.h_out) {
 #pragma unroll
-    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+      for (int i = 0; i < V; ++i) g.h_out[r * g.ld_h + cc + i] = va[i];
+    }
+    __syncwarp();
+    store_f32<V>(th + rb * kRowF + lc, va);
   }
-  const float amax = block_max(m, red);
-  const float a = block_scale(amax);
-  const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
-  const int mode = round_mode(a);
-  if (threadIdx.x == 0) *scale_out = a;
-  if (cc >= cols) return;
-#pragma unroll 1
-  for (int ps = 0; ps < NP; ++ps) {
-    const int rb = lr + ps * RPP;
-    const int64_t r = r0 + rb;
-    if (r >= rows) break;
-    float v[V];
-    val(rb, lc, v);
-    int code[V];
-    sr_vec<V>(v, a, inv_a, mode, seed + (uint64_t)((row_offset + r) * cols + cc + 1) * kGolden, code);
-    store_codes<V>(dst + r * ldq + cc, code, V, true);
-  }
+  // h quantized like a linear input (K1, fused)
+  quantize_block<V, 1>(
+      p, bi * gridDim.x + bj, r0, c0, red,
+      [&](int rb, int cb, float (&v)[V]) { load_vec<float, V>(th + rb * kRowF + cb, v); }, true, m);
 }
 
+// GluCombine backward (trainsim.cpp:248-263) fused with the two dY
+// quantizers: ga = fl(fl(gy * b) * silu'(a)), gb = fl(gy * silu(a)) from the
+// staged dH and 10-bit contexts; one pass for both block absmaxes, one pass
+// stochastic-rounding both into [q(ga) | q(gb)] with their own RNG streams
+// (quant.cpp:55-84).
 template <typename T>
 __global__ void __launch_bounds__(kQuantThreads)
 fbq_glu_backward_kernel(GluBwdParams g) {
@@ -440,8 +440,9 @@ fbq_glu_backward_kernel(GluBwdParams g) {
   int16_t* tca = reinterpret_cast<int16_t*>(tg + kTileElems);
   int16_t* tcb = tca + kTileElems;
   __shared__ float sa_row[kBlock], sb_row[kBlock];
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[kQuantThreads / 32], red2[kQuantThreads / 32];
   constexpr int V = Tiling<T>::V;
+  constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
@@ -454,55 +455,81 @@ fbq_glu_backward_kernel(GluBwdParams g) {
     sb_row[threadIdx.x] = r < g.rows ? g.ctx_b_scales[r * gcols + bj] : 0.0f;
   }
   __syncthreads();
-  // dequantized contexts: fl(code * scale) (quant.cpp:86-104); codes read as
-  // one 16-byte smem vector per 8 values
+  // dequantized contexts: fl(code * scale) (quant.cpp:86-104); a zero scale
+  // has all-zero codes, so no special case is needed
   auto deq = [&](const int16_t* t, float s, int rb, int cb, float (&v)[V]) {
+    int16_t c[V];
+    if constexpr (V == 8) *reinterpret_cast<uint4*>(c) = *reinterpret_cast<const uint4*>(t + rb * kBlock + cb);
+    else *reinterpret_cast<uint2*>(c) = *reinterpret_cast<const uint2*>(t + rb * kBlock + cb);
 #pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = s == 0.0f ? 0.0f : __fmul_rn((float)t[rb * kBlock + cb + i], s);
+    for (int i = 0; i < V; ++i) v[i] = __fmul_rn((float)c[i], s);
   };
-  // ga = fl(fl(gy * b) * silu'(a)),  gb = fl(gy * silu(a))   (trainsim.cpp:256-259)
-  auto ga = [&](int rb, int cb, float (&v)[V]) {
+  auto eval = [&](int rb, int cb, float (&ga)[V], float (&gb)[V]) {
     float a[V], b[V];
-    load_vec<T, V>(tg + rb * kBlock + cb, v);
+    load_vec<T, V>(tg + rb * kBlock + cb, ga);
     deq(tca, sa_row[rb], rb, cb, a);
     deq(tcb, sb_row[rb], rb, cb, b);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const float sg = g.exact_math ? silu_grad_ref(a[i]) : silu_grad_fast(a[i]);
-      v[i] = __fmul_rn(__fmul_rn(v[i], b[i]), sg);
+      const float gy = ga[i];
+      float sg, sl;
+      if (g.exact_math) {
+        sg = silu_grad_ref(a[i]);
+        sl = silu_ref(a[i]);
+      } else {
+        const float sig = sigmoid_fast(a[i]);
+        sg = sig * (1.0f + a[i] * (1.0f - sig));
+        sl = a[i] * sig;
+      }
+      ga[i] = __fmul_rn(__fmul_rn(gy, b[i]), sg);
+      gb[i] = __fmul_rn(gy, sl);
     }
   };
-  auto gb = [&](int rb, int cb, float (&v)[V]) {
-    float a[V];
-    load_vec<T, V>(tg + rb * kBlock + cb, v);
-    deq(tca, sa_row[rb], rb, cb, a);
-#pragma unroll
-    for (int i = 0; i < V; ++i)
-      v[i] = __fmul_rn(v[i], g.exact_math ? silu_ref(a[i]) : silu_fast(a[i]));
-  };
-  if (g.g_out) {
-    constexpr int VPR = kBlock / V, RPP = kQuantThreads / VPR, NP = kBlock / RPP;
-    const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t cc = c0 + lc;
+  float ma = 0.0f, mb = 0.0f;
 #pragma unroll 1
-    for (int ps = 0; ps < NP; ++ps) {
-      const int rb = lr + ps * RPP;
-      const int64_t r = r0 + rb;
-      if (r >= g.rows || c0 + lc >= g.cols) continue;
-      float v[V], w[V];
-      ga(rb, lc, v);
-      gb(rb, lc, w);
+  for (int ps = 0; ps < NP; ++ps) {
+    const int rb = lr + ps * RPP;
+    float va[V], vb[V];
+    eval(rb, lc, va, vb);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      ma = fmaxf(ma, fabsf(va[i]));
+      mb = fmaxf(mb, fabsf(vb[i]));
+    }
+    const int64_t r = r0 + rb;
+    if (g.g_out && r < g.rows && cc < g.cols) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        g.g_out[r * g.cols + c0 + lc + i] = v[i];
-        g.g_out[g.rows * g.cols + r * g.cols + c0 + lc + i] = w[i];
+        g.g_out[r * g.cols + cc + i] = va[i];
+        g.g_out[g.rows * g.cols + r * g.cols + cc + i] = vb[i];
       }
     }
   }
-  sr_block<V>(g.gq, g.ldq, g.gq_scales + bi * (2 * gcols) + bj, g.seed_a, g.row_offset, g.rows,
-              g.cols, r0, c0, red, ga);
-  __syncthreads();
-  sr_block<V>(g.gq + g.cols, g.ldq, g.gq_scales + bi * (2 * gcols) + gcols + bj, g.seed_b,
-              g.row_offset, g.rows, g.cols, r0, c0, red, gb);
+  const float a_s = block_scale(block_max(ma, red));
+  const float b_s = block_scale(block_max(mb, red2));
+  const float inv_a = a_s > 0.0f ? __frcp_rn(a_s) : 0.0f, inv_b = b_s > 0.0f ? __frcp_rn(b_s) : 0.0f;
+  const int mode_a = round_mode(a_s), mode_b = round_mode(b_s);
+  if (threadIdx.x == 0) {
+    g.gq_scales[bi * (2 * gcols) + bj] = a_s;
+    g.gq_scales[bi * (2 * gcols) + gcols + bj] = b_s;
+  }
+  if (cc >= g.cols) return;
+#pragma unroll 1
+  for (int ps = 0; ps < NP; ++ps) {
+    const int rb = lr + ps * RPP;
+    const int64_t r = r0 + rb;
+    if (r >= g.rows) break;
+    float va[V], vb[V];
+    eval(rb, lc, va, vb);
+    const uint64_t lin1 = (uint64_t)((g.row_offset + r) * g.cols + cc + 1);
+    uint32_t code[V];
+    sr_vec<V>(va, a_s, inv_a, mode_a, g.seed_a + lin1 * kGolden, code);
+    store_codes<V>(g.gq + r * g.ldq + cc, code, V, true);
+    sr_vec<V>(vb, b_s, inv_b, mode_b, g.seed_b + lin1 * kGolden, code);
+    store_codes<V>(g.gq + r * g.ldq + g.cols + cc, code, V, true);
+  }
 }
 
 // Delay-threshold controller on device (policy.cpp:97-109, Algorithm 2):
@@ -534,16 +561,43 @@ __global__ void fbq_dequantize_kernel(DequantParams p) {
   }
 }
 
-// Element-wise rounding probes (exhaustive / adversarial tests of rtn_code
-// and sr_code against the reference double formulas).
+// Element-wise rounding probes (exhaustive / adversarial tests against the
+// reference double formulas).  path 0: the scalar rtn_code / sr_code; 1: the
+// vector fast paths the kernels use (rtn_vec / sr_vec, requires |x| <= 127 a;
+// bits[i] is then the splitmix64 COUNTER z, not the mixed bits); 2: the 10-bit
+// context RTN (group_rtn's path, level 511, |x| <= 511 a; out_rtn holds n int16).
 __global__ void fbq_round_probe_kernel(const float* x, const float* a, const uint64_t* bits,
-                                       int8_t* out_rtn, int8_t* out_sr, int64_t n) {
+                                       int8_t* out_rtn, int8_t* out_sr, int64_t n, int path) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float ai = a[i];
-    const float inv = __frcp_rn(ai);
-    if (out_rtn) out_rtn[i] = (int8_t)rtn_code(x[i], ai, inv);
-    if (out_sr) out_sr[i] = (int8_t)sr_code(x[i], ai, inv, bits[i]);
+    const float inv = ai > 0.0f ? __frcp_rn(ai) : 0.0f;
+    if (path == 0) {
+      if (out_rtn) out_rtn[i] = (int8_t)rtn_code(x[i], ai, inv);
+      if (out_sr) out_sr[i] = (int8_t)sr_code(x[i], ai, inv, bits[i]);
+    } else {
+      const float v[1] = {x[i]};
+      uint32_t w[1];
+      if (path == 2) {
+        const float s = ai;
+        if (s >= kTinyScale) {
+          if (rtn_fast_vec<1>(v, inv, rtn_window(511.0f), w)) rtn_exact_vec<1>(v, s, inv, 511.0f, w);
+        } else {
+          w[0] = s > 0.0f ? (uint32_t)rtn_code_slow(v[0], s, 511.0f) : 0u;
+        }
+        reinterpret_cast<int16_t*>(out_rtn)[i] = (int16_t)(uint16_t)w[0];  // int16 output
+        continue;
+      }
+      const int mode = round_mode(ai);
+      if (out_rtn) {
+        rtn_vec<1>(v, ai, inv, mode, w);
+        out_rtn[i] = (int8_t)(uint8_t)w[0];
+      }
+      if (out_sr) {
+        sr_vec<1>(v, ai, inv, mode, bits[i], w);
+        out_sr[i] = (int8_t)(uint8_t)w[0];
+      }
+    }
   }
 }
 
@@ -593,7 +647,7 @@ cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf
   const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
                   (unsigned)((g.rows + kBlock - 1) / kBlock));
   if (bf16) {
-    const size_t smem = 2 * sizeof(__nv_bfloat16) * kTileElems;
+    const size_t smem = 2 * sizeof(__nv_bfloat16) * kTileElems;  // a|b rows, then h (fp32) in place
     if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16>, smem)) return e;
     fbq_glu_forward_kernel<__nv_bfloat16><<<grid, kQuantThreads, smem, s>>>(g, p);
   } else {
@@ -637,11 +691,11 @@ cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_round_probe(const float* x, const float* a, const uint64_t* bits,
-                               int8_t* out_rtn, int8_t* out_sr, int64_t n, cudaStream_t s) {
+                               int8_t* out_rtn, int8_t* out_sr, int64_t n, int path, cudaStream_t s) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  fbq_round_probe_kernel<<<blocks, 256, 0, s>>>(x, a, bits, out_rtn, out_sr, n);
+  fbq_round_probe_kernel<<<blocks, 256, 0, s>>>(x, a, bits, out_rtn, out_sr, n, path);
   return cudaGetLastError();
 }
 

@@ -80,6 +80,6 @@ cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_
                               double r_min, double r_max, double alpha, double* last_rate,
                               cudaStream_t s);
 cudaError_t launch_round_probe(const float* x, const float* a, const uint64_t* bits,
-                               int8_t* out_rtn, int8_t* out_sr, int64_t n, cudaStream_t s);
+                               int8_t* out_rtn, int8_t* out_sr, int64_t n, int path, cudaStream_t s);
 
 }  // namespace fbq

@@ -29,3 +29,15 @@ elif what == "quant":
     for _ in range(2):
         fbq.fallback_quantize(x, theta=4.2)
 torch.cuda.synchronize()
+if what == "mlp":
+    import bench
+    from paper_2503_08040_b200 import linear
+    T = 8192
+    wg, wu, wd = bench.make_weights()
+    mlp = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.bfloat16, mid_dtype=torch.bfloat16, exact=False)
+    x = bench.make_activations(T, bench.D_MODEL, 1000, "cuda", torch.bfloat16)
+    gy = bench.make_grads(T, bench.D_MODEL, 2000, "cuda", torch.bfloat16)
+    mlp.set_thresholds(4.0, 1.0)
+    for i in range(2):
+        mlp.zero_grad(); mlp.forward(x, i); mlp.backward(gy, i); mlp.controller_step()
+    torch.cuda.synchronize()
