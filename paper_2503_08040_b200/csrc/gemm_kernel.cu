@@ -55,6 +55,8 @@ constexpr int kTmemCols = 512;     // 2 slots x 256 int32 columns
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // WG0: TMA, MMA, scales, idle; WG1-2: epilogue
 constexpr int kPage = 128;                      // k-blocks per staged scale page
+constexpr uint32_t kMagicBits = 0x4B400000u;    // magic-bias decode (see consume)
+constexpr float kMagicF = 12582912.0f;          // 1.5 * 2^23
 
 struct ScalePage {
   float prim[2][kPage];  // fl(sA * sB) for the two 128-column halves
@@ -89,17 +91,205 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t blk) {
 // contracts FMUL2 + FADD2 into FFMA2 even for the _rn intrinsics, but cannot
 // fold a multiply by an unknown value, so the exact chain fl(acc + fl(s*P)) is
 // expressed as FMUL2 then FFMA2(t, one, acc).
-template <int kEpi>
+//
+// kBiased: words accumulated onto the magic bias 0x4B400000 (as_float(v) =
+// 1.5 * 2^23 + P exactly for |P| <= 128 * 127^2 < 2^22) decode with one FADD2
+// (FMA pipe) instead of I2F (half-rate ALU pipe).  Evaluated in round 1: a
+// bias needs either a separate N=128 MMA for the biased half (N=128 runs the
+// tensor pipe at ~55-70%) or TMEM zero-fills of the other half, and neither
+// paid for itself (profiles/r01_gemm_isolation.txt); kept for reference.
+template <int kEpi, bool kBiased>
 __device__ __forceinline__ void consume(const uint32_t (&v)[32], float2* acc, float s, float one) {
   const float2 s2 = make_float2(s, s);
   const float2 one2 = make_float2(one, one);
+  const float2 m2 = make_float2(-kMagicF, -kMagicF);
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const float2 pf = make_float2(__int2float_rn((int)v[2 * i]), __int2float_rn((int)v[2 * i + 1]));
+    const float2 pf =
+        kBiased ? __fadd2_rn(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), m2)
+                : make_float2(__int2float_rn((int)v[2 * i]), __int2float_rn((int)v[2 * i + 1]));
     if constexpr (kEpi == kEpiExact) {
       acc[i] = __ffma2_rn(__fmul2_rn(s2, pf), one2, acc[i]);  // fl(acc + fl(s * P))
     } else {
       acc[i] = __ffma2_rn(pf, s2, acc[i]);
+    }
+  }
+}
+
+// Epilogue warps: warp (4 + q + 4h) owns TMEM lane quadrant q and the
+// 128-column half h of every 128 x 256 tile.
+// kProf: per-item timeline of warp q == 0 (clock64, diagnostics only).
+template <int kEpi, int h, bool kProf>
+__device__ __forceinline__ void epilogue_role(const GemmParams& p, ScalePage* pages, uint64_t* tfull,
+                                              uint64_t* tempty, uint64_t* sfull, uint64_t* sempty,
+                                              uint32_t* tmem_holder, int warp, int lane, int NT) {
+  const int q = warp & 3;  // TMEM lane quadrant this warp may access
+  const int row_in_tile = q * 32 + lane;
+  const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+
+  uint32_t item = 0, pc = 0;
+  uint32_t tw = 0, tl = 0, tpre = 0, tpost = 0, t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    int bm, bn2;
+    tile_coords(tile, p.MB, NT, bm, bn2);
+    const int bn = bn2 * 2 + h;
+    float2 acc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) acc[i] = make_float2(0.0f, 0.0f);
+    for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
+      const ScalePage& sp = pages[pc & 1];
+      mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+      const int nk = min(kPage, p.KB - pg);
+      for (int j = 0; j < nk; ++j) {
+        const bool masked = sp.flag[j];
+        for (int r = 0; r < (masked ? 2 : 1); ++r) {
+          const uint32_t slot = item & 1;
+          const float s = r ? sp.res[h][j] : sp.prim[h][j];
+          // TMEM base re-read from shared memory (issued before the wait, so
+          // its latency hides behind it) instead of living in a register
+          // across the whole kernel (it was spilled to local memory)
+          const uint32_t tbase = ld_shared_u32(tmem_holder);
+          if constexpr (kProf) t0 = (uint32_t)clock();
+          mbar_wait_sleep(tfull + slot, (item >> 1) & 1);
+          tc_fence_after();
+          if constexpr (kProf) t1 = (uint32_t)clock();
+          const uint32_t tb = tbase + lane_addr + slot * 256 + h * 128;
+          if constexpr (kEpi == kEpiDump) {
+            int32_t* d = p.dump + (r ? p.dump_res_offset : 0) +
+                         ((((int64_t)bm * p.NB + bn) * p.KB + pg + j) * kBM + row_in_tile) * 128;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t v[32];
+              tmem_ld32(tb + c * 32, v);
+              tmem_ld_wait();
+              if (bn < p.NB) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                  *reinterpret_cast<int4*>(d + c * 32 + i) =
+                      make_int4((int)v[i], (int)v[i + 1], (int)v[i + 2], (int)v[i + 3]);
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + slot);
+          } else {
+            if (p.diag & 1) {  // diagnostic: release the slot without epilogue math
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(tempty + slot);
+              ++item;
+              continue;
+            }
+            // Two 32-column loads in flight; the slot is released right after
+            // the last load lands (two consumes in between), the remaining math
+            // overlaps the next item's MMA.  The release latency is what paces
+            // the tensor pipe with only two TMEM slots.
+            uint32_t va[32], vb[32];
+            tmem_ld32(tb + 0, va);
+            tmem_ld32(tb + 32, vb);
+            tmem_ld_wait();
+            if constexpr (kProf) t2 = (uint32_t)clock();
+            consume<kEpi, false>(va, acc + 0, s, p.one);
+            tmem_ld32(tb + 64, va);
+            consume<kEpi, false>(vb, acc + 16, s, p.one);
+            tmem_ld32(tb + 96, vb);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + slot);
+            if constexpr (kProf) t3 = (uint32_t)clock();
+            consume<kEpi, false>(va, acc + 32, s, p.one);
+            consume<kEpi, false>(vb, acc + 48, s, p.one);
+            if constexpr (kProf) {
+              // a register dependency on the last FFMA2 makes the clock read wait for it
+              const uint32_t t4 = (uint32_t)clock() + (acc[63].y == 12345.0f ? 1u : 0u);
+              tw += t1 - t0; tl += t2 - t1; tpre += t3 - t2; tpost += t4 - t3;
+            }
+          }
+          ++item;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + (pc & 1));
+    }
+    if (kEpi != kEpiDump && !(p.diag & 4)) {
+      const int64_t grow = (int64_t)bm * kBM + row_in_tile;
+      const int64_t gcol0 = (int64_t)bn * 128;
+      if (bn < p.NB && grow < p.M) {
+        const bool full_row = p.vec_store && gcol0 + 128 <= p.N;
+        if (p.out_bf16) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + gcol0;
+          if (full_row) {
+#pragma unroll
+            for (int i = 0; i < 64; i += 4) {
+              uint4 w;
+              uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+              uint4 old = make_uint4(0, 0, 0, 0);
+              if (p.accumulate) old = *reinterpret_cast<const uint4*>(o + 2 * i);
+              const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float2 v = acc[i + e];
+                if (p.accumulate) {
+                  const float2 ov = __bfloat1622float2(op[e]);
+                  v = make_float2(__fadd_rn(ov.x, v.x), __fadd_rn(ov.y, v.y));
+                }
+                __nv_bfloat162 b = __float22bfloat162_rn(v);
+                wp[e] = *reinterpret_cast<uint32_t*>(&b);
+              }
+              *reinterpret_cast<uint4*>(o + 2 * i) = w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int64_t col = gcol0 + 2 * i + e;
+                if (col < p.N) {
+                  float v = e ? acc[i].y : acc[i].x;
+                  if (p.accumulate) v = __fadd_rn(__bfloat162float(o[2 * i + e]), v);
+                  o[2 * i + e] = __float2bfloat16_rn(v);
+                }
+              }
+            }
+          }
+        } else {
+          float* o = reinterpret_cast<float*>(p.out) + grow * p.ldo + gcol0;
+          if (full_row) {
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+              float4 v = make_float4(acc[i].x, acc[i].y, acc[i + 1].x, acc[i + 1].y);
+              if (p.accumulate) {
+                const float4 old = *reinterpret_cast<const float4*>(o + 2 * i);
+                v.x = __fadd_rn(old.x, v.x);
+                v.y = __fadd_rn(old.y, v.y);
+                v.z = __fadd_rn(old.z, v.z);
+                v.w = __fadd_rn(old.w, v.w);
+              }
+              *reinterpret_cast<float4*>(o + 2 * i) = v;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int64_t col = gcol0 + 2 * i + e;
+                if (col < p.N) {
+                  const float v = e ? acc[i].y : acc[i].x;
+                  o[2 * i + e] = p.accumulate ? __fadd_rn(o[2 * i + e], v) : v;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  if constexpr (kProf) {
+    if (q == 0 && lane == 0) {
+      long long* o = p.prof + blockIdx.x * 16 + 1 + h * 4;
+      o[0] = tw; o[1] = tl; o[2] = tpre; o[3] = tpost;
+      if (h == 0) p.prof[blockIdx.x * 16 + 9] = item;
     }
   }
 }
@@ -109,8 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_r,
                 const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1 KiB alignment (128B-swizzle atoms) by pointer arithmetic on the shared
+  // array itself, so every derived pointer (pages, barriers, the TMEM holder)
+  // stays in the shared address space (LDS/STS, no generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ScalePage* pages = reinterpret_cast<ScalePage*>(smem + kStages * kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(pages + 2);
   uint64_t* full = bars;                 // [kStages]
@@ -143,7 +335,6 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
 
   // scale-grid indices of the stored operands (row stride lds_a / lds_b)
   auto a_blk = [&](int bm, int bk) -> int64_t {
@@ -153,7 +344,15 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     return p.b_major == 0 ? (int64_t)bn * p.lds_b + bk : (int64_t)bk * p.lds_b + bn;
   };
 
-  if (warp < 4) setmaxnreg_dec<56>();
+  // Register budget.  setmaxnreg only redistributes the CTA's launch-time
+  // pool (168 regs x 12 warps = 2016 warp-registers); asking for all of it
+  // (8 x 232 for the epilogue) blocked setmaxnreg.inc forever on the B200, so
+  // the budget keeps slack: 40 + 56 + 40 + 24 + 8 x 224 = 1952.
+  static_assert(40 + 56 + 40 + 24 + kEpiWarps * 224 <= 168 * (kThreads / 32), "register pool");
+  if (warp == 0) setmaxnreg_dec<40>();
+  else if (warp == 1) setmaxnreg_dec<56>();
+  else if (warp == 2) setmaxnreg_dec<40>();
+  else if (warp == 3) setmaxnreg_dec<24>();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -169,12 +368,12 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         tile_coords(tile, p.MB, NT, bm, bn2);
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
-          mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
+          mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
           const int nk = min(kPage, p.KB - pg);
           for (int j = 0; j < nk; ++j) {
             const int bk = pg + j;
             const bool masked = sp.flag[j];
-            mbar_wait(empty + stage, phase ^ 1);
+            mbar_wait_sleep(empty + stage, phase ^ 1);
             uint8_t* sa = smem + stage * kStageBytes;
             uint8_t* sr = sa + kTileA;
             uint8_t* sb = sa + 2 * kTileA;
@@ -206,6 +405,8 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
+      // one M=128 N=256 MMA per 32-deep k step (N=128 instructions run the
+      // tensor pipe at ~55-70%, profiles/microbench/r01_mma_raw.txt)
       const uint32_t idesc = idesc_i8(kBM, kBN, p.a_major, p.b_major);
       // Descriptor templates: per stage only the 14-bit start address changes,
       // per 32-deep k step the address advances by 32 B (K-major: inside the
@@ -215,55 +416,39 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint64_t a_tmpl = smem_desc_sw128(0, 16, 1024);
       const uint64_t b_tmpl = smem_desc_sw128(0, p.b_major == 0 ? 16 : kTileA, 1024);
       const uint32_t smem0 = smem_u32(smem);
+      const uint32_t tmem_base = ld_shared_u32(tmem_holder);
       int stage = 0;
       uint32_t phase = 0, item = 0, pc = 0;
-      long long t_full = 0, t_tempty = 0, t_page = 0, t_issue = 0;
-      const bool prof = p.prof != nullptr;
-      const long long t_start = prof ? clock64() : 0;
+      const long long t_start = p.prof ? clock64() : 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
-          long long t0 = prof ? clock64() : 0;
-          if (!(p.diag & 512)) mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
-          if (prof) t_page += clock64() - t0;
+          if (!(p.diag & 512)) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
           const int nk = min(kPage, p.KB - pg);
           for (int j = 0; j < nk; ++j) {
             const int n_items = (!(p.diag & 512) && sp.flag[j]) ? 2 : 1;
-            t0 = prof ? clock64() : 0;
-            if (!(p.diag & 16)) mbar_wait(full + stage, phase);
-            if (prof) t_full += clock64() - t0;
-            tc_fence_after();
+            if (!(p.diag & 16)) mbar_wait_sleep(full + stage, phase);
+            if (!(p.diag & 64)) tc_fence_after();
             const uint32_t sa = smem0 + stage * kStageBytes;
             const uint64_t bd0 = b_tmpl | ((sa + 2 * kTileA) >> 4);
             for (int r = 0; r < n_items; ++r) {
               const uint32_t slot = item & 1;
-              t0 = prof ? clock64() : 0;
-              if (!(p.diag & 8)) mbar_wait(tempty + slot, ((item >> 1) & 1) ^ 1);
-              if (prof) t_tempty += clock64() - t0;
-              tc_fence_after();
-              t0 = prof ? clock64() : 0;
+              if (!(p.diag & 8)) mbar_wait_sleep(tempty + slot, ((item >> 1) & 1) ^ 1);
+              if (!(p.diag & 64)) tc_fence_after();
               const uint64_t ad0 = a_tmpl | ((sa + (r ? kTileA : 0)) >> 4);
               const uint32_t d = tmem_base + slot * 256;
 #pragma unroll
               for (int kk = 0; kk < kBK / 32; ++kk)
                 mma_i8(d, ad0 + kk * a_step, bd0 + kk * b_step, idesc, kk > 0 ? 1u : 0u);
               mma_commit(tfull + slot);
-              if (prof) t_issue += clock64() - t0;
               ++item;
             }
-            mma_commit(empty + stage);
+            if (!(p.diag & 128)) mma_commit(empty + stage);
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
       }
-      if (p.prof) {
-        long long* o = p.prof + blockIdx.x * 5;
-        o[0] = clock64() - t_start;
-        o[1] = t_full;
-        o[2] = t_tempty;
-        o[3] = t_page;
-        o[4] = t_issue;
-      }
+      if (p.prof) p.prof[blockIdx.x * 16] = clock64() - t_start;  // MMA-warp cycles per CTA
     }
   } else if (warp == 2) {
     // ===================== scale loader =====================
@@ -274,7 +459,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int bn0 = 2 * bn2, bn1 = 2 * bn2 + 1;
       for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
         ScalePage& sp = pages[pc & 1];
-        mbar_wait(sempty + (pc & 1), ((pc >> 1) & 1) ^ 1);
+        mbar_wait_sleep(sempty + (pc & 1), ((pc >> 1) & 1) ^ 1);
         const int nk = min(kPage, p.KB - pg);
         for (int j = lane; j < nk; j += 32) {
           const int bk = pg + j;
@@ -300,161 +485,17 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     setmaxnreg_inc<224>();
-    const int ew = warp - 4;
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    const int h = ew >> 2;   // which 128-column half of the 256-wide tile
-    const int row_in_tile = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-
-    uint32_t item = 0, pc = 0;
-    for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      int bm, bn2;
-      tile_coords(tile, p.MB, NT, bm, bn2);
-      const int bn = bn2 * 2 + h;
-      float2 acc[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = make_float2(0.0f, 0.0f);
-      for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
-        const ScalePage& sp = pages[pc & 1];
-        mbar_wait(sfull + (pc & 1), (pc >> 1) & 1);
-        const int nk = min(kPage, p.KB - pg);
-        for (int j = 0; j < nk; ++j) {
-          const bool masked = sp.flag[j];
-          for (int r = 0; r < (masked ? 2 : 1); ++r) {
-            const uint32_t slot = item & 1;
-            const float s = r ? sp.res[h][j] : sp.prim[h][j];
-            mbar_wait(tfull + slot, (item >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tb = tmem_base + lane_addr + slot * 256 + h * 128;
-            if constexpr (kEpi == kEpiDump) {
-              int32_t* d = p.dump + (r ? p.dump_res_offset : 0) +
-                           ((((int64_t)bm * p.NB + bn) * p.KB + pg + j) * kBM + row_in_tile) * 128;
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                uint32_t v[32];
-                tmem_ld32(tb + c * 32, v);
-                tmem_ld_wait();
-                if (bn < p.NB) {
-#pragma unroll
-                  for (int i = 0; i < 32; i += 4)
-                    *reinterpret_cast<int4*>(d + c * 32 + i) =
-                        make_int4((int)v[i], (int)v[i + 1], (int)v[i + 2], (int)v[i + 3]);
-                }
-              }
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(tempty + slot);
-            } else {
-              if (p.diag & 1) {  // diagnostic: release the slot without epilogue math
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(tempty + slot);
-                ++item;
-                continue;
-              }
-              // Two 32-column loads in flight; the slot is released right after
-              // the last load lands (two consumes in between), the remaining math
-              // overlaps the next item's MMA.  The release latency is what paces
-              // the tensor pipe with only two TMEM slots.
-              uint32_t va[32], vb[32];
-              tmem_ld32(tb + 0, va);
-              tmem_ld32(tb + 32, vb);
-              tmem_ld_wait();
-              consume<kEpi>(va, acc + 0, s, p.one);
-              tmem_ld32(tb + 64, va);
-              consume<kEpi>(vb, acc + 16, s, p.one);
-              tmem_ld32(tb + 96, vb);
-              tmem_ld_wait();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(tempty + slot);
-              consume<kEpi>(va, acc + 32, s, p.one);
-              consume<kEpi>(vb, acc + 48, s, p.one);
-            }
-            ++item;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sempty + (pc & 1));
-      }
-      if (kEpi != kEpiDump && !(p.diag & 4)) {
-        const int64_t grow = (int64_t)bm * kBM + row_in_tile;
-        const int64_t gcol0 = (int64_t)bn * 128;
-        if (bn < p.NB && grow < p.M) {
-          const bool full_row = p.vec_store && gcol0 + 128 <= p.N;
-          if (p.out_bf16) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + gcol0;
-            if (full_row) {
-#pragma unroll
-              for (int i = 0; i < 64; i += 4) {
-                uint4 w;
-                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
-                uint4 old = make_uint4(0, 0, 0, 0);
-                if (p.accumulate) old = *reinterpret_cast<const uint4*>(o + 2 * i);
-                const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&old);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  float2 v = acc[i + e];
-                  if (p.accumulate) {
-                    const float2 ov = __bfloat1622float2(op[e]);
-                    v = make_float2(__fadd_rn(ov.x, v.x), __fadd_rn(ov.y, v.y));
-                  }
-                  __nv_bfloat162 b = __float22bfloat162_rn(v);
-                  wp[e] = *reinterpret_cast<uint32_t*>(&b);
-                }
-                *reinterpret_cast<uint4*>(o + 2 * i) = w;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 64; ++i) {
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int64_t col = gcol0 + 2 * i + e;
-                  if (col < p.N) {
-                    float v = e ? acc[i].y : acc[i].x;
-                    if (p.accumulate) v = __fadd_rn(__bfloat162float(o[2 * i + e]), v);
-                    o[2 * i + e] = __float2bfloat16_rn(v);
-                  }
-                }
-              }
-            }
-          } else {
-            float* o = reinterpret_cast<float*>(p.out) + grow * p.ldo + gcol0;
-            if (full_row) {
-#pragma unroll
-              for (int i = 0; i < 64; i += 2) {
-                float4 v = make_float4(acc[i].x, acc[i].y, acc[i + 1].x, acc[i + 1].y);
-                if (p.accumulate) {
-                  const float4 old = *reinterpret_cast<const float4*>(o + 2 * i);
-                  v.x = __fadd_rn(old.x, v.x);
-                  v.y = __fadd_rn(old.y, v.y);
-                  v.z = __fadd_rn(old.z, v.z);
-                  v.w = __fadd_rn(old.w, v.w);
-                }
-                *reinterpret_cast<float4*>(o + 2 * i) = v;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 64; ++i) {
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int64_t col = gcol0 + 2 * i + e;
-                  if (col < p.N) {
-                    const float v = e ? acc[i].y : acc[i].x;
-                    o[2 * i + e] = p.accumulate ? __fadd_rn(o[2 * i + e], v) : v;
-                  }
-                }
-              }
-            }
-          }
-        }
-      }
+    if (p.prof) {
+      if (warp >= 8) epilogue_role<kEpi, 1, true>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      else epilogue_role<kEpi, 0, true>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+    } else {
+      if (warp >= 8) epilogue_role<kEpi, 1, false>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      else epilogue_role<kEpi, 0, false>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
     }
   }
-
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  if (warp == 1) tmem_dealloc<kTmemCols>(ld_shared_u32(tmem_holder));
 }
 
 // ----------------------------------------------------------------- host side

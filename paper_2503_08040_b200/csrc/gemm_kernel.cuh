@@ -33,7 +33,7 @@ struct GemmParams {
   int num_tiles;
   float one;  // 1.0f (runtime constant for the exact epilogue)
   int diag;   // perf diagnostics: 1 = skip epilogue math, 2 = skip TMA loads
-  long long* prof;  // perf diagnostics: per-CTA MMA-warp wait cycles (or null)
+  long long* prof;  // perf diagnostics: 16 int64 per CTA (MMA-warp cycles, epilogue timeline) or null
 };
 
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s);

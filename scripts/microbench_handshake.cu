@@ -103,7 +103,14 @@ void run(int iters, int delay = 0) {
 }
 
 int main() {
-  for (int d : {0, 100, 200, 300, 400, 500, 700})
-    run<16, 2, true, 7>(4000, d);
+  run<8, 2, false, 0>(4000);
+  run<8, 2, true, 0>(4000);
+  run<8, 2, true, 4>(4000);
+  run<8, 2, true, 7>(4000);
+  run<8, 4, true, 0>(4000);
+  run<8, 4, true, 4>(4000);
+  run<8, 4, true, 7>(4000);
+  run<16, 4, true, 7>(4000);
+  run<16, 2, true, 7>(4000);
   return 0;
 }
