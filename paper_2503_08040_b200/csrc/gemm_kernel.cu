@@ -356,10 +356,15 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      tma_prefetch(&map_a);
-      tma_prefetch(&map_b);
-      if (has_res) tma_prefetch(&map_r);
+    // The whole warp walks the schedule (waits included) and lane 0 issues: a
+    // warp whose lanes 1-31 sit in the final __syncthreads while lane 0 loops
+    // is diverged, and the divergent path steals the issuing lane's slots.
+    {
+      if (lane == 0) {
+        tma_prefetch(&map_a);
+        tma_prefetch(&map_b);
+        if (has_res) tma_prefetch(&map_r);
+      }
       const uint64_t pol = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0, pc = 0;
@@ -377,34 +382,36 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             uint8_t* sa = smem + stage * kStageBytes;
             uint8_t* sr = sa + kTileA;
             uint8_t* sb = sa + 2 * kTileA;
-            if (p.diag & 2) {  // diagnostic: no operand traffic
-              mbar_arrive(full + stage);
-              if (++stage == kStages) { stage = 0; phase ^= 1; }
-              continue;
+            if (lane == 0) {
+              if (p.diag & 2) {  // diagnostic: no operand traffic
+                mbar_arrive(full + stage);
+              } else {
+                mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
+                const int k0 = bk * kBK, m0 = bm * kBM, n0 = bn2 * kBN;
+                if (p.a_major == 0) {
+                  tma_load_2d(sa, &map_a, full + stage, k0, m0, pol);
+                  if (masked) tma_load_2d(sr, &map_r, full + stage, k0, m0, pol);
+                } else {
+                  tma_load_2d(sa, &map_a, full + stage, m0, k0, pol);
+                  if (masked) tma_load_2d(sr, &map_r, full + stage, m0, k0, pol);
+                }
+                if (p.b_major == 0) {
+                  tma_load_2d(sb, &map_b, full + stage, k0, n0, pol);
+                } else {
+                  tma_load_2d(sb, &map_b, full + stage, n0, k0, pol);
+                  tma_load_2d(sb + kTileA, &map_b, full + stage, n0 + 128, k0, pol);
+                }
+              }
             }
-            mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
-            const int k0 = bk * kBK, m0 = bm * kBM, n0 = bn2 * kBN;
-            if (p.a_major == 0) {
-              tma_load_2d(sa, &map_a, full + stage, k0, m0, pol);
-              if (masked) tma_load_2d(sr, &map_r, full + stage, k0, m0, pol);
-            } else {
-              tma_load_2d(sa, &map_a, full + stage, m0, k0, pol);
-              if (masked) tma_load_2d(sr, &map_r, full + stage, m0, k0, pol);
-            }
-            if (p.b_major == 0) {
-              tma_load_2d(sb, &map_b, full + stage, k0, n0, pol);
-            } else {
-              tma_load_2d(sb, &map_b, full + stage, n0, k0, pol);
-              tma_load_2d(sb + kTileA, &map_b, full + stage, n0 + 128, k0, pol);
-            }
+            __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (whole warp walks, lane 0 issues) =====================
+    {
       // one M=128 N=256 MMA per 32-deep k step (N=128 instructions run the
       // tensor pipe at ~55-70%, profiles/microbench/r01_mma_raw.txt)
       const uint32_t idesc = idesc_i8(kBM, kBN, p.a_major, p.b_major);
@@ -437,18 +444,22 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
               if (!(p.diag & 64)) tc_fence_after();
               const uint64_t ad0 = a_tmpl | ((sa + (r ? kTileA : 0)) >> 4);
               const uint32_t d = tmem_base + slot * 256;
+              if (lane == 0) {
 #pragma unroll
-              for (int kk = 0; kk < kBK / 32; ++kk)
-                mma_i8(d, ad0 + kk * a_step, bd0 + kk * b_step, idesc, kk > 0 ? 1u : 0u);
-              mma_commit(tfull + slot);
+                for (int kk = 0; kk < kBK / 32; ++kk)
+                  mma_i8(d, ad0 + kk * a_step, bd0 + kk * b_step, idesc, kk > 0 ? 1u : 0u);
+                mma_commit(tfull + slot);
+              }
+              __syncwarp();
               ++item;
             }
-            if (!(p.diag & 128)) mma_commit(empty + stage);
+            if (!(p.diag & 128) && lane == 0) mma_commit(empty + stage);
+            __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
       }
-      if (p.prof) p.prof[blockIdx.x * 16] = clock64() - t_start;  // MMA-warp cycles per CTA
+      if (p.prof && lane == 0) p.prof[blockIdx.x * 16] = clock64() - t_start;  // MMA-warp cycles per CTA
     }
   } else if (warp == 2) {
     // ===================== scale loader =====================

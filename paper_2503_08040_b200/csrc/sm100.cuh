@@ -56,6 +56,27 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
+// Polling wait with an exponential __nanosleep backoff between probes: keeps
+// waiting warps off the shared-memory pipe the tensor core reads operands from.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -188,9 +209,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// Arrive on an mbarrier given by its shared::cluster address (possibly in the
+// peer CTA).  Default .release.cta semantics: a .cluster-scope release makes
+// ptxas emit MEMBAR.ALL.GPU + CCTL.IVALL, which waits for every outstanding
+// global store of the thread (~thousands of cycles on the TMEM-slot release
+// path); the tcgen05 before/after_thread_sync fences order the TMEM accesses.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem) {

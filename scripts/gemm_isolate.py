@@ -11,6 +11,8 @@ lib.fbq_debug_set_gemm_diag.argtypes = [fbq.K.cint]
 lib.fbq_debug_set_gemm_prof.argtypes = [fbq.K.vp]
 M, N, K = 8192, 14336, 4096
 x = torch.randn(M, K, device="cuda"); w = torch.randn(N, K, device="cuda") * 0.02
+if os.environ.get("ZERO_DATA"):  # low-power operands: every code is +-1 (power-throttling probe)
+    x = torch.ones(M, K, device="cuda"); w = torch.ones(N, K, device="cuda")
 wq = fbq.transpose(fbq.quantize_rtn(w)); qa = fbq.quantize_rtn(x)
 out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
 prof = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
@@ -27,8 +29,13 @@ def run(d):
     prof.zero_(); lib.fbq_debug_set_gemm_prof(prof.data_ptr())
     fbq.block_quant_gemm(qa, wq, out=out, exact=False); torch.cuda.synchronize()
     lib.fbq_debug_set_gemm_prof(None)
-    cyc = prof.view(148, 16)[:, 0].double().mean().item() / items
-    print(f"diag={d:4d}: {t*1e3:.3f} ms {2*M*N*K/t/1e12:6.0f} TOPS  MMA-warp cycles/item {cyc:6.0f} ({512/cyc*100:.0f}% of tensor peak)", flush=True)
-for d in [1 | 256, 1 | 2 | 256, 1 | 16 | 256, 1 | 8 | 256, 1 | 4 | 256, 1 | 2 | 4 | 256, 287, 287 | 64]:
+    pr = prof.view(148, 16)
+    n = int((pr[:, 0] > 0).sum().item())  # MMA threads that recorded (one per CTA pair)
+    pr = pr[:n].double().mean(0).tolist()
+    it = pr[4] if pr[4] > 0 else items  # items per MMA thread (k-blocks + residual items)
+    print(f"diag={d:4d}: {t*1e3:.3f} ms {2*M*N*K/t/1e12:6.0f} TOPS  MMA-warp cycles/item {pr[0]/it:6.0f} "
+          f"(waits: full {pr[1]/it:5.0f} tempty {pr[2]/it:5.0f} rfull {pr[3]/it:5.0f}; {512/(pr[0]/it)*100:.0f}% of tensor peak)", flush=True)
+diags = [int(a) for a in sys.argv[1:]] or [1 | 256, 1 | 2 | 256, 1 | 16 | 256, 1 | 8 | 256, 1 | 4 | 256, 1 | 2 | 4 | 256, 287, 287 | 64]
+for d in diags:
     run(d)
 lib.fbq_debug_set_gemm_diag(0)

@@ -219,3 +219,22 @@ def test_dequantize(F, orc):
     assert np.array_equal(host(F.dequantize(fa.primary)), orc.dequantize(c, s))
     want = orc.dequantize_fallback(c, s, mask, rc, rs)
     assert np.array_equal(host(F.dequantize_fallback(fa)).view(np.int32), want.view(np.int32))
+
+
+def test_gemm_many_tiles_odd_pairs(F, orc):
+    """Persistent CTA-pair schedule: several pair tiles per cluster, an odd
+    number of block rows (the last pair's second CTA is out of range), two
+    scale pages along K, fallback blocks on both CTAs of a pair and on one."""
+    m, n, k = 1152, 640, 4608
+    a, b, mask = _quant_pair(orc, m, n, k, seed=41, rate=0.15)
+    w = np.ascontiguousarray(b.T)
+    wq = F.quantize_rtn(dev(w))
+    wc, ws = orc.quantize_rtn(w)
+    bc, bs = orc.transpose_qt(wc, ws)
+    fa = F.fallback_quantize(dev(a), dev(mask))
+    y = F.fallback_gemm(fa, F.transpose(wq))
+    ac, as_, rc, rs = orc.fallback_quantize(a, mask)
+    want = orc.block_gemm(ac, as_, bc, bs, mask=mask, res_codes=rc, res_scales=rs)
+    assert np.array_equal(host(y).view(np.int32), want.view(np.int32))
+    y2 = F.fallback_gemm(fa, F.transpose(wq), exact=False)
+    assert rel_fro(host(y2), want) <= FMA_TOL
