@@ -212,6 +212,9 @@ void fbq_debug_set_gemm_diag(int flags);
 /* device buffer of 5 x num_SMs int64 receiving, per CTA, the MMA warp's total,
  * operand-wait, TMEM-slot-wait, scale-page-wait and MMA-issue cycles (null disables). */
 void fbq_debug_set_gemm_prof(long long* dev_buf);
+/* Quantizer diagnostics: 1 = use the one-block-per-CTA K1 instead of the
+ * persistent TMA-pipelined K1 (A/B timing; results are identical). */
+void fbq_debug_set_quant_diag(int flags);
 
 /* ---- host entry points (reference value semantics; host buffers) --------
  * A fallback-quantized linear layer + SwiGLU MLP driver mirroring

@@ -40,6 +40,7 @@ const char* fbq_version(void) { return "fbq-b200 0.1 (sm_100a)"; }
 void fbq_debug_set_gemm_diag(int flags) { g_gemm_diag = flags; }
 /* device buffer of 5 x num_SMs int64: MMA-warp total / full-wait / tmem-wait / page-wait / issue cycles */
 void fbq_debug_set_gemm_prof(long long* dev_buf) { g_gemm_prof = dev_buf; }
+void fbq_debug_set_quant_diag(int flags) { fbq::g_quant_diag = flags; }
 int fbq_block_side(void) { return 128; }
 
 int fbq_malloc(void** ptr, size_t bytes) {

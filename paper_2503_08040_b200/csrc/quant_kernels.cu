@@ -28,8 +28,11 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include <cuda.h>
+
 #include "fbq_round.cuh"
 #include "quant_kernels.cuh"
+#include "sm100.cuh"
 
 namespace fbq {
 
@@ -319,6 +322,312 @@ fbq_quantize_block_kernel(QuantParams p) {
   constexpr int V = Tiling<T>::V;
   quantize_block<V, kSR>(p, bi * gridDim.x + bj, r0, c0, red,
                          [&](int rb, int cb, float (&v)[V]) { load_vec<T, V>(tile + rb * kBlock + cb, v); });
+}
+
+// ------------------------------------------------------------------ K1, register-resident
+// The RTN / fallback-detect path (no stochastic planes): every thread keeps its
+// 64 values of the block in registers as loaded (32 registers of packed bf16 or
+// 64 of fp32) -- no shared-memory staging, one unpack per pass, row pointers
+// hoisted out of the pass loop.  The smem-staged K1 above spends ~22
+// instructions per element (issue-bound at ~52 % of HBM on 8192 x 14336 bf16);
+// this one ~8.
+template <typename T>
+__device__ __forceinline__ void unpack(const uint4& raw, float (&v)[16 / sizeof(T)]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  } else {
+    v[0] = __uint_as_float(raw.x);
+    v[1] = __uint_as_float(raw.y);
+    v[2] = __uint_as_float(raw.z);
+    v[3] = __uint_as_float(raw.w);
+  }
+}
+// exact RTN of one vector (out of line: taken with probability ~2^-12 per element)
+template <typename T>
+__device__ __noinline__ uint2 rtn_exact_raw(uint4 raw, float a, float inv_a, float level) {
+  constexpr int V = 16 / sizeof(T);
+  float v[V];
+  unpack<T>(raw, v);
+  uint32_t w[V];
+  rtn_exact_vec<V>(v, a, inv_a, level, w);
+  uint2 out;
+  out.x = pack4_lo8(w);
+  out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
+  return out;
+}
+template <typename T>
+__device__ __noinline__ uint2 rtn_slow_raw(uint4 raw, float a, float level) {
+  constexpr int V = 16 / sizeof(T);
+  float v[V];
+  unpack<T>(raw, v);
+  uint32_t w[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) w[i] = (uint32_t)rtn_code_slow(v[i], a, level);
+  uint2 out;
+  out.x = pack4_lo8(w);
+  out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
+  return out;
+}
+// RTN codes of one vector, packed (V = 8: 8 bytes, V = 4: 4 bytes in .x).
+// mode: 0 zero scale, 1 tiny scale (reference double path), 2 fast path.
+template <typename T>
+__device__ __forceinline__ uint2 rtn_raw(const uint4& raw, float a, float inv_a, int mode) {
+  constexpr int V = 16 / sizeof(T);
+  if (mode == 2) {
+    float v[V];
+    unpack<T>(raw, v);
+    uint32_t w[V];
+    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) return rtn_exact_raw<T>(raw, a, inv_a, 127.0f);
+    uint2 out;
+    out.x = pack4_lo8(w);
+    out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
+    return out;
+  }
+  if (mode == 1) return rtn_slow_raw<T>(raw, a, 127.0f);
+  return make_uint2(0u, 0u);
+}
+__device__ __forceinline__ float code_of(const uint2& c, int i) {
+  const uint32_t w = i < 4 ? c.x : c.y;
+  return (float)(int8_t)(uint8_t)(w >> (8 * (i & 3)));
+}
+
+// One block's work given its raw values in registers (all threads; contains
+// CTA barriers).
+template <typename T>
+__device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t bi, int64_t bj,
+                                                   int64_t blk, const uint4 (&raw)[Tiling<T>::NP],
+                                                   float* red) {
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t r0 = bi * kBlock + lr, cc = bj * kBlock + lc;
+  const bool col_ok = cc < p.cols;  // cols % V == 0: whole vectors
+  const int64_t left = p.rows - r0;  // rows from this thread's first row to the end
+  const int nrow = left <= 0 ? 0 : (left >= (int64_t)NP * RPP ? NP : (int)((left + RPP - 1) / RPP));
+  // ---- block absmax -> scale (quant.cpp:27-32) ----
+  float m = 0.0f;
+  if constexpr (sizeof(T) == 2) {
+    // |bf16| orders like its low 15 bits as an unsigned integer: packed 16x2
+    // integer max on the raw words, no unpacking (LOP3 + VIMNMX3.U16x2)
+    uint32_t mm = 0;
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {
+      mm = __vmaxu2(mm, raw[ps].x & 0x7FFF7FFFu);
+      mm = __vmaxu2(mm, raw[ps].y & 0x7FFF7FFFu);
+      mm = __vmaxu2(mm, raw[ps].z & 0x7FFF7FFFu);
+      mm = __vmaxu2(mm, raw[ps].w & 0x7FFF7FFFu);
+    }
+    m = __uint_as_float(max(mm >> 16, mm & 0xFFFFu) << 16);
+  } else {
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {
+      float v[V];
+      unpack<T>(raw[ps], v);
+#pragma unroll
+      for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+    }
+  }
+  const float amax = block_max(m, red);
+  const float a = block_scale(amax);
+  const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
+  const int mode = round_mode(a);
+  bool flagged = false;
+  if (p.mask_mode == kMaskThreshold) {
+    const double theta = p.theta_dev ? *p.theta_dev : p.theta;
+    flagged = (double)amax > theta;  // policy.cpp:77, strict, in double
+  } else if (p.mask_mode == kMaskGiven) {
+    flagged = (p.mask_bits[blk >> 5] >> (blk & 31)) & 1u;
+  }
+  if (threadIdx.x == 0) {
+    if (p.scales) p.scales[blk] = a;
+    if (p.amax_out) p.amax_out[blk] = amax;
+    if (p.mask_mode == kMaskThreshold && flagged) atomicOr(p.mask_bits + (blk >> 5), 1u << (blk & 31));
+    if (flagged && p.masked_count) atomicAdd(p.masked_count, 1);
+    if (p.res_scales && !flagged) p.res_scales[blk] = 0.0f;
+  }
+  // ---- RTN codes (kernels.cpp:24-40) ----
+  uint2 code[NP];
+  int8_t* cp = p.codes ? p.codes + r0 * p.ldq + cc : nullptr;
+#pragma unroll
+  for (int ps = 0; ps < NP; ++ps) {
+    code[ps] = rtn_raw<T>(raw[ps], a, inv_a, mode);
+    if (cp && col_ok && ps < nrow) {
+      int8_t* dst = cp + (int64_t)ps * RPP * p.ldq;
+      if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), code[ps]);
+      else __stcs(reinterpret_cast<unsigned int*>(dst), code[ps].x);
+    }
+  }
+  if (!flagged) return;  // block-uniform
+  // ---- fallback residual (quant.cpp:146-172): res = fl(x - fl(c * a)) ----
+  float rm = 0.0f;
+#pragma unroll
+  for (int ps = 0; ps < NP; ++ps) {
+    float v[V];
+    unpack<T>(raw[ps], v);
+#pragma unroll
+    for (int i = 0; i < V; ++i) rm = fmaxf(rm, fabsf(__fsub_rn(v[i], __fmul_rn(code_of(code[ps], i), a))));
+  }
+  const float ra = block_scale(block_max(rm, red));
+  const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
+  const int rmode = round_mode(ra);
+  if (threadIdx.x == 0 && p.res_scales) p.res_scales[blk] = ra;
+  if (!p.res_codes || !col_ok) return;
+  int8_t* rp = p.res_codes + r0 * p.ldq + cc;
+#pragma unroll
+  for (int ps = 0; ps < NP; ++ps) {
+    if (ps >= nrow) break;
+    float v[V];
+    unpack<T>(raw[ps], v);
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn(code_of(code[ps], i), a));
+    uint32_t w[V];
+    rtn_vec<V>(v, ra, inv_ra, rmode, w);
+    int8_t* dst = rp + (int64_t)ps * RPP * p.ldq;
+    if constexpr (V == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(pack4_lo8(w), pack4_lo8(w + 4));
+    else *reinterpret_cast<uint32_t*>(dst) = pack4_lo8(w);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_block_reg(const QuantParams& p, int64_t bi, int64_t bj,
+                                               uint4 (&raw)[Tiling<T>::NP]) {
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t r0 = bi * kBlock + lr, cc = bj * kBlock + lc;
+  const bool col_ok = cc < p.cols;
+  const int64_t left = p.rows - r0;
+  const int nrow = left <= 0 ? 0 : (left >= (int64_t)NP * RPP ? NP : (int)((left + RPP - 1) / RPP));
+  const T* xp = reinterpret_cast<const T*>(p.x) + r0 * p.ldx + cc;
+#pragma unroll
+  for (int ps = 0; ps < NP; ++ps)
+    raw[ps] = (col_ok && ps < nrow) ? __ldcs(reinterpret_cast<const uint4*>(xp + (int64_t)ps * RPP * p.ldx))
+                                    : make_uint4(0, 0, 0, 0);
+}
+
+// One 128 x 128 block per CTA (fp32 inputs: 64 registers of raw values per
+// thread leave no room for a register double buffer).
+template <typename T>
+__global__ void __launch_bounds__(kQuantThreads, 2)
+fbq_quantize_reg_kernel(QuantParams p) {
+  __shared__ float red[kQuantThreads / 32];
+  uint4 raw[Tiling<T>::NP];
+  load_block_reg<T>(p, blockIdx.y, blockIdx.x, raw);
+  quantize_block_reg<T>(p, blockIdx.y, blockIdx.x, (int64_t)blockIdx.y * gridDim.x + blockIdx.x, raw, red);
+}
+
+// Persistent + TMA ring + register compute (bf16): tiles land in a kQStages
+// shared-memory ring by TMA while the CTA quantizes the current tile from
+// registers; a slot is handed back to TMA as soon as its values are in registers.
+template <typename T, int kQStages, int kMinBlocks>
+__global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
+fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantParams p, int nblk,
+                            int gcols) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  T* tiles = reinterpret_cast<T*>(dsm);
+  __shared__ __align__(8) uint64_t full[kQStages];
+  __shared__ float red[kQuantThreads / 32];
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  constexpr uint32_t kTileBytes = sizeof(T) * kTileElems;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQStages; ++s) sm100::mbar_init(full + s, 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&map_x);
+  }
+  __syncthreads();
+  const uint64_t pol = sm100::l2_policy_evict_first();  // X is streamed once
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQStages; ++s) {
+      const int b = (int)blockIdx.x + s * (int)gridDim.x;
+      if (b >= nblk) break;
+      sm100::mbar_arrive_expect_tx(full + s, kTileBytes);
+      sm100::tma_load_2d(tiles + s * kTileElems, &map_x, full + s, (b % gcols) * kBlock, (b / gcols) * kBlock, pol);
+    }
+  }
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  int s = 0;
+  uint32_t phase = 0;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    sm100::mbar_wait(full + s, phase);
+    uint4 raw[NP];
+    const T* tile = tiles + s * kTileElems + lr * kBlock + lc;
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) raw[ps] = *reinterpret_cast<const uint4*>(tile + ps * RPP * kBlock);
+    __syncthreads();  // every thread holds its values: slot s goes back to TMA
+    if (threadIdx.x == 0) {
+      const int nb = b + kQStages * (int)gridDim.x;
+      if (nb < nblk) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sm100::mbar_arrive_expect_tx(full + s, kTileBytes);
+        sm100::tma_load_2d(tiles + s * kTileElems, &map_x, full + s, (nb % gcols) * kBlock, (nb / gcols) * kBlock, pol);
+      }
+    }
+    if (++s == kQStages) { s = 0; phase ^= 1; }
+    const int bi = b / gcols;
+    quantize_block_reg<T>(p, bi, b - bi * gcols, b, raw, red);
+  }
+}
+
+// Persistent, TMA-pipelined K1 (the HBM-bound path for TMA-compatible inputs).
+// One-block-per-CTA staging leaves each CTA idle on HBM while it computes and
+// idle on the ALUs while it loads (measured 11-37 % of HBM).  Here each CTA
+// walks blocks b = blockIdx.x, blockIdx.x + gridDim.x, ... with a kQStages
+// ring of 128 x 128 tiles filled by TMA (zero fill outside the tensor = the
+// reference's truncated edge blocks, matching stage_tile): while the CTA runs
+// quantize_block on tile i, tiles i+1 .. i+kQStages-1 are in flight.
+template <typename T, int kSR, int kQStages>
+__global__ void __launch_bounds__(kQuantThreads)
+fbq_quantize_tma_kernel(const __grid_constant__ CUtensorMap map_x, QuantParams p, int64_t nblk,
+                        int gcols) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  T* tiles = reinterpret_cast<T*>(dsm);
+  __shared__ __align__(8) uint64_t full[kQStages];
+  __shared__ float red[kQuantThreads / 32];
+  constexpr int V = Tiling<T>::V;
+  constexpr uint32_t kTileBytes = sizeof(T) * kTileElems;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQStages; ++s) sm100::mbar_init(full + s, 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&map_x);
+  }
+  __syncthreads();
+  const uint64_t pol = sm100::l2_policy_evict_first();  // X is streamed once
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQStages; ++s) {
+      const int64_t b = blockIdx.x + (int64_t)s * gridDim.x;
+      if (b >= nblk) break;
+      sm100::mbar_arrive_expect_tx(full + s, kTileBytes);
+      sm100::tma_load_2d(tiles + s * kTileElems, &map_x, full + s, (int)(b % gcols) * kBlock,
+                         (int)(b / gcols) * kBlock, pol);
+    }
+  }
+  int s = 0;
+  uint32_t phase = 0;
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    sm100::mbar_wait(full + s, phase);
+    const T* tile = tiles + s * kTileElems;
+    const int64_t bi = b / gcols, bj = b % gcols;
+    quantize_block<V, kSR>(p, b, bi * kBlock, bj * kBlock, red,
+                           [&](int rb, int cb, float (&v)[V]) { load_vec<T, V>(tile + rb * kBlock + cb, v); });
+    __syncthreads();  // every thread is done reading slot s
+    if (threadIdx.x == 0) {
+      const int64_t nb = b + (int64_t)kQStages * gridDim.x;
+      if (nb < nblk) {
+        // order this CTA's generic-proxy reads of the slot before the TMA (async-proxy) write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sm100::mbar_arrive_expect_tx(full + s, kTileBytes);
+        sm100::tma_load_2d(tiles + s * kTileElems, &map_x, full + s, (int)(nb % gcols) * kBlock,
+                           (int)(nb / gcols) * kBlock, pol);
+      }
+    }
+    if (++s == kQStages) { s = 0; phase ^= 1; }
+  }
 }
 
 // ------------------------------------------------------------------ GLU
@@ -631,12 +940,141 @@ static cudaError_t launch_k1(QuantParams p, dim3 grid, cudaStream_t s) {
   return launch_k1_sr<T, kVec, 0>(p, grid, s);
 }
 
+typedef CUresult (*PFN_encodeTiledQ)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiledQ encode_fn() {
+  static PFN_encodeTiledQ fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiledQ>(ptr);
+  }
+  return fn;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename T, int kSR, int kQStages>
+static cudaError_t launch_k1_tma(const QuantParams& p, cudaStream_t s) {
+  const size_t smem = (size_t)kQStages * sizeof(T) * kTileElems;
+  static int ctas_per_sm = 0;
+  if (!ctas_per_sm) {
+    if (cudaError_t e = opt_in_smem(fbq_quantize_tma_kernel<T, kSR, kQStages>, smem)) return e;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_kernel<T, kSR, kQStages>,
+                                                      kQuantThreads, smem) != cudaSuccess || n < 1)
+      n = 1;
+    ctas_per_sm = n;
+  }
+  CUtensorMap m;
+  PFN_encodeTiledQ enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const size_t esz = sizeof(T);
+  cuuint64_t dims[2] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(p.ldx * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)kBlock, (cuuint32_t)kBlock};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&m, sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+          const_cast<void*>(p.x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const int gcols = (int)((p.cols + kBlock - 1) / kBlock);
+  const int64_t nblk = (int64_t)gcols * ((p.rows + kBlock - 1) / kBlock);
+  int64_t grid = (int64_t)num_sms() * ctas_per_sm;
+  if (grid > nblk) grid = nblk;
+  fbq_quantize_tma_kernel<T, kSR, kQStages><<<(unsigned)grid, kQuantThreads, smem, s>>>(m, p, nblk, gcols);
+  return cudaGetLastError();
+}
+template <typename T, int kQStages, int kMinBlocks>
+static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
+  const size_t smem = (size_t)kQStages * sizeof(T) * kTileElems;
+  static int ctas_per_sm = 0;
+  if (!ctas_per_sm) {
+    if (cudaError_t e = opt_in_smem(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks>, smem)) return e;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks>,
+                                                      kQuantThreads, smem) != cudaSuccess || n < 1)
+      n = 1;
+    ctas_per_sm = n;
+  }
+  CUtensorMap m;
+  PFN_encodeTiledQ enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const size_t esz = sizeof(T);
+  cuuint64_t dims[2] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(p.ldx * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)kBlock, (cuuint32_t)kBlock};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&m, sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+          const_cast<void*>(p.x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const int gcols = (int)((p.cols + kBlock - 1) / kBlock);
+  const int64_t nblk = (int64_t)gcols * ((p.rows + kBlock - 1) / kBlock);
+  int64_t grid = (int64_t)num_sms() * ctas_per_sm;
+  if (grid > nblk) grid = nblk;
+  fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks><<<(unsigned)grid, kQuantThreads, smem, s>>>(m, p, (int)nblk, gcols);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_k1_tma_any(QuantParams p, cudaStream_t s) {
+  if (!p.sr_codes && p.sr_codes2) {
+    p.sr_codes = p.sr_codes2;
+    p.sr_seed = p.sr_seed2;
+    p.sr_codes2 = nullptr;
+  }
+  // ring depth: 3 x 32 KiB (bf16, two CTAs per SM) / 3 x 64 KiB (fp32, one CTA per SM)
+  if (p.sr_codes2) return launch_k1_tma<T, 2, 3>(p, s);
+  if (p.sr_codes) return launch_k1_tma<T, 1, 3>(p, s);
+  return launch_k1_tma<T, 0, 3>(p, s);
+}
+
+// diagnostics: 1 = force the smem-staged one-block-per-CTA K1, 2 = the
+// persistent TMA-pipelined K1 for SR launches, 4 = bf16 TMA ring 3 stages x
+// 2 CTAs per SM (A/B comparisons; results are identical)
+int g_quant_diag = 0;
+
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
   const dim3 grid((unsigned)((p.cols + kBlock - 1) / kBlock),
                   (unsigned)((p.rows + kBlock - 1) / kBlock));
   const size_t esz = bf16 ? 2 : 4;
   const bool vec = (reinterpret_cast<uintptr_t>(p.x) % 16 == 0) && ((p.ldx * esz) % 16 == 0) &&
                    (p.cols % (16 / esz) == 0);
+  // TMA path: 16-byte aligned base and row stride (the tensor-map rules), and
+  // enough blocks to fill the machine (small tensors keep the simple kernel)
+  const int64_t nblk = (int64_t)grid.x * grid.y;
+  // register-resident K1: RTN / fallback detect with 8-byte aligned code planes
+  const bool sr = p.sr_codes || p.sr_codes2;
+  if (vec && !sr && !(g_quant_diag & 1) && p.vec_store) {
+    if (bf16 && nblk >= 2 * num_sms() && p.rows < (1ll << 31) && p.cols < (1ll << 31))
+      // 2-stage ring, three CTAs (24 warps) per SM: measured faster than
+      // 3 stages x 2 CTAs (latency hiding of the rounding passes matters more)
+      return (g_quant_diag & 4) ? launch_k1_tma_reg<__nv_bfloat16, 3, 2>(p, s)
+                                : launch_k1_tma_reg<__nv_bfloat16, 2, 3>(p, s);
+    if (bf16) fbq_quantize_reg_kernel<__nv_bfloat16><<<grid, kQuantThreads, 0, s>>>(p);
+    else fbq_quantize_reg_kernel<float><<<grid, kQuantThreads, 0, s>>>(p);
+    return cudaGetLastError();
+  }
+  if (vec && (g_quant_diag & 2) && nblk >= 2 * num_sms() && p.rows < (1ll << 31) &&
+      p.cols < (1ll << 31))
+    return bf16 ? launch_k1_tma_any<__nv_bfloat16>(p, s) : launch_k1_tma_any<float>(p, s);
   if (bf16) return vec ? launch_k1<__nv_bfloat16, true>(p, grid, s)
                        : launch_k1<__nv_bfloat16, false>(p, grid, s);
   return vec ? launch_k1<float, true>(p, grid, s) : launch_k1<float, false>(p, grid, s);

@@ -73,6 +73,7 @@ struct DequantParams {
 };
 
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s);
+extern int g_quant_diag;  // 1 = one-block-per-CTA K1 (diagnostics, fbq_debug_set_quant_diag)
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
 cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s);
