@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--tokens", type=int, default=TOKENS, help="tokens per GPU")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -361,16 +361,28 @@ def run_ours(args, rank, world, local):
             mlp_h = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.bfloat16,
                                   exact=False)
             mlp_h.set_thresholds(th_gu, th_d)
+            flags = mlp_h.STEP_ZERO_GRAD | mlp_h.STEP_CONTROLLER  # the device step's work
             for i in range(2):
-                mlp_h.step_host(xh, gyh, i, yh, gxh)
+                mlp_h.step_host_async(xh, gyh, i, yh, gxh, flags)
+            mlp_h.host_sync()
             t0 = time.perf_counter()
             for i in range(args.e2e_steps):
-                mlp_h.step_host(xh, gyh, 2 + i, yh, gxh)
+                mlp_h.step_host_async(xh, gyh, 2 + i, yh, gxh, flags)
+            mlp_h.host_sync()
             dt = (time.perf_counter() - t0) / args.e2e_steps
+            # the synchronous one-step API, for reference (warm, then 3 steps)
+            mlp_h.step_host(xh, gyh, 98, yh, gxh)
+            t1 = time.perf_counter()
+            for i in range(3):
+                mlp_h.step_host(xh, gyh, 99 + i, yh, gxh)
+            dt_sync = (time.perf_counter() - t1) / 3
             bytes_io = T * D_MODEL * 4
             e2e = {"value": T / dt, "unit": "tokens/s", "h2d_bytes_per_step": 2 * bytes_io,
-                   "d2h_bytes_per_step": 2 * bytes_io,
-                   "api": "fbq_mlp_step_host (host fp32 x, dY in; y, dX out; pinned)"}
+                   "d2h_bytes_per_step": 2 * bytes_io, "steps": args.e2e_steps,
+                   "api": "fbq_mlp_step_host_async + fbq_mlp_host_sync (host fp32 x, dY in; "
+                          "y, dX out; pinned; zero_grad + fwd + bwd + controller per step; "
+                          "step i's copies overlap step i-1's compute), wall clock",
+                   "sync_api_tokens_per_s": T / dt_sync}
             del mlp_h
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}

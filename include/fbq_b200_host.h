@@ -65,6 +65,18 @@ int fbq_mlp_zero_grad(void* mlp, fbq_stream_t stream);
 int fbq_mlp_step_host(void* mlp, const float* x, const float* gy, int64_t tokens, int step,
                       float* y, float* gx);
 
+/* Pipelined host API: enqueue one step (zero_grad if FBQ_STEP_ZERO_GRAD, fwd,
+ * bwd, controller_step if FBQ_STEP_CONTROLLER) over host fp32 buffers and
+ * return.  Step i's H2D copies overlap step i-1's compute and step i-1's D2H
+ * copies overlap step i's (two device slots).  Host buffers must stay valid,
+ * and outputs must not be read, until fbq_mlp_host_sync returns; pinned
+ * buffers make the copies truly asynchronous. */
+#define FBQ_STEP_ZERO_GRAD 1
+#define FBQ_STEP_CONTROLLER 2
+int fbq_mlp_step_host_async(void* mlp, const float* x, const float* gy, int64_t tokens, int step,
+                            float* y, float* gx, int flags);
+int fbq_mlp_host_sync(void* mlp);
+
 /* Set the device-resident thresholds (gate/up share one, down has its own). */
 int fbq_mlp_set_thresholds(void* mlp, double theta_gate_up, double theta_down);
 /* Optional CUDA-event timing of every GEMM launch (on the launching stream);

@@ -165,6 +165,11 @@ struct Mlp {
   }
 
   ~Mlp() {
+    if (a_cs) {
+      cudaStreamSynchronize(a_cs);
+      cudaStreamSynchronize(a_d2h);
+    }
+    async_free();
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd})
@@ -338,6 +343,90 @@ struct Mlp {
     CU_TRY(cudaStreamSynchronize(s));
     CU_TRY(cudaStreamSynchronize(copy_stream));
   }
+
+  // ---- pipelined host-buffer steps (fbq_mlp_step_host_async) ----
+  // Two device slots of (x, dY, y, dX): step i's H2D copies run on their own
+  // stream while step i-1 computes, and step i-1's D2H copies (y right after
+  // its forward, dX after its backward) overlap step i's compute -- a training
+  // loop's batch prefetch.  Each step still moves its own inputs in and its
+  // own results out.
+  cudaStream_t a_cs = nullptr, a_h2d = nullptr, a_d2h = nullptr;
+  DevBuf ax[2], agy[2], ay[2], agx[2];
+  cudaEvent_t a_in[2] = {}, a_fwd[2] = {}, a_done[2] = {}, a_out[2] = {};
+  bool a_used[2] = {false, false};
+  int64_t a_count = 0;
+
+  void async_init() {
+    if (a_cs) return;
+    CU_TRY(cudaStreamCreateWithFlags(&a_cs, cudaStreamNonBlocking));
+    CU_TRY(cudaStreamCreateWithFlags(&a_h2d, cudaStreamNonBlocking));
+    CU_TRY(cudaStreamCreateWithFlags(&a_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      ax[i] = DevBuf(T * D * 4);
+      agy[i] = DevBuf(T * D * 4);
+      ay[i] = DevBuf(T * D * 4);
+      agx[i] = DevBuf(T * D * 4);
+      for (cudaEvent_t* e : {&a_in[i], &a_fwd[i], &a_done[i], &a_out[i]})
+        CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+  }
+  void async_free() {
+    for (cudaStream_t st : {a_cs, a_h2d, a_d2h})
+      if (st) cudaStreamDestroy(st);
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {a_in[i], a_fwd[i], a_done[i], a_out[i]})
+        if (e) cudaEventDestroy(e);
+  }
+
+  void zero_grad(cudaStream_t s) {
+    CU_TRY(cudaMemsetAsync(g_gu.p, 0, 2 * F * D * 4, s));
+    CU_TRY(cudaMemsetAsync(g_d.p, 0, D * F * 4, s));
+  }
+
+  void step_host_async(const float* x, const float* gy, int64_t tok, int step, float* y, float* gx,
+                       int flags) {
+    if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
+    if (tok == 0) return;
+    async_init();
+    const int slot = (int)(a_count++ & 1);
+    const size_t bytes = tok * D * 4;
+    // inputs: the slot's previous step must be done reading them
+    if (a_used[slot]) CU_TRY(cudaStreamWaitEvent(a_h2d, a_done[slot], 0));
+    CU_TRY(cudaMemcpyAsync(ax[slot].p, x, bytes, cudaMemcpyHostToDevice, a_h2d));
+    CU_TRY(cudaMemcpyAsync(agy[slot].p, gy, bytes, cudaMemcpyHostToDevice, a_h2d));
+    CU_TRY(cudaEventRecord(a_in[slot], a_h2d));
+    // compute: inputs landed, and the slot's previous outputs are copied out
+    CU_TRY(cudaStreamWaitEvent(a_cs, a_in[slot], 0));
+    if (a_used[slot]) CU_TRY(cudaStreamWaitEvent(a_cs, a_out[slot], 0));
+    const int saved = c.act_dtype;
+    c.act_dtype = FBQ_F32;  // the host API is fp32 like the reference
+    try {
+      if (flags & FBQ_STEP_ZERO_GRAD) zero_grad(a_cs);
+      forward(ax[slot].p, tok, 0, step, ay[slot].p, a_cs);
+      CU_TRY(cudaEventRecord(a_fwd[slot], a_cs));
+      backward(agy[slot].p, tok, 0, step, agx[slot].p, a_cs);
+      if (flags & FBQ_STEP_CONTROLLER) controller(a_cs);
+      CU_TRY(cudaEventRecord(a_done[slot], a_cs));
+    } catch (...) {
+      c.act_dtype = saved;
+      throw;
+    }
+    c.act_dtype = saved;
+    last_blocks[0] = cdiv(tok, 128) * gD;
+    last_blocks[1] = cdiv(tok, 128) * gF;
+    // outputs: y as soon as the forward is done, dX after the backward
+    CU_TRY(cudaStreamWaitEvent(a_d2h, a_fwd[slot], 0));
+    CU_TRY(cudaMemcpyAsync(y, ay[slot].p, bytes, cudaMemcpyDeviceToHost, a_d2h));
+    CU_TRY(cudaStreamWaitEvent(a_d2h, a_done[slot], 0));
+    CU_TRY(cudaMemcpyAsync(gx, agx[slot].p, bytes, cudaMemcpyDeviceToHost, a_d2h));
+    CU_TRY(cudaEventRecord(a_out[slot], a_d2h));
+    a_used[slot] = true;
+  }
+  void host_sync() {
+    if (!a_cs) return;
+    CU_TRY(cudaStreamSynchronize(a_cs));
+    CU_TRY(cudaStreamSynchronize(a_d2h));
+  }
 };
 
 thread_local std::string g_host_err;
@@ -417,11 +506,20 @@ int fbq_mlp_controller_step(void* m, fbq_stream_t stream) {
 int fbq_mlp_zero_grad(void* m, fbq_stream_t stream) {
   if (!m) return FBQ_ERR_ARG;
   return guarded([&] {
-    auto* mlp = static_cast<Mlp*>(m);
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    CU_TRY(cudaMemsetAsync(mlp->g_gu.p, 0, 2 * mlp->F * mlp->D * 4, s));
-    CU_TRY(cudaMemsetAsync(mlp->g_d.p, 0, mlp->D * mlp->F * 4, s));
+    static_cast<Mlp*>(m)->zero_grad(reinterpret_cast<cudaStream_t>(stream));
   });
+}
+
+int fbq_mlp_step_host_async(void* m, const float* x, const float* gy, int64_t tokens, int step,
+                            float* y, float* gx, int flags) {
+  if (!m || (tokens > 0 && (!x || !gy || !y || !gx))) return FBQ_ERR_ARG;
+  if (flags & ~(FBQ_STEP_ZERO_GRAD | FBQ_STEP_CONTROLLER)) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<Mlp*>(m)->step_host_async(x, gy, tokens, step, y, gx, flags); });
+}
+
+int fbq_mlp_host_sync(void* m) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<Mlp*>(m)->host_sync(); });
 }
 
 int fbq_mlp_step_host(void* m, const float* x, const float* gy, int64_t tokens, int step,

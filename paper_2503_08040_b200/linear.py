@@ -40,6 +40,9 @@ _sigs = {
     "fbq_mlp_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fbq_mlp_step_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
                                     C.c_void_p, C.c_void_p]),
+    "fbq_mlp_step_host_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                          C.c_void_p, C.c_void_p, C.c_int]),
+    "fbq_mlp_host_sync": (C.c_int, [C.c_void_p]),
     "fbq_mlp_grad_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
     "fbq_mlp_get_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fbq_mlp_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -151,6 +154,20 @@ class GluMlp:
         _check(lib.fbq_mlp_step_host(self._h, ptr(x), ptr(gy), t, step, ptr(y), ptr(gx)),
                "step_host")
         return y, gx
+
+    STEP_ZERO_GRAD, STEP_CONTROLLER = 1, 2
+
+    def step_host_async(self, x, gy, step: int, y, gx, flags: int = 0):
+        """Enqueue one pipelined host-buffer step (fbq_mlp_step_host_async); the
+        buffers must stay alive and y/gx must not be read before host_sync()."""
+        def ptr(a):
+            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+        _check(lib.fbq_mlp_step_host_async(self._h, ptr(x), ptr(gy), x.shape[0], step, ptr(y),
+                                           ptr(gx), flags), "step_host_async")
+
+    def host_sync(self):
+        _check(lib.fbq_mlp_host_sync(self._h), "host_sync")
 
     def grads_host(self):
         gg = np.empty((self.d_ff, self.d_model), np.float32)

@@ -142,3 +142,32 @@ def test_mlp_token_shards_match_full_batch(mods):
         parts.append(m.grads_host())
     for i, g in enumerate(full.grads_host()):
         assert rel_fro(parts[0][i] + parts[1][i], g) < 1e-6
+
+
+def test_mlp_pipelined_host_api_matches_sync(mods):
+    """fbq_mlp_step_host_async (two device slots, copies overlapping the
+    neighbouring steps' compute) returns every step's outputs bit-identical to
+    the synchronous host API, and leaves the same gradients and controller state."""
+    import torch
+    linear, _ = mods
+    wg, wu, wd = weights(11)
+    kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True, threshold_init=2.0)
+    m1 = linear.GluMlp(wg, wu, wd, T, **kw)
+    m2 = linear.GluMlp(wg, wu, wd, T, **kw)
+    steps = [inputs(20 + i) for i in range(4)]
+    want = []
+    for i, (x, gy) in enumerate(steps):
+        m1.zero_grad()
+        want.append(m1.step_host(x, gy, i))
+        m1.controller_step()
+    torch.cuda.synchronize()
+    outs = [(np.empty_like(x), np.empty_like(x)) for x, _ in steps]
+    flags = m2.STEP_ZERO_GRAD | m2.STEP_CONTROLLER
+    for i, ((x, gy), (y, gx)) in enumerate(zip(steps, outs)):
+        m2.step_host_async(x, gy, i, y, gx, flags)
+    m2.host_sync()
+    for (y, gx), (yw, gxw) in zip(outs, want):
+        assert np.array_equal(y, yw) and np.array_equal(gx, gxw)
+    for a, b in zip(m1.grads_host(), m2.grads_host()):
+        assert np.array_equal(a, b)
+    assert m1.controller_state() == m2.controller_state()
