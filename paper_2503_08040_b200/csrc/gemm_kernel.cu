@@ -54,7 +54,8 @@ constexpr int kStageBytes = 2 * kTileA + kTileB;
 constexpr int kTmemCols = 512;     // 2 slots x 256 int32 columns
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // WG0: TMA, MMA, scales, idle; WG1-2: epilogue
-constexpr int kPage = 128;                      // k-blocks per staged scale page
+constexpr int kPage = 32;                       // k-blocks per staged scale page
+constexpr int kOutChunk = 4096;                 // per-warp output staging buffer (TMA store box)
 constexpr uint32_t kMagicBits = 0x4B400000u;    // magic-bias decode (see consume)
 constexpr float kMagicF = 12582912.0f;          // 1.5 * 2^23
 
@@ -65,7 +66,8 @@ struct ScalePage {
 };
 
 constexpr size_t kSmemBytes =
-    1024 + (size_t)kStages * kStageBytes + 2 * sizeof(ScalePage) + 256;
+    1024 + (size_t)kStages * kStageBytes + (size_t)kEpiWarps * kOutChunk + 2 * sizeof(ScalePage) + 256;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 // Grouped rasterisation: tiles walk kGroupM block-rows at a time (bm fastest),
 // so the ~148 CTAs resident at once share kGroupM A row-panels and ~148/kGroupM
@@ -120,7 +122,8 @@ __device__ __forceinline__ void consume(const uint32_t (&v)[32], float2* acc, fl
 // 128-column half h of every 128 x 256 tile.
 // kProf: per-item timeline of warp q == 0 (clock64, diagnostics only).
 template <int kEpi, int h, bool kProf>
-__device__ __forceinline__ void epilogue_role(const GemmParams& p, ScalePage* pages, uint64_t* tfull,
+__device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtensorMap* map_o,
+                                              uint8_t* obuf, ScalePage* pages, uint64_t* tfull,
                                               uint64_t* tempty, uint64_t* sfull, uint64_t* sempty,
                                               uint32_t* tmem_holder, int warp, int lane, int NT) {
   const int q = warp & 3;  // TMEM lane quadrant this warp may access
@@ -212,7 +215,72 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, ScalePage* pa
       __syncwarp();
       if (lane == 0) mbar_arrive(sempty + (pc & 1));
     }
-    if (kEpi != kEpiDump && !(p.diag & 4)) {
+    if (kEpi != kEpiDump && !(p.diag & 4) && p.tma_store) {
+      // Staged TMA stores: the warp's 32 rows x 128 columns go out in 4 KiB
+      // boxes (64 bf16 or 32 fp32 columns x 32 rows), written into a 128B-
+      // swizzled staging buffer (16-byte chunk j of row r at chunk j ^ (r & 7):
+      // conflict-free) and handed to TMA, which clips ragged edges; the warp
+      // only waits for the previous box to be READ from shared memory.  Tile-end
+      // stores thus no longer hold back the TMEM drain (direct per-row stores
+      // cost ~16 % of the GEMM).  p.tma_store == 2: fp32 reduce-add (accumulate).
+      const int64_t row0 = (int64_t)bm * kBM + q * 32;
+      if (bn < p.NB && row0 < p.M) {
+        const int cols_per_box = p.out_bf16 ? 64 : 32;
+        const int nbox = 128 / cols_per_box;
+        uint8_t* rowp = obuf + lane * 128;
+        for (int c = 0; c < nbox; ++c) {
+          if (p.tma_store != 3 && lane == 0) bulk_wait_read0();  // the previous box left the buffer
+          __syncwarp();
+          if (p.out_bf16) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // 8 x 16 B = 64 bf16 of this lane's row
+              const float2* a = acc + c * 32 + j * 4;
+              uint4 w;
+              __nv_bfloat162 b0 = __float22bfloat162_rn(a[0]), b1 = __float22bfloat162_rn(a[1]);
+              __nv_bfloat162 b2 = __float22bfloat162_rn(a[2]), b3 = __float22bfloat162_rn(a[3]);
+              w.x = *reinterpret_cast<uint32_t*>(&b0);
+              w.y = *reinterpret_cast<uint32_t*>(&b1);
+              w.z = *reinterpret_cast<uint32_t*>(&b2);
+              w.w = *reinterpret_cast<uint32_t*>(&b3);
+              *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // 8 x 16 B = 32 fp32 of this lane's row
+              const float2* a = acc + c * 16 + j * 2;
+              *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(a[0].x, a[0].y, a[1].x, a[1].y);
+            }
+          }
+          if (p.tma_store == 3) {
+            // coalesced copy-out: lane l moves 16-byte chunk (l & 7) of rows
+            // 4i + (l >> 3): every STG.128 writes four full 128 B lines
+            __syncwarp();
+            const int64_t gcol = (int64_t)bn * 128 + c * cols_per_box;
+            const int esz = p.out_bf16 ? 2 : 4;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 4 * i + (lane >> 3), j = lane & 7;
+              const uint4 v = *reinterpret_cast<const uint4*>(obuf + r * 128 + ((j ^ (r & 7)) << 4));
+              const int64_t grow = row0 + r;
+              const int64_t col = gcol + j * (16 / esz);
+              if (grow < p.M && col < p.N)
+                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + (grow * p.ldo + col) * esz) = v;
+            }
+            __syncwarp();
+          } else {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int c0 = bn * 128 + c * cols_per_box;
+              if (p.tma_store == 2) tma_reduce_add_2d(map_o, obuf, c0, (int)row0);
+              else tma_store_2d(map_o, obuf, c0, (int)row0);
+              bulk_commit();
+            }
+          }
+        }
+      }
+    } else if (kEpi != kEpiDump && !(p.diag & 4)) {
       const int64_t grow = (int64_t)bm * kBM + row_in_tile;
       const int64_t gcol0 = (int64_t)bn * 128;
       if (bn < p.NB && grow < p.M) {
@@ -285,6 +353,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, ScalePage* pa
       }
     }
   }
+  if (p.tma_store && lane == 0) bulk_wait0();  // this warp's stores are complete
   if constexpr (kProf) {
     if (q == 0 && lane == 0) {
       long long* o = p.prof + blockIdx.x * 16 + 1 + h * 4;
@@ -297,13 +366,15 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, ScalePage* pa
 template <int kEpi>
 __global__ void __launch_bounds__(kThreads, 1)
 fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_r,
-                const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
+                const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_o,
+                const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1 KiB alignment (128B-swizzle atoms) by pointer arithmetic on the shared
   // array itself, so every derived pointer (pages, barriers, the TMEM holder)
   // stays in the shared address space (LDS/STS, no generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  ScalePage* pages = reinterpret_cast<ScalePage*>(smem + kStages * kStageBytes);
+  uint8_t* ostage = smem + kStages * kStageBytes;  // [kEpiWarps][kOutChunk], 1 KiB aligned
+  ScalePage* pages = reinterpret_cast<ScalePage*>(ostage + kEpiWarps * kOutChunk);
   uint64_t* bars = reinterpret_cast<uint64_t*>(pages + 2);
   uint64_t* full = bars;                 // [kStages]
   uint64_t* empty = bars + kStages;      // [kStages]
@@ -497,11 +568,11 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // ===================== epilogue =====================
     setmaxnreg_inc<224>();
     if (p.prof) {
-      if (warp >= 8) epilogue_role<kEpi, 1, true>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
-      else epilogue_role<kEpi, 0, true>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      if (warp >= 8) epilogue_role<kEpi, 1, true>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      else epilogue_role<kEpi, 0, true>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
     } else {
-      if (warp >= 8) epilogue_role<kEpi, 1, false>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
-      else epilogue_role<kEpi, 0, false>(p, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      if (warp >= 8) epilogue_role<kEpi, 1, false>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      else epilogue_role<kEpi, 0, false>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
     }
   }
   tc_fence_before();
@@ -556,8 +627,8 @@ int gemm_num_sms() {
 
 template <int kEpi>
 static cudaError_t launch_typed(const CUtensorMap& ma, const CUtensorMap& mr,
-                                const CUtensorMap& mb, const GemmParams& p, int grid,
-                                cudaStream_t s) {
+                                const CUtensorMap& mb, const CUtensorMap& mo, const GemmParams& p,
+                                int grid, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fbq_gemm_kernel<kEpi>,
@@ -566,7 +637,7 @@ static cudaError_t launch_typed(const CUtensorMap& ma, const CUtensorMap& mr,
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  fbq_gemm_kernel<kEpi><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, p);
+  fbq_gemm_kernel<kEpi><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, mo, p);
   return cudaGetLastError();
 }
 
@@ -586,12 +657,30 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
   else ok &= make_map(&mb, o.b_codes, N, K, o.ldb, 128, 128);
   if (!ok) return cudaErrorInvalidValue;
 
+  // output tensor map for the staged TMA stores: 4 KiB boxes of 32 rows x 128 B,
+  // 128B swizzle (the staging layout); fp32 accumulate uses the reduce-add form
+  CUtensorMap mo = ma;
+  p.tma_store = 0;
+  if (epi != kEpiDump && p.out && p.vec_store && !(p.accumulate && p.out_bf16) && !(p.diag & 8192) &&
+      p.M < (1ll << 31) && p.N < (1ll << 31)) {
+    PFN_encodeTiled enc = get_encode();
+    const size_t esz = p.out_bf16 ? 2 : 4;
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)(p.ldo * esz)};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc && enc(&mo, p.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   2, p.out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.tma_store = p.accumulate ? 2 : ((p.diag & 16384) ? 3 : 1);
+  }
   p.num_tiles = p.MB * ((p.NB + 1) / 2);
   const int grid = p.num_tiles < gemm_num_sms() ? p.num_tiles : gemm_num_sms();
   switch (epi) {
-    case kEpiExact: return launch_typed<kEpiExact>(ma, mr, mb, p, grid, s);
-    case kEpiFma: return launch_typed<kEpiFma>(ma, mr, mb, p, grid, s);
-    default: return launch_typed<kEpiDump>(ma, mr, mb, p, grid, s);
+    case kEpiExact: return launch_typed<kEpiExact>(ma, mr, mb, mo, p, grid, s);
+    case kEpiFma: return launch_typed<kEpiFma>(ma, mr, mb, mo, p, grid, s);
+    default: return launch_typed<kEpiDump>(ma, mr, mb, mo, p, grid, s);
   }
 }
 

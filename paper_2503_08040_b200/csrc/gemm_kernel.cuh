@@ -28,6 +28,7 @@ struct GemmParams {
   int out_bf16;
   int accumulate;
   int vec_store;
+  int tma_store;            // 0: direct stores; 1: staged TMA stores; 2: staged TMA reduce-add (fp32 accumulate)
   int32_t* dump;            // kEpiDump: [MB][NB][KB][128][128] primary, then residual
   int64_t dump_res_offset;  // element offset of the residual products
   int num_tiles;
