@@ -199,6 +199,61 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------- C2 quantizer sweep
+def quant_sweep(device, hbm_peak):
+    """BASELINE configs[1]: quantize + fallback-detect (K1, threshold mode) on
+    Llama-3.1-8B activation shapes at fallback ratios 0/5/20 %, bf16 and fp32,
+    through the C ABI with preallocated outputs (CUDA events on the launch
+    stream; the in-stream zeroing of the 4-byte count and the bitmap is part
+    of the op).  Algorithmic bytes = in + codes + residual codes of flagged
+    blocks + scales (primary + residual) + bitmap; inputs (>= 100 MB) exceed L2."""
+    import torch
+    from paper_2503_08040_b200 import fbq
+    from paper_2503_08040_b200 import _capi as K
+    stream = torch.cuda.current_stream()
+    out = {}
+    for (R, C) in [(8192, 4096), (8192, 14336)]:
+        nb = (R // 128) * (C // 128)
+        codes = torch.empty(R, C, dtype=torch.int8, device=device)
+        res = torch.empty_like(codes)
+        scales = torch.empty(nb, dtype=torch.float32, device=device)
+        rscales = torch.empty_like(scales)
+        bits = torch.zeros((nb + 31) // 32, dtype=torch.int32, device=device)
+        count = torch.zeros(1, dtype=torch.int32, device=device)
+        for dt in (torch.bfloat16, torch.float32):
+            x = make_activations(R, C, 5, device, dt)
+            sc = fbq.score_blocks(x).flatten().sort(descending=True).values
+            for rate in (0.0, 0.05, 0.20):
+                k = int(round(rate * nb))
+                theta = float(sc[k].item()) if rate > 0 else float(sc[0].item()) * 2.0
+
+                def run():
+                    bits.zero_()
+                    count.zero_()
+                    K.call("fbq_cuda_quantize_fallback", x.data_ptr(), K.FBQ_BF16 if dt == torch.bfloat16 else K.FBQ_F32,
+                           R, C, C, K.FBQ_MASK_THRESHOLD, theta, bits.data_ptr(), codes.data_ptr(), C,
+                           scales.data_ptr(), res.data_ptr(), rscales.data_ptr(), count.data_ptr(),
+                           None, None, 0, 0, stream.cuda_stream)
+                for _ in range(3):
+                    run()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(20):
+                    run()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 20 * 1e-3
+                f = int(count.item()) / nb
+                byt = R * C * (x.element_size() + 1) + f * R * C + nb * 4 * (1 + f) + nb / 8
+                out[f"{R}x{C} {str(dt)[6:]} rate={rate:.2f}"] = {
+                    "us": round(t * 1e6, 1), "GBps": round(byt / t / 1e9, 0),
+                    "frac_hbm": round(byt / t / 1e9 / hbm_peak, 3), "flagged": round(f, 4)}
+            del x
+    return {"unit": "GB/s of algorithmic bytes", "peak_GBps": hbm_peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)", "cases": out}
+
+
 # ----------------------------------------------------------------- GEMM sweep
 def gemm_sweep(device):
     import torch
@@ -387,8 +442,12 @@ def run_ours(args, rank, world, local):
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
-        sweep = None
+        sweep = qsweep = None
         if not args.no_sweep:
+            try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
+                qsweep = quant_sweep(device, peaks.get("hbm_gbs", 6522.1))
+            except Exception as ex:  # pragma: no cover
+                qsweep = {"error": str(ex)[:200]}
             try:
                 sweep = gemm_sweep(device)
             except Exception as ex:  # pragma: no cover
@@ -428,6 +487,7 @@ def run_ours(args, rank, world, local):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gemm_sweep": sweep,
+            "quant_sweep": qsweep,
         }
         print(json.dumps(result), flush=True)
     if world > 1:
