@@ -254,6 +254,64 @@ def quant_sweep(device, hbm_peak):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)", "cases": out}
 
 
+# ----------------------------------------------------------------- C4: Qwen-2.5-7B block linears
+def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
+    """BASELINE configs[3] on one GPU: the Qwen-2.5-7B transformer-block linears
+    (q, k, v, o: 3584 -> 3584/512/512/3584 as QuantLinear; gate/up/down
+    3584 -> 18944 -> 3584 as the fused SwiGLU driver) fwd+bwd with the
+    compressed (int8 stochastic) activation contexts, 8192 tokens, bf16
+    activations, synthetic inputs with outlier channels; the attention core
+    (softmax) is not part of the path.  zero_grad + fwd + bwd + controller."""
+    import torch
+    from paper_2503_08040_b200 import linear
+    H, F, KV = 3584, 18944, 512
+    rng = torch.Generator(device="cpu")
+    rng.manual_seed(11)
+
+    def w(o, i):
+        return (torch.randn(o, i, generator=rng) * 0.02).numpy()
+    qkvo = [linear.QuantLinear(w(o, H), tokens, layer_id=10 + n, threshold_init=30.0)
+            for n, o in enumerate((H, KV, KV, H))]
+    mlp = linear.GluMlp(w(F, H), w(F, H), w(H, F), tokens, act_dtype=torch.bfloat16,
+                        mid_dtype=torch.bfloat16, exact=False, layer_id_base=20, threshold_init=30.0)
+    mlp.set_thresholds(30.0, 3.0)
+    x = make_activations(tokens, H, 31, device, torch.bfloat16)
+    attn = make_activations(tokens, H, 32, device, torch.bfloat16)
+    gys = {H: make_grads(tokens, H, 33, device, torch.bfloat16),
+           KV: make_grads(tokens, KV, 34, device, torch.bfloat16)}
+    outs = {H: torch.empty(tokens, H, device=device, dtype=torch.bfloat16),
+            KV: torch.empty(tokens, KV, device=device, dtype=torch.bfloat16)}
+    gx = torch.empty(tokens, H, device=device, dtype=torch.bfloat16)
+
+    def step(i):
+        for n, l in enumerate(qkvo):
+            l.zero_grad()
+            o = l.out_features
+            l.forward(attn if n == 3 else x, i, out=outs[o])
+            l.backward(gys[o], i, out=gx)
+            l.controller_step()
+        mlp.zero_grad()
+        mlp.forward(x, i, 0, out=outs[H])
+        mlp.backward(gys[H], i, 0, out=gx)
+        mlp.controller_step()
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for i in range(steps):
+        step(warmup + i)
+    e1.record(s)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / steps * 1e-3
+    ops = 2 * tokens * (2 * H * H + 2 * H * KV + 3 * H * F) * 3
+    rates = {f"{n}": round(l.controller_state()[0], 4) for n, l in zip("qkvo", qkvo)}
+    return {"workload": "Qwen-2.5-7B block linears q/k/v/o + SwiGLU MLP, fwd+bwd, 8192 tokens, 1 GPU",
+            "tokens_per_s": round(tokens / t, 1), "ms_per_step": round(t * 1e3, 3),
+            "gemm_TOPS_effective": round(ops / t / 1e12, 1), "fallback_rates_qkvo": rates}
+
+
 # ----------------------------------------------------------------- GEMM sweep
 def gemm_sweep(device):
     import torch
@@ -442,7 +500,7 @@ def run_ours(args, rank, world, local):
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
-        sweep = qsweep = None
+        sweep = qsweep = c4 = None
         if not args.no_sweep:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
                 qsweep = quant_sweep(device, peaks.get("hbm_gbs", 6522.1))
@@ -452,6 +510,10 @@ def run_ours(args, rank, world, local):
                 sweep = gemm_sweep(device)
             except Exception as ex:  # pragma: no cover
                 sweep = {"error": str(ex)[:200]}
+            try:
+                c4 = qwen_block_linears(device)
+            except Exception as ex:  # pragma: no cover
+                c4 = {"error": str(ex)[:200]}
 
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -488,6 +550,7 @@ def run_ours(args, rank, world, local):
             "clocks": clk.summary(),
             "gemm_sweep": sweep,
             "quant_sweep": qsweep,
+            "qwen_block_c4": c4,
         }
         print(json.dumps(result), flush=True)
     if world > 1:

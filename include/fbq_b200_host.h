@@ -96,6 +96,37 @@ int fbq_mlp_get_grads(void* mlp, float* g_gate, float* g_up, float* g_down);
 /* rates[2] = last fallback rate of gate/up and down; thresholds[2] likewise */
 int fbq_mlp_get_controller(void* mlp, double* rates, double* thresholds);
 
+/* ---- one fallback-quantized linear layer: QuantLinearLayer (trainsim.hpp:38-73,
+ * trainsim.cpp:61-135) with 128 x 128 blocks, 8-bit operands, the stochastic X
+ * context, threshold fallback and the delay-threshold controller on device.
+ * Layer RNG streams: layer_seed(seed, layer_id, tag 0 = context / 1 = dY, step). */
+typedef struct fbq_linear_config {
+  int64_t in_features;    /* K of the forward GEMM (% 16 == 0) */
+  int64_t out_features;   /* N of the forward GEMM (% 16 == 0) */
+  int64_t max_tokens;     /* capacity of the device workspaces */
+  int act_dtype;          /* FBQ_F32 / FBQ_BF16: x, dY, y, dX */
+  int epilogue;           /* FBQ_EPI_EXACT (bit-exact) or FBQ_EPI_FMA */
+  int layer_id;           /* QuantLinearLayer layer_id (RNG stream) */
+  uint64_t seed;          /* 0x5eed (QuantConfig::seed) */
+  double threshold_init;  /* 1.0 */
+  double r_min, r_max, alpha; /* 0.1, 0.3, 1.3 */
+} fbq_linear_config;
+void fbq_linear_default_config(fbq_linear_config* cfg);
+/* weight: host fp32, out_features x in_features (row-major, like the reference) */
+void* fbq_linear_create(const fbq_linear_config* cfg, const float* weight);
+void fbq_linear_destroy(void* linear);
+/* y = forward(x) (device buffers, tokens x in -> tokens x out); keeps the context */
+int fbq_linear_forward_device(void* linear, const void* x, int64_t tokens, int64_t row_offset,
+                              int step, void* y, fbq_stream_t stream);
+/* dX = backward(dY); accumulates dW (fp32, device, fbq_linear_grad_ptr) */
+int fbq_linear_backward_device(void* linear, const void* gy, int64_t tokens, int64_t row_offset,
+                               int step, void* gx, fbq_stream_t stream);
+int fbq_linear_controller_step(void* linear, fbq_stream_t stream);
+int fbq_linear_zero_grad(void* linear, fbq_stream_t stream);
+float* fbq_linear_grad_ptr(void* linear);
+/* last observed fallback rate and the current threshold (synchronous read) */
+int fbq_linear_get_controller(void* linear, double* last_rate, double* threshold);
+
 #ifdef __cplusplus
 }
 #endif

@@ -426,3 +426,65 @@ class RefMlp:
         if getattr(self, "h", None):
             self.lib.ref_mlp_destroy(self.h)
             self.h = None
+
+
+class RefLinear:
+    """The reference's own QuantLinearLayer (trainsim.cpp:61-135), block 128,
+    through oracle/_ref (test infrastructure)."""
+
+    def __init__(self, w, threshold=1.0, layer_id=0, g=128):
+        r = REF_oracle()
+        if r is None:
+            raise FileNotFoundError("oracle/_ref not built")
+        lib = r._l.lib
+        self.lib = lib
+        lib.ref_linear_create.restype = C.c_void_p
+        lib.ref_linear_create.argtypes = [F32, i64, i64, i64, dbl, cint]
+        lib.ref_linear_destroy.argtypes = [C.c_void_p]
+        lib.ref_linear_forward.argtypes = [C.c_void_p, F32, i64, cint, F32]
+        lib.ref_linear_backward.argtypes = [C.c_void_p, F32, i64, cint, F32]
+        lib.ref_linear_grad.argtypes = [C.c_void_p, F32]
+        lib.ref_linear_controller.argtypes = [C.c_void_p, F64, F64]
+        lib.ref_linear_zero_grad.argtypes = [C.c_void_p]
+        self.w = np.ascontiguousarray(w, np.float32)
+        self.out_features, self.in_features = self.w.shape
+        self.h = lib.ref_linear_create(self.w, self.out_features, self.in_features, g, threshold,
+                                       layer_id)
+        if not self.h:
+            raise RuntimeError(r._err().decode())
+        self._err = r._err
+
+    def _rc(self, rc):
+        if rc:
+            raise RuntimeError(self._err().decode())
+
+    def forward(self, x, step):
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.zeros((x.shape[0], self.out_features), np.float32)
+        self._rc(self.lib.ref_linear_forward(self.h, x, x.shape[0], step, y))
+        return y
+
+    def backward(self, gy, step):
+        gy = np.ascontiguousarray(gy, np.float32)
+        gx = np.zeros((gy.shape[0], self.in_features), np.float32)
+        self._rc(self.lib.ref_linear_backward(self.h, gy, gy.shape[0], step, gx))
+        return gx
+
+    def grad(self):
+        g = np.zeros_like(self.w)
+        self._rc(self.lib.ref_linear_grad(self.h, g))
+        return g
+
+    def controller_step(self):
+        rate = np.zeros(1)
+        th = np.zeros(1)
+        self._rc(self.lib.ref_linear_controller(self.h, rate, th))
+        return float(rate[0]), float(th[0])
+
+    def zero_grad(self):
+        self._rc(self.lib.ref_linear_zero_grad(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_linear_destroy(self.h)
+            self.h = None

@@ -360,4 +360,63 @@ int ref_mlp_controller(void* h, double* rates3, double* thresholds3) {
     });
 }
 
+// ---------------------------------------------------------------------------
+// One QuantLinearLayer (trainsim.hpp:38-73, trainsim.cpp:61-135), block side g:
+// the reference a single fallback-quantized linear is checked against.
+struct RefLinear {
+    QuantConfig cfg;
+    std::unique_ptr<QuantLinearLayer> l;
+    int64_t in = 0, out = 0;
+};
+
+void* ref_linear_create(const float* w, int64_t out_features, int64_t in_features, int64_t g,
+                        double threshold, int layer_id) {
+    try {
+        auto* r = new RefLinear;
+        r->cfg.block = g;
+        r->cfg.threshold_init = threshold;
+        r->in = in_features;
+        r->out = out_features;
+        r->l = std::make_unique<QuantLinearLayer>("linear", layer_id,
+                                                  make_dense(w, out_features, in_features), r->cfg);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_linear_destroy(void* h) { delete static_cast<RefLinear*>(h); }
+int ref_linear_forward(void* h, const float* x, int64_t tokens, int step, float* y) {
+    return guarded([&] {
+        auto* r = static_cast<RefLinear*>(h);
+        const DenseMatrix out = r->l->forward(make_dense(x, tokens, r->in), step);
+        std::memcpy(y, out.data(), out.size() * sizeof(float));
+    });
+}
+int ref_linear_backward(void* h, const float* gy, int64_t tokens, int step, float* gx) {
+    return guarded([&] {
+        auto* r = static_cast<RefLinear*>(h);
+        const DenseMatrix out = r->l->backward(make_dense(gy, tokens, r->out), step);
+        std::memcpy(gx, out.data(), out.size() * sizeof(float));
+    });
+}
+int ref_linear_grad(void* h, float* gw) {
+    return guarded([&] {
+        auto* r = static_cast<RefLinear*>(h);
+        std::memcpy(gw, r->l->grad_weight().data(), r->l->grad_weight().size() * 4);
+    });
+}
+// last observed rate, then controller_step (trainsim.cpp:129-133) and the new threshold
+int ref_linear_controller(void* h, double* rate, double* threshold) {
+    return guarded([&] {
+        auto* r = static_cast<RefLinear*>(h);
+        *rate = r->l->last_fallback_rate();
+        r->l->controller_step();
+        *threshold = r->l->threshold();
+    });
+}
+int ref_linear_zero_grad(void* h) {
+    return guarded([&] { static_cast<RefLinear*>(h)->l->zero_grad(); });
+}
+
 } // extern "C"

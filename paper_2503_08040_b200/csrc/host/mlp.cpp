@@ -429,6 +429,92 @@ struct Mlp {
   }
 };
 
+// One fallback-quantized linear layer on the device: QuantLinearLayer
+// (trainsim.cpp:61-135) with 128 x 128 blocks.
+//   forward   RTN(W) (serves fwd K-major and dgrad MN-major), K1(X): threshold
+//             fallback codes + the stochastic context in one pass, Y = fallback_gemm
+//   backward  K2(dY), dX = bqg(dY, W), dW += bqg(dY^T, ctx)
+struct QuantLinear {
+  fbq_linear_config c;
+  int64_t In, Out, T, ldIn, ldOut, gIn, gOut, gT;
+  DevBuf w, g, w_codes, w_scales, x_codes, x_scales, x_res, x_res_scales, x_mask, ctx, gy_codes,
+      gy_scales, theta, count, rate;
+  int64_t last_blocks = 1;
+
+  QuantLinear(const fbq_linear_config& cfg, const float* wt) : c(cfg) {
+    In = c.in_features;
+    Out = c.out_features;
+    T = c.max_tokens;
+    if (In <= 0 || Out <= 0 || T <= 0) throw CudaError(FBQ_ERR_SHAPE, "bad linear shape");
+    if (In % 16 || Out % 16) throw CudaError(FBQ_ERR_UNSUPPORTED, "need in/out features % 16 == 0");
+    ldIn = ld16(In);
+    ldOut = ld16(Out);
+    gIn = cdiv(In, 128);
+    gOut = cdiv(Out, 128);
+    gT = cdiv(T, 128);
+    w = DevBuf(Out * In * 4);
+    g = DevBuf(Out * In * 4);
+    CU_TRY(cudaMemcpy(w.p, wt, Out * In * 4, cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemset(g.p, 0, Out * In * 4));
+    w_codes = DevBuf(Out * ldIn);
+    w_scales = DevBuf(gOut * gIn * 4);
+    x_codes = DevBuf(T * ldIn);
+    x_res = DevBuf(T * ldIn);
+    ctx = DevBuf(T * ldIn);
+    x_scales = DevBuf(gT * gIn * 4);
+    x_res_scales = DevBuf(gT * gIn * 4);
+    x_mask = DevBuf(cdiv(gT * gIn, 32) * 4);
+    gy_codes = DevBuf(T * ldOut);
+    gy_scales = DevBuf(gT * gOut * 4);
+    theta = DevBuf(sizeof(double));
+    count = DevBuf(sizeof(int32_t));
+    rate = DevBuf(sizeof(double));
+    CU_TRY(cudaMemcpy(theta.p, &c.threshold_init, sizeof(double), cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemset(count.p, 0, sizeof(int32_t)));
+    CU_TRY(cudaMemset(rate.p, 0, sizeof(double)));
+  }
+
+  void forward(const void* x, int64_t tok, int64_t row_off, int step, void* y, cudaStream_t s) {
+    if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
+    if (tok == 0) return;
+    // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97)
+    FBQ_TRY(fbq_cuda_quantize_rtn(w.p, FBQ_F32, Out, In, In, w_codes.as<int8_t>(), ldIn,
+                                  w_scales.as<float>(), s));
+    // score_blocks + mask_threshold + fallback_quantize + the SR context (trainsim.cpp:80-102)
+    FBQ_TRY(fbq_cuda_quantize_linear_input(
+        x, c.act_dtype, tok, In, In, FBQ_MASK_THRESHOLD, c.threshold_init, theta.as<double>(),
+        x_mask.as<uint32_t>(), x_codes.as<int8_t>(), ldIn, x_scales.as<float>(),
+        x_res.as<int8_t>(), x_res_scales.as<float>(), count.as<int32_t>(), ctx.as<int8_t>(),
+        layer_seed(c.seed, c.layer_id, 0, step), nullptr, 0, row_off, s));
+    FBQ_TRY(fbq_cuda_gemm(x_codes.as<int8_t>(), ldIn, x_scales.as<float>(), FBQ_K_MAJOR,
+                          w_codes.as<int8_t>(), ldIn, w_scales.as<float>(), FBQ_K_MAJOR,
+                          x_mask.as<uint32_t>(), x_res.as<int8_t>(), x_res_scales.as<float>(), tok,
+                          Out, In, y, c.act_dtype, Out, 0, c.epilogue, s));
+    last_blocks = cdiv(tok, 128) * gIn;
+  }
+
+  void backward(const void* gy, int64_t tok, int64_t row_off, int step, void* gx, cudaStream_t s) {
+    if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
+    if (tok == 0) return;
+    FBQ_TRY(fbq_cuda_quantize_stochastic(gy, c.act_dtype, tok, Out, Out,
+                                         layer_seed(c.seed, c.layer_id, 1, step), row_off,
+                                         gy_codes.as<int8_t>(), ldOut, gy_scales.as<float>(), s));
+    // grad_x = bqg(q(dY), q(W)): W codes (Out x In) read MN-major (trainsim.cpp:121-122)
+    FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldOut, gy_scales.as<float>(), FBQ_K_MAJOR,
+                          w_codes.as<int8_t>(), ldIn, w_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
+                          nullptr, nullptr, tok, In, Out, gx, c.act_dtype, In, 0, c.epilogue, s));
+    // grad_w += bqg(q(dY)^T, ctx) (trainsim.cpp:124-125)
+    FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldOut, gy_scales.as<float>(), FBQ_MN_MAJOR,
+                          ctx.as<int8_t>(), ldIn, x_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
+                          nullptr, nullptr, Out, In, tok, g.p, FBQ_F32, In, 1, c.epilogue, s));
+  }
+
+  void controller(cudaStream_t s) {
+    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), count.as<int32_t>(), last_blocks,
+                                       c.r_min, c.r_max, c.alpha, rate.as<double>(), s));
+  }
+};
+
 thread_local std::string g_host_err;
 
 template <class F>
@@ -598,3 +684,67 @@ int fbq_mlp_get_controller(void* m, double* rates, double* thresholds) {
 }
 
 }  // extern "C"
+
+void fbq_linear_default_config(fbq_linear_config* cfg) {
+  if (!cfg) return;
+  *cfg = fbq_linear_config{};
+  cfg->act_dtype = FBQ_BF16;
+  cfg->epilogue = FBQ_EPI_FMA;
+  cfg->layer_id = 0;
+  cfg->seed = 0x5eedull;
+  cfg->threshold_init = 1.0;
+  cfg->r_min = 0.1;
+  cfg->r_max = 0.3;
+  cfg->alpha = 1.3;
+}
+
+void* fbq_linear_create(const fbq_linear_config* cfg, const float* weight) {
+  if (!cfg || !weight) {
+    g_host_err = "fbq_linear_create: null argument";
+    return nullptr;
+  }
+  try {
+    return new QuantLinear(*cfg, weight);
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return nullptr;
+  }
+}
+void fbq_linear_destroy(void* l) { delete static_cast<QuantLinear*>(l); }
+
+int fbq_linear_forward_device(void* l, const void* x, int64_t tokens, int64_t row_offset, int step,
+                              void* y, fbq_stream_t stream) {
+  if (!l || (tokens > 0 && (!x || !y)) || row_offset < 0) return FBQ_ERR_ARG;
+  return guarded([&] {
+    static_cast<QuantLinear*>(l)->forward(x, tokens, row_offset, step, y,
+                                          reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int fbq_linear_backward_device(void* l, const void* gy, int64_t tokens, int64_t row_offset,
+                               int step, void* gx, fbq_stream_t stream) {
+  if (!l || (tokens > 0 && (!gy || !gx)) || row_offset < 0) return FBQ_ERR_ARG;
+  return guarded([&] {
+    static_cast<QuantLinear*>(l)->backward(gy, tokens, row_offset, step, gx,
+                                           reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int fbq_linear_controller_step(void* l, fbq_stream_t stream) {
+  if (!l) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<QuantLinear*>(l)->controller(reinterpret_cast<cudaStream_t>(stream)); });
+}
+int fbq_linear_zero_grad(void* l, fbq_stream_t stream) {
+  if (!l) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* q = static_cast<QuantLinear*>(l);
+    CU_TRY(cudaMemsetAsync(q->g.p, 0, q->Out * q->In * 4, reinterpret_cast<cudaStream_t>(stream)));
+  });
+}
+float* fbq_linear_grad_ptr(void* l) { return l ? static_cast<QuantLinear*>(l)->g.as<float>() : nullptr; }
+int fbq_linear_get_controller(void* l, double* last_rate, double* threshold) {
+  if (!l || !last_rate || !threshold) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* q = static_cast<QuantLinear*>(l);
+    CU_TRY(cudaMemcpy(last_rate, q->rate.p, sizeof(double), cudaMemcpyDeviceToHost));
+    CU_TRY(cudaMemcpy(threshold, q->theta.p, sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}

@@ -58,6 +58,30 @@ for _n, (_r, _a) in _sigs.items():
     _f.argtypes = _a
 
 
+class LinearConfig(C.Structure):
+    _fields_ = [("in_features", C.c_int64), ("out_features", C.c_int64), ("max_tokens", C.c_int64),
+                ("act_dtype", C.c_int), ("epilogue", C.c_int), ("layer_id", C.c_int),
+                ("seed", C.c_uint64), ("threshold_init", C.c_double), ("r_min", C.c_double),
+                ("r_max", C.c_double), ("alpha", C.c_double)]
+
+
+for _name, (_res, _args) in {
+    "fbq_linear_default_config": (None, [C.c_void_p]),
+    "fbq_linear_create": (C.c_void_p, [C.c_void_p, _F32P]),
+    "fbq_linear_destroy": (None, [C.c_void_p]),
+    "fbq_linear_forward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                            C.c_void_p, C.c_void_p]),
+    "fbq_linear_backward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                             C.c_void_p, C.c_void_p]),
+    "fbq_linear_controller_step": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_linear_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_linear_grad_ptr": (C.c_void_p, [C.c_void_p]),
+    "fbq_linear_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+}.items():
+    _f = getattr(lib, _name)
+    _f.restype, _f.argtypes = _res, _args
+
+
 def _check(st, what):
     if st != K.FBQ_OK:
         raise K.FbqError(st, f"{what} ({lib.fbq_host_last_error().decode()})")
@@ -197,3 +221,63 @@ class GluMlp:
         t = (C.c_double * 2)()
         _check(lib.fbq_mlp_get_controller(self._h, r, t), "get_controller")
         return list(r), list(t)
+
+
+class QuantLinear:
+    """One fallback-quantized linear layer on B200 -- the reference's
+    QuantLinearLayer (trainsim.hpp:38-73, trainsim.cpp:61-135): forward keeps the
+    stochastic X context, backward returns dX and accumulates dW."""
+
+    def __init__(self, weight, max_tokens, *, act_dtype=torch.bfloat16, exact=False,
+                 threshold_init=1.0, seed=0x5EED, layer_id=0, r_min=0.1, r_max=0.3, alpha=1.3):
+        w = np.ascontiguousarray(np.asarray(weight, np.float32))
+        self.out_features, self.in_features = w.shape
+        cfg = LinearConfig()
+        lib.fbq_linear_default_config(C.byref(cfg))
+        cfg.in_features, cfg.out_features, cfg.max_tokens = self.in_features, self.out_features, max_tokens
+        cfg.act_dtype = {torch.float32: K.FBQ_F32, torch.bfloat16: K.FBQ_BF16}[act_dtype]
+        cfg.epilogue = K.FBQ_EPI_EXACT if exact else K.FBQ_EPI_FMA
+        cfg.layer_id, cfg.seed, cfg.threshold_init = layer_id, seed, threshold_init
+        cfg.r_min, cfg.r_max, cfg.alpha = r_min, r_max, alpha
+        self.cfg, self.act_dtype, self.max_tokens = cfg, act_dtype, max_tokens
+        h = lib.fbq_linear_create(C.byref(cfg), w)
+        if not h:
+            raise K.FbqError(K.FBQ_ERR_ARG, f"fbq_linear_create ({lib.fbq_host_last_error().decode()})")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.fbq_linear_destroy(h)
+            self._h = None
+
+    def forward(self, x: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        x = x.contiguous()
+        y = out if out is not None else torch.empty(x.shape[0], self.out_features, device=x.device,
+                                                    dtype=self.act_dtype)
+        _check(lib.fbq_linear_forward_device(self._h, x.data_ptr(), x.shape[0], row_offset, step,
+                                             y.data_ptr(), _stream()), "linear forward")
+        return y
+
+    def backward(self, gy: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        gy = gy.contiguous()
+        gx = out if out is not None else torch.empty(gy.shape[0], self.in_features, device=gy.device,
+                                                     dtype=self.act_dtype)
+        _check(lib.fbq_linear_backward_device(self._h, gy.data_ptr(), gy.shape[0], row_offset, step,
+                                              gx.data_ptr(), _stream()), "linear backward")
+        return gx
+
+    def controller_step(self):
+        _check(lib.fbq_linear_controller_step(self._h, _stream()), "linear controller_step")
+
+    def zero_grad(self):
+        _check(lib.fbq_linear_zero_grad(self._h, _stream()), "linear zero_grad")
+
+    def grad(self) -> torch.Tensor:
+        return torch.as_tensor(_DevArray(lib.fbq_linear_grad_ptr(self._h),
+                                         (self.out_features, self.in_features)), device="cuda")
+
+    def controller_state(self):
+        r, t = C.c_double(), C.c_double()
+        _check(lib.fbq_linear_get_controller(self._h, C.byref(r), C.byref(t)), "linear get_controller")
+        return r.value, t.value

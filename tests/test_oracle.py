@@ -186,3 +186,24 @@ def test_reference_backends_bit_equal(ref):
         want = c0.astype(np.int64)
         want[:, :n] += a[:, :k].astype(np.int64) @ b[:, :n].astype(np.int64)
         assert np.array_equal(outs[0], want)
+
+
+def test_ref_linear_forward_matches_restated_composition():
+    """The QuantLinearLayer shim (oracle/ref_capi.cpp) against the C restatement
+    composed like trainsim.cpp:80-98: threshold mask, fallback_quantize,
+    quantize_rtn(W^T), fallback_gemm."""
+    from oracle.oracle import C_oracle, REF_oracle, RefLinear
+    if REF_oracle() is None:
+        pytest.skip("oracle/_ref not built")
+    orc = C_oracle()
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((256, 384)).astype(np.float32)
+    x[:, 5] *= 40.0
+    w = (rng.standard_normal((128, 384)) * 0.05).astype(np.float32)
+    y = RefLinear(w, threshold=4.0).forward(x, 0)
+    mask = orc.mask_threshold(orc.score_blocks_absmax(x), 4.0)
+    c, s, rc, rs = orc.fallback_quantize(x, mask)
+    wc, ws = orc.quantize_rtn(w)
+    bc, bs = orc.transpose_qt(wc, ws)
+    want = orc.block_gemm(c, s, bc, bs, mask=mask, res_codes=rc, res_scales=rs)
+    assert np.array_equal(y.view(np.int32), want.view(np.int32))
