@@ -358,7 +358,28 @@ def gemm_sweep(device):
         out[name] = row
         del x, w, wq, y, xi, wi
         torch.cuda.empty_cache()
-    return {"unit": "TOPS effective (2MNK/t; residual MMAs not credited)", "shapes": out}
+    # C5 M sweep on the Llama-3.1-70B MLP shape (8192 -> 28672), 5 % fallback,
+    # next to cuBLAS bf16 of the same shape
+    N, K = 28672, 8192
+    w = torch.randn(N, K, device=device) * 0.02
+    wq = fbq.transpose(fbq.quantize_rtn(w))
+    wb = w.to(torch.bfloat16)
+    msweep = {}
+    for M in (1024, 4096, 16384, 65536):
+        x = make_activations(M, K, 12, device, torch.bfloat16)
+        fa = fbq.fallback_quantize(x, fbq.mask_topk(fbq.score_blocks(x), 0.05))
+        y = torch.empty(M, N, device=device, dtype=torch.bfloat16)
+        iters = 3 if M >= 65536 else 10
+        t = timeit(lambda: fbq.fallback_gemm(fa, wq, out=y, exact=False), iters=iters)
+        tb = timeit(lambda: torch.matmul(x, wb.t(), out=y), iters=iters)
+        msweep[f"M={M}"] = {"fbq_TOPS": round(2 * M * N * K / t / 1e12, 1),
+                            "cublas_bf16_TFLOPS": round(2 * M * N * K / tb / 1e12, 1)}
+        del x, fa, y
+        torch.cuda.empty_cache()
+    del w, wq, wb
+    torch.cuda.empty_cache()
+    return {"unit": "TOPS effective (2MNK/t; residual MMAs not credited)", "shapes": out,
+            "c5_m_sweep_28672x8192_rate_0.05": msweep}
 
 
 # ----------------------------------------------------------------- our arm
