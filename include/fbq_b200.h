@@ -76,6 +76,15 @@ int fbq_synchronize(void);
 int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
                           float* amax, fbq_stream_t stream);
 
+/* mask_topk -- policy.cpp:56-71 / policy.hpp:30-31: exactly k = ceil(rate * n)
+ * (clamped to n) blocks with the largest scores, ties toward the lower block
+ * index, written as a bitmap (bit b = block b; the whole bitmap is rewritten).
+ * scores: the n fp32 block absmaxes of fbq_cuda_block_absmax (non-negative).
+ * masked_count (optional) receives k.  One device pass, no host round trip;
+ * rate outside [0, 1] -> FBQ_ERR_ARG (policy.cpp:57). */
+int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* mask_bits,
+                       int32_t* masked_count, fbq_stream_t stream);
+
 /* K1: fused quantize_rtn (quant.cpp:36-53) + score_blocks(AbsMax) + mask_threshold
  * (policy.cpp:73-80) + fallback_quantize (quant.cpp:128-176, quant.hpp:74-75) +
  * masked-block count (mask_rate numerator, policy.cpp:82-87) + optional fused

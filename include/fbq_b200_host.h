@@ -110,6 +110,8 @@ typedef struct fbq_linear_config {
   uint64_t seed;          /* 0x5eed (QuantConfig::seed) */
   double threshold_init;  /* 1.0 */
   double r_min, r_max, alpha; /* 0.1, 0.3, 1.3 */
+  int fallback_mode;      /* FallbackMode (trainsim.hpp:15): 0 Threshold, 1 FixedRate, 2 Off */
+  double fixed_rate;      /* FixedRate: mask_topk(score_blocks(x), fixed_rate) on the device */
 } fbq_linear_config;
 void fbq_linear_default_config(fbq_linear_config* cfg);
 /* weight: host fp32, out_features x in_features (row-major, like the reference) */

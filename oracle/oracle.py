@@ -432,14 +432,14 @@ class RefLinear:
     """The reference's own QuantLinearLayer (trainsim.cpp:61-135), block 128,
     through oracle/_ref (test infrastructure)."""
 
-    def __init__(self, w, threshold=1.0, layer_id=0, g=128):
+    def __init__(self, w, threshold=1.0, layer_id=0, g=128, fallback_mode="threshold", fixed_rate=0.0):
         r = REF_oracle()
         if r is None:
             raise FileNotFoundError("oracle/_ref not built")
         lib = r._l.lib
         self.lib = lib
         lib.ref_linear_create.restype = C.c_void_p
-        lib.ref_linear_create.argtypes = [F32, i64, i64, i64, dbl, cint]
+        lib.ref_linear_create.argtypes = [F32, i64, i64, i64, dbl, cint, cint, dbl]
         lib.ref_linear_destroy.argtypes = [C.c_void_p]
         lib.ref_linear_forward.argtypes = [C.c_void_p, F32, i64, cint, F32]
         lib.ref_linear_backward.argtypes = [C.c_void_p, F32, i64, cint, F32]
@@ -448,8 +448,9 @@ class RefLinear:
         lib.ref_linear_zero_grad.argtypes = [C.c_void_p]
         self.w = np.ascontiguousarray(w, np.float32)
         self.out_features, self.in_features = self.w.shape
+        mode = {"threshold": 0, "fixed_rate": 1, "off": 2}[fallback_mode]
         self.h = lib.ref_linear_create(self.w, self.out_features, self.in_features, g, threshold,
-                                       layer_id)
+                                       layer_id, mode, fixed_rate)
         if not self.h:
             raise RuntimeError(r._err().decode())
         self._err = r._err

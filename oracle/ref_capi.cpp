@@ -370,11 +370,14 @@ struct RefLinear {
 };
 
 void* ref_linear_create(const float* w, int64_t out_features, int64_t in_features, int64_t g,
-                        double threshold, int layer_id) {
+                        double threshold, int layer_id, int fallback_mode, double fixed_rate) {
     try {
         auto* r = new RefLinear;
         r->cfg.block = g;
         r->cfg.threshold_init = threshold;
+        r->cfg.fallback_mode = fallback_mode == 1 ? FallbackMode::FixedRate
+                             : fallback_mode == 2 ? FallbackMode::Off : FallbackMode::Threshold;
+        r->cfg.fixed_rate = fixed_rate;
         r->in = in_features;
         r->out = out_features;
         r->l = std::make_unique<QuantLinearLayer>("linear", layer_id,

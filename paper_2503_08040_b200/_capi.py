@@ -33,6 +33,7 @@ _SIGS = {
     "fbq_last_cuda_error": (cint, []),
     "fbq_block_side": (cint, []),
     "fbq_cuda_block_absmax": (cint, [vp, cint, i64, i64, i64, vp, vp]),
+    "fbq_cuda_mask_topk": (cint, [vp, i64, dbl, vp, vp, vp]),
     "fbq_cuda_quantize_fallback": (cint, [vp, cint, i64, i64, i64, cint, dbl, vp, vp, i64, vp, vp,
                                           vp, vp, vp, vp, u64, i64, vp]),
     "fbq_cuda_quantize_rtn": (cint, [vp, cint, i64, i64, i64, vp, i64, vp, vp]),

@@ -1,6 +1,7 @@
 // extern "C" boundary: argument checking + dispatch to the sm_100a kernels.
 // See include/fbq_b200.h for the contract of every entry point.
 #include <cuda_runtime.h>
+#include <cmath>
 #include <cstdint>
 
 #include "../../include/fbq_b200.h"
@@ -215,6 +216,18 @@ int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, 
   return fbq_cuda_quantize_fallback(x, dtype, rows, cols, ldx, FBQ_MASK_NONE, 1.0, nullptr,
                                     nullptr, cols, nullptr, nullptr, nullptr, nullptr, amax,
                                     nullptr, 0, 0, stream);
+}
+
+int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* mask_bits,
+                       int32_t* masked_count, fbq_stream_t stream) {
+  if (!(rate >= 0.0 && rate <= 1.0)) return FBQ_ERR_ARG;  // policy.cpp:57
+  if (n < 0 || n >= (1ll << 32)) return FBQ_ERR_SHAPE;
+  if (n == 0) return FBQ_OK;
+  if (!scores || !mask_bits) return FBQ_ERR_ARG;
+  int64_t k = (int64_t)std::ceil(rate * (double)n);  // policy.cpp:58-59
+  if (k > n) k = n;
+  return cuda_status(fbq::launch_topk(scores, n, k, mask_bits, masked_count,
+                                      reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int fbq_cuda_quantize_rtn(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,

@@ -15,6 +15,7 @@
 // GEMMs read the forward code planes MN-major instead of transposing them.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -438,8 +439,9 @@ struct QuantLinear {
   fbq_linear_config c;
   int64_t In, Out, T, ldIn, ldOut, gIn, gOut, gT;
   DevBuf w, g, w_codes, w_scales, x_codes, x_scales, x_res, x_res_scales, x_mask, ctx, gy_codes,
-      gy_scales, theta, count, rate;
+      gy_scales, theta, count, rate, amax;
   int64_t last_blocks = 1;
+  double last_fixed_rate = 0.0;  // FixedRate / Off: mask_rate of the last forward (k / n)
 
   QuantLinear(const fbq_linear_config& cfg, const float* wt) : c(cfg) {
     In = c.in_features;
@@ -469,6 +471,10 @@ struct QuantLinear {
     theta = DevBuf(sizeof(double));
     count = DevBuf(sizeof(int32_t));
     rate = DevBuf(sizeof(double));
+    amax = DevBuf(gT * gIn * 4);
+    if (c.fallback_mode < 0 || c.fallback_mode > 2) throw CudaError(FBQ_ERR_ARG, "bad fallback_mode");
+    if (c.fallback_mode == 1 && !(c.fixed_rate >= 0.0 && c.fixed_rate <= 1.0))
+      throw CudaError(FBQ_ERR_ARG, "fixed_rate must be in [0, 1]");
     CU_TRY(cudaMemcpy(theta.p, &c.threshold_init, sizeof(double), cudaMemcpyHostToDevice));
     CU_TRY(cudaMemset(count.p, 0, sizeof(int32_t)));
     CU_TRY(cudaMemset(rate.p, 0, sizeof(double)));
@@ -480,12 +486,26 @@ struct QuantLinear {
     // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97)
     FBQ_TRY(fbq_cuda_quantize_rtn(w.p, FBQ_F32, Out, In, In, w_codes.as<int8_t>(), ldIn,
                                   w_scales.as<float>(), s));
-    // score_blocks + mask_threshold + fallback_quantize + the SR context (trainsim.cpp:80-102)
+    // score_blocks + mask (trainsim.cpp:80-93) + fallback_quantize + the SR context (:95-102)
+    int mode = FBQ_MASK_THRESHOLD;
+    const int64_t nblk = cdiv(tok, 128) * gIn;
+    if (c.fallback_mode == 1) {  // FixedRate: score pass, device TopK, then the given mask
+      FBQ_TRY(fbq_cuda_block_absmax(x, c.act_dtype, tok, In, In, amax.as<float>(), s));
+      FBQ_TRY(fbq_cuda_mask_topk(amax.as<float>(), nblk, c.fixed_rate, x_mask.as<uint32_t>(),
+                                 count.as<int32_t>(), s));
+      mode = FBQ_MASK_GIVEN;
+      int64_t k = (int64_t)std::ceil(c.fixed_rate * (double)nblk);
+      last_fixed_rate = nblk ? (double)(k > nblk ? nblk : k) / (double)nblk : 0.0;
+    } else if (c.fallback_mode == 2) {  // Off: an all-zero mask
+      CU_TRY(cudaMemsetAsync(x_mask.p, 0, cdiv(nblk, 32) * 4, s));
+      mode = FBQ_MASK_GIVEN;
+      last_fixed_rate = 0.0;
+    }
     FBQ_TRY(fbq_cuda_quantize_linear_input(
-        x, c.act_dtype, tok, In, In, FBQ_MASK_THRESHOLD, c.threshold_init, theta.as<double>(),
+        x, c.act_dtype, tok, In, In, mode, c.threshold_init, mode == FBQ_MASK_THRESHOLD ? theta.as<double>() : nullptr,
         x_mask.as<uint32_t>(), x_codes.as<int8_t>(), ldIn, x_scales.as<float>(),
-        x_res.as<int8_t>(), x_res_scales.as<float>(), count.as<int32_t>(), ctx.as<int8_t>(),
-        layer_seed(c.seed, c.layer_id, 0, step), nullptr, 0, row_off, s));
+        x_res.as<int8_t>(), x_res_scales.as<float>(), mode == FBQ_MASK_THRESHOLD ? count.as<int32_t>() : nullptr,
+        ctx.as<int8_t>(), layer_seed(c.seed, c.layer_id, 0, step), nullptr, 0, row_off, s));
     FBQ_TRY(fbq_cuda_gemm(x_codes.as<int8_t>(), ldIn, x_scales.as<float>(), FBQ_K_MAJOR,
                           w_codes.as<int8_t>(), ldIn, w_scales.as<float>(), FBQ_K_MAJOR,
                           x_mask.as<uint32_t>(), x_res.as<int8_t>(), x_res_scales.as<float>(), tok,
@@ -510,6 +530,7 @@ struct QuantLinear {
   }
 
   void controller(cudaStream_t s) {
+    if (c.fallback_mode != 0) return;  // trainsim.cpp:129-133: Threshold mode only
     FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), count.as<int32_t>(), last_blocks,
                                        c.r_min, c.r_max, c.alpha, rate.as<double>(), s));
   }
@@ -696,6 +717,8 @@ void fbq_linear_default_config(fbq_linear_config* cfg) {
   cfg->r_min = 0.1;
   cfg->r_max = 0.3;
   cfg->alpha = 1.3;
+  cfg->fallback_mode = 0;
+  cfg->fixed_rate = 0.0;
 }
 
 void* fbq_linear_create(const fbq_linear_config* cfg, const float* weight) {
@@ -744,7 +767,8 @@ int fbq_linear_get_controller(void* l, double* last_rate, double* threshold) {
   if (!l || !last_rate || !threshold) return FBQ_ERR_ARG;
   return guarded([&] {
     auto* q = static_cast<QuantLinear*>(l);
-    CU_TRY(cudaMemcpy(last_rate, q->rate.p, sizeof(double), cudaMemcpyDeviceToHost));
+    if (q->c.fallback_mode == 0) CU_TRY(cudaMemcpy(last_rate, q->rate.p, sizeof(double), cudaMemcpyDeviceToHost));
+    else *last_rate = q->last_fixed_rate;
     CU_TRY(cudaMemcpy(threshold, q->theta.p, sizeof(double), cudaMemcpyDeviceToHost));
   });
 }

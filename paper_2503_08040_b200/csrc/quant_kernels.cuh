@@ -73,7 +73,10 @@ struct DequantParams {
 };
 
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s);
-extern int g_quant_diag;  // 1 = one-block-per-CTA K1 (diagnostics, fbq_debug_set_quant_diag)
+extern int g_quant_diag;
+// mask_topk (policy.cpp:56-71) on device: exactly k blocks (policy_kernels.cu)
+cudaError_t launch_topk(const float* scores, int64_t n, int64_t k, uint32_t* mask_bits,
+                        int32_t* count, cudaStream_t s);  // 1 = one-block-per-CTA K1 (diagnostics, fbq_debug_set_quant_diag)
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
 cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s);

@@ -352,14 +352,25 @@ def mask_topk(scores: torch.Tensor, rate: float) -> torch.Tensor:
     """policy.cpp:56-71: exactly ceil(rate*n) top scores, ties -> lower index."""
     if rate < 0.0 or rate > 1.0:
         raise ValueError("rate must be in [0, 1]")
-    flat = scores.reshape(-1).to(torch.float64)
-    n = flat.numel()
-    k = min(n, math.ceil(rate * n))
-    # stable sort on descending score keeps ascending index among ties
-    order = torch.sort(-flat, stable=True).indices[:k]
-    m = torch.zeros(n, dtype=torch.uint8, device=scores.device)
-    m[order] = 1
-    return m.view(scores.shape)
+    n = scores.numel()
+    if not scores.is_cuda:
+        # host-resident scores: the host policy, like the reference's own
+        # mask_topk; stable sort on descending score keeps ascending index among ties
+        flat = scores.reshape(-1).to(torch.float64)
+        k = min(n, math.ceil(rate * n))
+        order = torch.sort(-flat, stable=True).indices[:k]
+        m = torch.zeros(n, dtype=torch.uint8)
+        m[order] = 1
+        return m.view(scores.shape)
+    # device scores (score_blocks): fbq_cuda_mask_topk, no host round trip.
+    # the AbsMax scores are fp32 values widened to double: exact in fp32
+    flat = scores.reshape(-1).to(torch.float32).contiguous()
+    bits = torch.empty(cdiv(max(n, 1), 32), dtype=torch.int32, device=scores.device)
+    if n:
+        K.call("fbq_cuda_mask_topk", flat.data_ptr(), n, float(rate), bits.data_ptr(), None,
+               _stream())
+    gr, gc = (scores.shape if scores.dim() == 2 else (1, n))
+    return bits_to_mask(bits, gr, gc).view(scores.shape)
 
 
 def mask_rate(mask: torch.Tensor) -> float:

@@ -62,7 +62,8 @@ class LinearConfig(C.Structure):
     _fields_ = [("in_features", C.c_int64), ("out_features", C.c_int64), ("max_tokens", C.c_int64),
                 ("act_dtype", C.c_int), ("epilogue", C.c_int), ("layer_id", C.c_int),
                 ("seed", C.c_uint64), ("threshold_init", C.c_double), ("r_min", C.c_double),
-                ("r_max", C.c_double), ("alpha", C.c_double)]
+                ("r_max", C.c_double), ("alpha", C.c_double), ("fallback_mode", C.c_int),
+                ("fixed_rate", C.c_double)]
 
 
 for _name, (_res, _args) in {
@@ -229,7 +230,8 @@ class QuantLinear:
     stochastic X context, backward returns dX and accumulates dW."""
 
     def __init__(self, weight, max_tokens, *, act_dtype=torch.bfloat16, exact=False,
-                 threshold_init=1.0, seed=0x5EED, layer_id=0, r_min=0.1, r_max=0.3, alpha=1.3):
+                 threshold_init=1.0, seed=0x5EED, layer_id=0, r_min=0.1, r_max=0.3, alpha=1.3,
+                 fallback_mode="threshold", fixed_rate=0.0):
         w = np.ascontiguousarray(np.asarray(weight, np.float32))
         self.out_features, self.in_features = w.shape
         cfg = LinearConfig()
@@ -239,6 +241,8 @@ class QuantLinear:
         cfg.epilogue = K.FBQ_EPI_EXACT if exact else K.FBQ_EPI_FMA
         cfg.layer_id, cfg.seed, cfg.threshold_init = layer_id, seed, threshold_init
         cfg.r_min, cfg.r_max, cfg.alpha = r_min, r_max, alpha
+        cfg.fallback_mode = {"threshold": 0, "fixed_rate": 1, "off": 2}[fallback_mode]
+        cfg.fixed_rate = fixed_rate
         self.cfg, self.act_dtype, self.max_tokens = cfg, act_dtype, max_tokens
         h = lib.fbq_linear_create(C.byref(cfg), w)
         if not h:

@@ -65,3 +65,28 @@ def test_linear_bf16_fast_path_within_tolerance(mods):
     gxr = ref.backward(gyb.float().cpu().numpy(), 0)
     assert rel_fro(y, yr) < 1e-2 and rel_fro(gx, gxr) < 1e-2
     assert rel_fro(dev.grad().cpu().numpy(), ref.grad()) < 1e-5
+
+
+@pytest.mark.parametrize("mode,rate", [("fixed_rate", 0.25), ("fixed_rate", 0.0), ("off", 0.0)])
+def test_linear_fixed_rate_and_off_modes(mods, mode, rate):
+    """FallbackMode::FixedRate (device TopK mask) and Off vs the reference."""
+    import torch
+    linear, RefLinear = mods
+    t, d_in, d_out = 384, 512, 256
+    rng = np.random.default_rng(6)
+    w = (rng.standard_normal((d_out, d_in)) * 0.05).astype(np.float32)
+    dev = linear.QuantLinear(w, t, act_dtype=torch.float32, exact=True, fallback_mode=mode,
+                             fixed_rate=rate, layer_id=2)
+    ref = RefLinear(w, layer_id=2, fallback_mode=mode, fixed_rate=rate)
+    for step in range(2):
+        x = outlier_matrix(t, d_in, seed=40 + step, body=0.5, channels=[1, 300], tokens=[5],
+                           mag_c=15.0, mag_t=30.0)
+        gy = outlier_matrix(t, d_out, seed=50 + step, body=1e-3)
+        y = dev.forward(torch.from_numpy(x).cuda(), step).cpu().numpy()
+        gx = dev.backward(torch.from_numpy(gy).cuda(), step).cpu().numpy()
+        assert np.array_equal(y.view(np.int32), ref.forward(x, step).view(np.int32))
+        assert np.array_equal(gx.view(np.int32), ref.backward(gy, step).view(np.int32))
+        dev.controller_step()
+        rate_r, th_r = ref.controller_step()
+        rate_d, th_d = dev.controller_state()
+        assert rate_d == rate_r and th_d == th_r

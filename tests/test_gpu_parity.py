@@ -238,3 +238,19 @@ def test_gemm_many_tiles_odd_pairs(F, orc):
     assert np.array_equal(host(y).view(np.int32), want.view(np.int32))
     y2 = F.fallback_gemm(fa, F.transpose(wq), exact=False)
     assert rel_fro(host(y2), want) <= FMA_TOL
+
+
+@pytest.mark.parametrize("rate", [0.0, 1e-4, 0.05, 0.2, 0.5, 1.0])
+def test_mask_topk_device_matches_reference(F, orc, rate):
+    """mask_topk (policy.cpp:56-71) on the device: exactly ceil(rate*n) blocks,
+    ties toward the lower index -- on AbsMax scores and on a tie-heavy grid."""
+    import torch
+    x = outlier_matrix(1280, 1664, seed=50, channels=[3, 900], tokens=[77])
+    scores = orc.score_blocks_absmax(x)
+    got = host(F.mask_topk(F.score_blocks(dev(x)), rate))
+    assert np.array_equal(got, orc.mask_topk(scores, rate))
+    # many exact ties: scores from a handful of values
+    rng = np.random.default_rng(int(rate * 1000) + 1)
+    tied = rng.choice(np.array([0.0, 0.5, 1.0, 2.0], np.float32), size=(37, 91)).astype(np.float64)
+    got = host(F.mask_topk(torch.from_numpy(tied).cuda(), rate))
+    assert np.array_equal(got, orc.mask_topk(tied, rate))
