@@ -76,6 +76,25 @@ int fbq_synchronize(void);
 int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
                           float* amax, fbq_stream_t stream);
 
+/* RmsNorm (trainsim.cpp:154-211) with its 10-bit 1 x 128 RTN input context
+ * (QuantConfig::nonlinear_bits / nonlinear_group, trainsim.hpp:26-28).
+ * forward: y = fl(fl(x / rms) * gain), rms = sqrtf(float(sum x^2 / cols) + 1e-6f)
+ *   with the sum of squares accumulated in double in column order (as the
+ *   reference); ctx_codes (int16, rows x ld_ctx) + ctx_scales (rows x
+ *   ceil(cols/128)) = quantize_rtn(x, 1 x 128, 10 bits).  rms_ws: rows floats.
+ * backward: x = dequantize(ctx); gx = float(g*dy*inv - x*corr) (double math,
+ *   row sums in column order); grad_gain[c] += float(float(dy*x) * inv) over the
+ *   rows in order.  row_ws: 2*rows doubles, term_ws: rows*cols floats.
+ * x / dy / y / gx share dtype (FBQ_F32 or FBQ_BF16); cols % 8 == 0, 16-byte
+ * aligned rows, ld_ctx % 8 == 0. */
+int fbq_cuda_rmsnorm_forward(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                             const float* gain, void* y, int64_t ldy, int16_t* ctx_codes,
+                             int64_t ld_ctx, float* ctx_scales, float* rms_ws, fbq_stream_t stream);
+int fbq_cuda_rmsnorm_backward(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales,
+                              const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
+                              const float* gain, void* gx, int64_t ldgx, float* grad_gain,
+                              double* row_ws, float* term_ws, fbq_stream_t stream);
+
 /* mask_topk -- policy.cpp:56-71 / policy.hpp:30-31: exactly k = ceil(rate * n)
  * (clamped to n) blocks with the largest scores, ties toward the lower block
  * index, written as a bitmap (bit b = block b; the whole bitmap is rewritten).

@@ -489,3 +489,54 @@ class RefLinear:
         if getattr(self, "h", None):
             self.lib.ref_linear_destroy(self.h)
             self.h = None
+
+
+class RefRmsNorm:
+    """The reference's own RmsNorm (trainsim.cpp:145-219) through oracle/_ref."""
+
+    def __init__(self, dim):
+        r = REF_oracle()
+        if r is None:
+            raise FileNotFoundError("oracle/_ref not built")
+        lib = r._l.lib
+        self.lib = lib
+        lib.ref_rms_create.restype = C.c_void_p
+        lib.ref_rms_create.argtypes = [i64]
+        lib.ref_rms_destroy.argtypes = [C.c_void_p]
+        lib.ref_rms_forward.argtypes = [C.c_void_p, F32, i64, F32]
+        lib.ref_rms_backward.argtypes = [C.c_void_p, F32, i64, F32]
+        lib.ref_rms_state.argtypes = [C.c_void_p, F32, F32]
+        lib.ref_rms_sgd.argtypes = [C.c_void_p, dbl]
+        self.dim = dim
+        self.h = lib.ref_rms_create(dim)
+        self._err = r._err
+
+    def _rc(self, rc):
+        if rc:
+            raise RuntimeError(self._err().decode())
+
+    def forward(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.zeros_like(x)
+        self._rc(self.lib.ref_rms_forward(self.h, x, x.shape[0], y))
+        return y
+
+    def backward(self, gy):
+        gy = np.ascontiguousarray(gy, np.float32)
+        gx = np.zeros_like(gy)
+        self._rc(self.lib.ref_rms_backward(self.h, gy, gy.shape[0], gx))
+        return gx
+
+    def state(self):
+        g = np.zeros(self.dim, np.float32)
+        gg = np.zeros(self.dim, np.float32)
+        self._rc(self.lib.ref_rms_state(self.h, g, gg))
+        return g, gg
+
+    def apply_sgd(self, lr):
+        self._rc(self.lib.ref_rms_sgd(self.h, lr))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_rms_destroy(self.h)
+            self.h = None

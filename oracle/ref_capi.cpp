@@ -422,4 +422,48 @@ int ref_linear_zero_grad(void* h) {
     return guarded([&] { static_cast<RefLinear*>(h)->l->zero_grad(); });
 }
 
+// ---------------------------------------------------------------------------
+// RmsNorm (trainsim.hpp:75-97) with the default QuantConfig (10-bit 1 x 128 context).
+struct RefRms {
+    QuantConfig cfg;
+    std::unique_ptr<RmsNorm> n;
+    int64_t dim = 0;
+};
+void* ref_rms_create(int64_t dim) {
+    try {
+        auto* r = new RefRms;
+        r->dim = dim;
+        r->n = std::make_unique<RmsNorm>("norm", dim, r->cfg);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_rms_destroy(void* h) { delete static_cast<RefRms*>(h); }
+int ref_rms_forward(void* h, const float* x, int64_t rows, float* y) {
+    return guarded([&] {
+        auto* r = static_cast<RefRms*>(h);
+        const DenseMatrix out = r->n->forward(make_dense(x, rows, r->dim));
+        std::memcpy(y, out.data(), out.size() * sizeof(float));
+    });
+}
+int ref_rms_backward(void* h, const float* gy, int64_t rows, float* gx) {
+    return guarded([&] {
+        auto* r = static_cast<RefRms*>(h);
+        const DenseMatrix out = r->n->backward(make_dense(gy, rows, r->dim));
+        std::memcpy(gx, out.data(), out.size() * sizeof(float));
+    });
+}
+int ref_rms_state(void* h, float* gain, float* grad_gain) {
+    return guarded([&] {
+        auto* r = static_cast<RefRms*>(h);
+        std::memcpy(gain, r->n->gain().data(), r->dim * 4);
+        std::memcpy(grad_gain, r->n->grad_gain().data(), r->dim * 4);
+    });
+}
+int ref_rms_sgd(void* h, double lr) {
+    return guarded([&] { static_cast<RefRms*>(h)->n->apply_sgd(lr); });
+}
+
 } // extern "C"

@@ -34,6 +34,9 @@ _SIGS = {
     "fbq_block_side": (cint, []),
     "fbq_cuda_block_absmax": (cint, [vp, cint, i64, i64, i64, vp, vp]),
     "fbq_cuda_mask_topk": (cint, [vp, i64, dbl, vp, vp, vp]),
+    "fbq_cuda_rmsnorm_forward": (cint, [vp, cint, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp]),
+    "fbq_cuda_rmsnorm_backward": (cint, [vp, i64, vp, vp, cint, i64, i64, i64, vp, vp, i64, vp, vp,
+                                         vp, vp]),
     "fbq_cuda_quantize_fallback": (cint, [vp, cint, i64, i64, i64, cint, dbl, vp, vp, i64, vp, vp,
                                           vp, vp, vp, vp, u64, i64, vp]),
     "fbq_cuda_quantize_rtn": (cint, [vp, cint, i64, i64, i64, vp, i64, vp, vp]),

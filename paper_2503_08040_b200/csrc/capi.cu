@@ -218,6 +218,42 @@ int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, 
                                     nullptr, 0, 0, stream);
 }
 
+static bool rms_layout_ok(int64_t cols, int64_t ld, const void* p, size_t esz) {
+  return cols % 8 == 0 && aligned16(p) && (ld * (int64_t)esz) % 16 == 0;
+}
+
+int fbq_cuda_rmsnorm_forward(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                             const float* gain, void* y, int64_t ldy, int16_t* ctx_codes,
+                             int64_t ld_ctx, float* ctx_scales, float* rms_ws, fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!x || !gain || !y || !ctx_codes || !ctx_scales || !rms_ws) return FBQ_ERR_ARG;
+  if (ldx < cols || ldy < cols || ld_ctx < cols) return FBQ_ERR_ARG;
+  const size_t esz = dtype == FBQ_F32 ? 4 : 2;
+  if (!rms_layout_ok(cols, ldx, x, esz) || !rms_layout_ok(cols, ldy, y, esz) ||
+      !rms_layout_ok(cols, ld_ctx, ctx_codes, 2) || cdiv(rows, 128) > 65535)
+    return FBQ_ERR_UNSUPPORTED;
+  return cuda_status(fbq::launch_rmsnorm_forward(x, dtype == FBQ_BF16, rows, cols, ldx, gain, y, ldy,
+                                                 ctx_codes, ld_ctx, ctx_scales, rms_ws,
+                                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_rmsnorm_backward(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales,
+                              const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
+                              const float* gain, void* gx, int64_t ldgx, float* grad_gain,
+                              double* row_ws, float* term_ws, fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!ctx_codes || !ctx_scales || !gy || !gain || !gx || !grad_gain || !row_ws || !term_ws)
+    return FBQ_ERR_ARG;
+  if (ldgy < cols || ldgx < cols || ld_ctx < cols) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_rmsnorm_backward(ctx_codes, ld_ctx, ctx_scales, gy, dtype == FBQ_BF16,
+                                                  rows, cols, ldgy, gain, gx, ldgx, grad_gain, row_ws,
+                                                  term_ws, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* mask_bits,
                        int32_t* masked_count, fbq_stream_t stream) {
   if (!(rate >= 0.0 && rate <= 1.0)) return FBQ_ERR_ARG;  // policy.cpp:57

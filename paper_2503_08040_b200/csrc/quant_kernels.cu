@@ -841,6 +841,221 @@ fbq_glu_backward_kernel(GluBwdParams g) {
   }
 }
 
+// ------------------------------------------------------------------ RMSNorm
+// RmsNorm (trainsim.cpp:154-211) with its 10-bit 1 x 128 input context.
+// The reference accumulates every row's sum of squares (and, backward, the
+// gain-weighted dot product) SEQUENTIALLY in double; to reproduce those exact
+// roundings one thread owns one row and walks the columns in order, reading
+// 128-row x 32-column tiles staged through shared memory (coalesced loads,
+// +1 padding against bank conflicts).  Everything per element is parallel.
+constexpr int kRmsRows = 128, kRmsCols = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kRmsRows)
+fbq_rms_rowstat_fwd_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                           float* __restrict__ rms) {
+  __shared__ float tile[kRmsRows][kRmsCols + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * kRmsRows;
+  double ss = 0.0;
+  for (int64_t c0 = 0; c0 < cols; c0 += kRmsCols) {
+    for (int i = threadIdx.x; i < kRmsRows * kRmsCols; i += kRmsRows) {
+      const int rr = i / kRmsCols, cc = i % kRmsCols;
+      const int64_t r = r0 + rr, c = c0 + cc;
+      tile[rr][cc] = (r < rows && c < cols) ? to_f32(x[r * ldx + c]) : 0.0f;
+    }
+    __syncthreads();
+    const int n = cols - c0 < kRmsCols ? (int)(cols - c0) : kRmsCols;
+    for (int cc = 0; cc < n; ++cc) {
+      const double v = (double)tile[threadIdx.x][cc];
+      ss = __fma_rn(v, v, ss);  // v*v is exact in double: == ss + v*v (trainsim.cpp:160-163)
+    }
+    __syncthreads();
+  }
+  const int64_t r = r0 + threadIdx.x;
+  if (r < rows)  // sqrt(float(ss / cols) + eps) in float (trainsim.cpp:164-165)
+    rms[r] = __fsqrt_rn(__fadd_rn(__double2float_rn(__ddiv_rn(ss, (double)cols)), 1e-6f));
+}
+
+// y = fl(fl(x / rms) * gain) and the 10-bit 1 x 128 RTN context of x
+// (quantize_rtn(x, GroupGeometry(1, 128), 10 bits), trainsim.cpp:166-177).
+template <typename T>
+__global__ void __launch_bounds__(kQuantThreads)
+fbq_rms_apply_fwd_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                         const float* __restrict__ gain, const float* __restrict__ rms,
+                         T* __restrict__ y, int64_t ldy, int16_t* ctx, int64_t ld_ctx,
+                         float* ctx_scales, float level) {
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int64_t bj = blockIdx.x, bi = blockIdx.y;
+  const int64_t gcols = (cols + kBlock - 1) / kBlock;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t cc = bj * kBlock + lc;
+  const bool col_ok = cc < cols;  // cols % V == 0
+  float g[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) g[i] = col_ok ? gain[cc + i] : 0.0f;
+#pragma unroll 1
+  for (int ps = 0; ps < NP; ++ps) {
+    const int64_t r = bi * kBlock + lr + ps * RPP;
+    if (r >= rows) break;  // row-uniform across the VPR threads of the group
+    float v[V];
+    if (col_ok) {
+      load_vec<T, V>(x + r * ldx + cc, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = 0.0f;
+    }
+    uint32_t code[V];
+    const float s = group_rtn<V, VPR>(v, code, level);
+    if (!col_ok) continue;
+    store_codes16<V>(ctx + r * ld_ctx + cc, code);
+    if (lc == 0) ctx_scales[r * gcols + bj] = s;
+    const float rr = rms[r];
+    T out[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float o = __fmul_rn(__fdiv_rn(v[i], rr), g[i]);
+      if constexpr (sizeof(T) == 2) out[i] = __float2bfloat16_rn(o);
+      else out[i] = o;
+    }
+    *reinterpret_cast<uint4*>(y + r * ldy + cc) = *reinterpret_cast<const uint4*>(out);
+  }
+}
+
+// backward row statistics (trainsim.cpp:186-199), sequential per row in double:
+// x = dequantize(ctx); ss = sum x^2; dot = sum fl(fl(g*dy)*x); rms = sqrt(ss/cols
+// + eps); inv = 1 / rms; corr = dot / (((cols*rms)*rms)*rms)
+template <typename T>
+__global__ void __launch_bounds__(kRmsRows)
+fbq_rms_rowstat_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
+                           const float* __restrict__ ctx_scales, const T* __restrict__ gy,
+                           int64_t ldgy, int64_t rows, int64_t cols, const float* __restrict__ gain,
+                           double* __restrict__ inv_out, double* __restrict__ corr_out) {
+  __shared__ float tx[kRmsRows][kRmsCols + 1];
+  __shared__ float tg[kRmsRows][kRmsCols + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * kRmsRows;
+  const int64_t gcols = (cols + kBlock - 1) / kBlock;
+  double ss = 0.0, dot = 0.0;
+  for (int64_t c0 = 0; c0 < cols; c0 += kRmsCols) {
+    for (int i = threadIdx.x; i < kRmsRows * kRmsCols; i += kRmsRows) {
+      const int rr = i / kRmsCols, cc = i % kRmsCols;
+      const int64_t r = r0 + rr, c = c0 + cc;
+      const bool ok = r < rows && c < cols;
+      // dequantize: fl(code * scale) (quant.cpp:86-104)
+      tx[rr][cc] = ok ? __fmul_rn((float)ctx[r * ld_ctx + c], ctx_scales[r * gcols + c / kBlock]) : 0.0f;
+      tg[rr][cc] = ok ? to_f32(gy[r * ldgy + c]) : 0.0f;
+    }
+    __syncthreads();
+    const int n = cols - c0 < kRmsCols ? (int)(cols - c0) : kRmsCols;
+    for (int cc = 0; cc < n; ++cc) {
+      const double v = (double)tx[threadIdx.x][cc];
+      ss = __fma_rn(v, v, ss);
+      const double h = __dmul_rn((double)gain[c0 + cc], (double)tg[threadIdx.x][cc]);
+      dot = __dadd_rn(dot, __dmul_rn(h, v));
+    }
+    __syncthreads();
+  }
+  const int64_t r = r0 + threadIdx.x;
+  if (r < rows) {
+    const double rms = __dsqrt_rn(__dadd_rn(__ddiv_rn(ss, (double)cols), (double)1e-6f));
+    inv_out[r] = __ddiv_rn(1.0, rms);
+    corr_out[r] = __ddiv_rn(dot, __dmul_rn(__dmul_rn(__dmul_rn((double)cols, rms), rms), rms));
+  }
+}
+
+// gx = float(h * inv - x * corr), h = g * dy (double); and the per-element
+// grad_gain term float(float(dy * x) * inv) into `term` (trainsim.cpp:200-205)
+template <typename T>
+__global__ void fbq_rms_apply_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
+                                         const float* __restrict__ ctx_scales, const T* __restrict__ gy,
+                                         int64_t ldgy, int64_t rows, int64_t cols,
+                                         const float* __restrict__ gain, const double* __restrict__ inv,
+                                         const double* __restrict__ corr, T* __restrict__ gx,
+                                         int64_t ldgx, float* __restrict__ term) {
+  const int64_t gcols = (cols + kBlock - 1) / kBlock;
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const float x = __fmul_rn((float)ctx[r * ld_ctx + c], ctx_scales[r * gcols + c / kBlock]);
+    const float dy = to_f32(gy[r * ldgy + c]);
+    const double h = __dmul_rn((double)gain[c], (double)dy);
+    const float o = __double2float_rn(__dsub_rn(__dmul_rn(h, inv[r]), __dmul_rn((double)x, corr[r])));
+    if constexpr (sizeof(T) == 2) gx[r * ldgx + c] = __float2bfloat16_rn(o);
+    else gx[r * ldgx + c] = o;
+    term[i] = __double2float_rn(__dmul_rn((double)__fmul_rn(dy, x), inv[r]));
+  }
+}
+
+// grad_gain[c] += term[r][c] for r = 0, 1, ... in order (float adds, the
+// reference's accumulation order); loads run far ahead of the add chain.
+__global__ void fbq_rms_grad_gain_kernel(const float* __restrict__ term, int64_t rows, int64_t cols,
+                                         float* __restrict__ grad_gain) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float acc = grad_gain[c];
+  int64_t r = 0;
+  for (; r + 8 <= rows; r += 8) {
+    float t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = term[(r + j) * cols + c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = __fadd_rn(acc, t[j]);
+  }
+  for (; r < rows; ++r) acc = __fadd_rn(acc, term[r * cols + c]);
+  grad_gain[c] = acc;
+}
+
+cudaError_t launch_rmsnorm_forward(const void* x, bool bf16, int64_t rows, int64_t cols, int64_t ldx,
+                                   const float* gain, void* y, int64_t ldy, int16_t* ctx,
+                                   int64_t ld_ctx, float* ctx_scales, float* rms, cudaStream_t s) {
+  const unsigned rb = (unsigned)((rows + kRmsRows - 1) / kRmsRows);
+  const dim3 grid((unsigned)((cols + kBlock - 1) / kBlock), (unsigned)((rows + kBlock - 1) / kBlock));
+  if (bf16) {
+    fbq_rms_rowstat_fwd_kernel<__nv_bfloat16><<<rb, kRmsRows, 0, s>>>(
+        reinterpret_cast<const __nv_bfloat16*>(x), rows, cols, ldx, rms);
+    fbq_rms_apply_fwd_kernel<__nv_bfloat16><<<grid, kQuantThreads, 0, s>>>(
+        reinterpret_cast<const __nv_bfloat16*>(x), rows, cols, ldx, gain, rms,
+        reinterpret_cast<__nv_bfloat16*>(y), ldy, ctx, ld_ctx, ctx_scales, 511.0f);
+  } else {
+    fbq_rms_rowstat_fwd_kernel<float><<<rb, kRmsRows, 0, s>>>(reinterpret_cast<const float*>(x), rows,
+                                                              cols, ldx, rms);
+    fbq_rms_apply_fwd_kernel<float><<<grid, kQuantThreads, 0, s>>>(
+        reinterpret_cast<const float*>(x), rows, cols, ldx, gain, rms, reinterpret_cast<float*>(y),
+        ldy, ctx, ld_ctx, ctx_scales, 511.0f);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales,
+                                    const void* gy, bool bf16, int64_t rows, int64_t cols,
+                                    int64_t ldgy, const float* gain, void* gx, int64_t ldgx,
+                                    float* grad_gain, double* row_ws, float* term, cudaStream_t s) {
+  const unsigned rb = (unsigned)((rows + kRmsRows - 1) / kRmsRows);
+  double* inv = row_ws;
+  double* corr = row_ws + rows;
+  const int64_t n = rows * cols;
+  int blocks = (n + 255) / 256 < 148 * 16 ? (int)((n + 255) / 256) : 148 * 16;
+  if (blocks < 1) blocks = 1;
+  if (bf16) {
+    auto g = reinterpret_cast<const __nv_bfloat16*>(gy);
+    fbq_rms_rowstat_bwd_kernel<__nv_bfloat16><<<rb, kRmsRows, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy,
+                                                                      rows, cols, gain, inv, corr);
+    fbq_rms_apply_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+        ctx, ld_ctx, ctx_scales, g, ldgy, rows, cols, gain, inv, corr,
+        reinterpret_cast<__nv_bfloat16*>(gx), ldgx, term);
+  } else {
+    auto g = reinterpret_cast<const float*>(gy);
+    fbq_rms_rowstat_bwd_kernel<float><<<rb, kRmsRows, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows,
+                                                              cols, gain, inv, corr);
+    fbq_rms_apply_bwd_kernel<float><<<blocks, 256, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows, cols,
+                                                           gain, inv, corr, reinterpret_cast<float*>(gx),
+                                                           ldgx, term);
+  }
+  fbq_rms_grad_gain_kernel<<<(unsigned)((cols + 127) / 128), 128, 0, s>>>(term, rows, cols, grad_gain);
+  return cudaGetLastError();
+}
+
 // Delay-threshold controller on device (policy.cpp:97-109, Algorithm 2):
 // rate = masked / blocks (policy.cpp:82-87); theta /= alpha below r_min,
 // *= alpha above r_max.  Keeps the per-step update off the host.

@@ -74,6 +74,14 @@ struct DequantParams {
 
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s);
 extern int g_quant_diag;
+// RmsNorm forward / backward with the 10-bit 1 x 128 context (trainsim.cpp:154-211)
+cudaError_t launch_rmsnorm_forward(const void* x, bool bf16, int64_t rows, int64_t cols, int64_t ldx,
+                                   const float* gain, void* y, int64_t ldy, int16_t* ctx,
+                                   int64_t ld_ctx, float* ctx_scales, float* rms, cudaStream_t s);
+cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales,
+                                    const void* gy, bool bf16, int64_t rows, int64_t cols,
+                                    int64_t ldgy, const float* gain, void* gx, int64_t ldgx,
+                                    float* grad_gain, double* row_ws, float* term, cudaStream_t s);
 // mask_topk (policy.cpp:56-71) on device: exactly k blocks (policy_kernels.cu)
 cudaError_t launch_topk(const float* scores, int64_t n, int64_t k, uint32_t* mask_bits,
                         int32_t* count, cudaStream_t s);  // 1 = one-block-per-CTA K1 (diagnostics, fbq_debug_set_quant_diag)

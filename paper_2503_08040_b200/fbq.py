@@ -430,3 +430,57 @@ def bits_at(seed: int, n: int) -> int:
 def layer_seed(base: int, layer_id: int, tag: int, step: int) -> int:
     """trainsim.cpp:16-19 (tag 0 = X context, 1 = dY)."""
     return derive_seed(base, layer_id * 4 + tag, step)
+
+
+# ------------------------------------------------------------------ RmsNorm
+class RmsNorm:
+    """RmsNorm (trainsim.hpp:75-97, trainsim.cpp:145-211) on the device: gain
+    starts at 1, the input is kept as its 10-bit 1 x 128 context, backward
+    accumulates grad_gain; apply_sgd / zero_grad as in the reference."""
+
+    def __init__(self, dim: int, device="cuda"):
+        self.dim = dim
+        self.gain = torch.ones(dim, dtype=torch.float32, device=device)
+        self.grad_gain = torch.zeros(dim, dtype=torch.float32, device=device)
+        self._ctx = None
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        x = _check_input(x)
+        r, c = x.shape
+        if c != self.dim:
+            raise ValueError("width does not match the gain vector")  # trainsim.cpp:156-158
+        y = torch.empty_like(x)
+        ldc = _ld16(c)
+        codes = torch.empty((r, ldc), dtype=torch.int16, device=x.device)
+        scales = torch.empty((r, cdiv(c, BLOCK)), dtype=torch.float32, device=x.device)
+        rms = torch.empty(r, dtype=torch.float32, device=x.device)
+        K.call("fbq_cuda_rmsnorm_forward", x.data_ptr(), _dtype_code(x), r, c, x.stride(0),
+               self.gain.data_ptr(), y.data_ptr(), y.stride(0), codes.data_ptr(), ldc,
+               scales.data_ptr(), rms.data_ptr(), _stream())
+        self._ctx = (codes, scales, r, c)
+        return y
+
+    def context(self):
+        """(int16 codes rows x ld, fp32 scales rows x ceil(cols/128)) of the last input."""
+        return self._ctx[:2]
+
+    def backward(self, gy: torch.Tensor) -> torch.Tensor:
+        if self._ctx is None:
+            raise RuntimeError("backward without context")  # trainsim.cpp:181-183
+        codes, scales, r, c = self._ctx
+        gy = _check_input(gy)
+        gx = torch.empty_like(gy)
+        row_ws = torch.empty(2 * r, dtype=torch.float64, device=gy.device)
+        term = torch.empty((r, c), dtype=torch.float32, device=gy.device)
+        K.call("fbq_cuda_rmsnorm_backward", codes.data_ptr(), codes.stride(0), scales.data_ptr(),
+               gy.data_ptr(), _dtype_code(gy), r, c, gy.stride(0), self.gain.data_ptr(),
+               gx.data_ptr(), gx.stride(0), self.grad_gain.data_ptr(), row_ws.data_ptr(),
+               term.data_ptr(), _stream())
+        return gx
+
+    def zero_grad(self):
+        self.grad_gain.zero_()
+
+    def apply_sgd(self, lr: float):
+        """gain[c] -= float(lr * double(grad_gain[c])) (trainsim.cpp:213-218)."""
+        self.gain.sub_((lr * self.grad_gain.double()).float())
