@@ -42,7 +42,8 @@ enum fbq_status {
   FBQ_ERR_SHAPE = 1,       /* dimension / geometry mismatch (reference: std::invalid_argument) */
   FBQ_ERR_UNSUPPORTED = 2, /* block side != 128, bits != 8, bad alignment */
   FBQ_ERR_CUDA = 3,        /* launch or runtime failure; see fbq_last_cuda_error() */
-  FBQ_ERR_ARG = 4          /* null pointer / bad enum / out-of-range value */
+  FBQ_ERR_ARG = 4,         /* null pointer / bad enum / out-of-range value */
+  FBQ_ERR_FORMAT = 5       /* malformed file (reference: FormatError, byte offset via fbq_io_last_offset) */
 };
 enum fbq_dtype { FBQ_F32 = 0, FBQ_BF16 = 1 };
 enum fbq_mask_mode {

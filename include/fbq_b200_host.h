@@ -129,6 +129,24 @@ float* fbq_linear_grad_ptr(void* linear);
 /* last observed fallback rate and the current threshold (synchronous read) */
 int fbq_linear_get_controller(void* linear, double* last_rate, double* threshold);
 
+/* ---- wire formats (host/io.cpp) ----
+ * .fmat: the reference's dense fp32 matrix file (matrix.cpp:75-142), byte-
+ * compatible, with its FormatError checks: FBQ_ERR_FORMAT + the reference's
+ * byte offset (fbq_io_last_offset) and message (fbq_io_last_error).
+ * .fqt: block-quantized / fallback tensor sidecar (codes, scales, bitmap,
+ * residual plane; 128 x 128 blocks, 8 bits), host buffers. */
+const char* fbq_io_last_error(void);
+uint64_t fbq_io_last_offset(void);
+int fbq_fmat_save(const char* path, const float* data, int64_t rows, int64_t cols);
+int fbq_fmat_info(const char* path, int64_t* rows, int64_t* cols);
+int fbq_fmat_load(const char* path, float* data, int64_t capacity, int64_t* rows, int64_t* cols);
+int fbq_fqt_save(const char* path, int64_t rows, int64_t cols, const int8_t* codes, int64_t ldq,
+                 const float* scales, const uint32_t* mask_bits, const int8_t* res_codes,
+                 const float* res_scales);
+int fbq_fqt_info(const char* path, int64_t* rows, int64_t* cols, int* has_fallback);
+int fbq_fqt_load(const char* path, int8_t* codes, int64_t ldq, float* scales, uint32_t* mask_bits,
+                 int8_t* res_codes, float* res_scales);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "fbq/error.hpp"
 #include "fbq/gemm.hpp"
 #include "fbq/kernels.hpp"
 #include "fbq/matrix.hpp"
@@ -420,6 +421,27 @@ int ref_linear_controller(void* h, double* rate, double* threshold) {
 }
 int ref_linear_zero_grad(void* h) {
     return guarded([&] { static_cast<RefLinear*>(h)->l->zero_grad(); });
+}
+
+// ---------------------------------------------------------------------------
+// .fmat I/O (matrix.cpp:92-140): status 0, or 1 with FormatError's byte offset.
+int ref_fmat_save(const char* path, const float* data, int64_t rows, int64_t cols) {
+    return guarded([&] { save_matrix(make_dense(data, rows, cols), path); });
+}
+int ref_fmat_load(const char* path, float* data, int64_t capacity, int64_t* rows, int64_t* cols,
+                  uint64_t* err_offset) {
+    try {
+        const DenseMatrix m = load_matrix(path);
+        *rows = m.rows();
+        *cols = m.cols();
+        if (m.size() > capacity) return 2;
+        std::memcpy(data, m.data(), m.size() * sizeof(float));
+        return 0;
+    } catch (const FormatError& e) {
+        *err_offset = e.byte_offset();
+        g_err = e.what();
+        return 1;
+    }
 }
 
 // ---------------------------------------------------------------------------
