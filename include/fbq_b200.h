@@ -111,8 +111,9 @@ int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* ma
  * quantize_stochastic context codes (quant.cpp:55-84, trainsim.cpp:100-102).
  * One read of x.  Any output pointer may be NULL to skip that output except
  * that mask modes != NONE need mask_bits, and res_codes/res_scales go together.
- * mask_bits is zeroed by this call in THRESHOLD mode; *masked_count is
- * overwritten.  sr_codes (if non-NULL) shares `scales` with the RTN codes and
+ * In THRESHOLD mode every bit of mask_bits (including the unused tail of the
+ * last word) is written by the kernel, so the caller need not clear it;
+ * *masked_count is overwritten.  sr_codes (if non-NULL) shares `scales` with the RTN codes and
  * uses RNG index (sr_row_offset + r) * cols + c (row offset = token-shard
  * start; 0 reproduces the reference). */
 int fbq_cuda_quantize_fallback(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,

@@ -88,15 +88,14 @@ static int fill_quant_params(fbq::QuantParams& p, const void* x, int64_t rows, i
   if ((res_codes == nullptr) != (res_scales == nullptr)) return FBQ_ERR_ARG;
   if ((codes || res_codes || sr_codes || sr_codes2) && ldq < cols) return FBQ_ERR_ARG;
   if (sr_row_offset < 0) return FBQ_ERR_ARG;
-  const int64_t grid = cdiv(rows, 128) * cdiv(cols, 128);
-  if (mask_mode == FBQ_MASK_THRESHOLD && grid > 0) {
-    if (int st = cuda_status(cudaMemsetAsync(mask_bits, 0, (size_t)cdiv(grid, 32) * 4, s)))
-      return st;
-  }
-  if (masked_count) {
-    if (int st = cuda_status(cudaMemsetAsync(masked_count, 0, sizeof(int32_t), s))) return st;
-  }
+  // Threshold mode writes every mask bit (set or clear) in the quantizer, so
+  // the bitmap is not zeroed here; the count is zeroed by a one-warp grid that
+  // the quantizer overlaps (programmatic dependent launch, p.pdl).
   p = fbq::QuantParams{};
+  if (masked_count) {
+    if (int st = cuda_status(fbq::launch_zero_count(masked_count, s))) return st;
+    p.pdl = 1;
+  }
   p.x = x;
   p.rows = rows;
   p.cols = cols;

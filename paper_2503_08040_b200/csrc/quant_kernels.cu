@@ -207,6 +207,27 @@ __device__ __forceinline__ int round_mode(float a) {
 // Entered by all threads of the CTA (it contains CTA barriers).
 // have_m: the caller already holds this thread's partial absmax `m_in` (and
 // the block barrier in block_max publishes the values `val` reads).
+// Threshold mode writes the block's own mask bit either way (set or clear),
+// so the bitmap needs no zeroing pass; the last block also clears the unused
+// tail bits of the final word.  The masked-block count is the one value that
+// must start at zero: it is zeroed by fbq_zero_count_kernel launched just
+// before this grid, which this grid may overlap (programmatic dependent
+// launch) up to the griddepcontrol.wait in front of the first atomicAdd.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void publish_flag(const QuantParams& p, int64_t blk, bool flagged) {
+  if (p.mask_mode == kMaskThreshold) {
+    const uint32_t bit = 1u << (blk & 31);
+    if (flagged) atomicOr(p.mask_bits + (blk >> 5), bit);
+    else atomicAnd(p.mask_bits + (blk >> 5), ~bit);
+    const int64_t last = ((p.rows + kBlock - 1) / kBlock) * ((p.cols + kBlock - 1) / kBlock) - 1;
+    if (blk == last && (last & 31) != 31) atomicAnd(p.mask_bits + (blk >> 5), (bit << 1) - 1u);
+  }
+  if (flagged && p.masked_count) {
+    pdl_wait();
+    atomicAdd(p.masked_count, 1);
+  }
+}
+
 template <int V, int kSR, class Val>
 __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk, int64_t r0,
                                                int64_t c0, float* red, Val&& val,
@@ -242,8 +263,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   if (threadIdx.x == 0) {
     if (p.scales) p.scales[blk] = a;
     if (p.amax_out) p.amax_out[blk] = amax;
-    if (p.mask_mode == kMaskThreshold && flagged) atomicOr(p.mask_bits + (blk >> 5), 1u << (blk & 31));
-    if (flagged && p.masked_count) atomicAdd(p.masked_count, 1);
+    publish_flag(p, blk, flagged);
     if (p.res_scales && !flagged) p.res_scales[blk] = 0.0f;
   }
 
@@ -446,8 +466,7 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   if (threadIdx.x == 0) {
     if (p.scales) p.scales[blk] = a;
     if (p.amax_out) p.amax_out[blk] = amax;
-    if (p.mask_mode == kMaskThreshold && flagged) atomicOr(p.mask_bits + (blk >> 5), 1u << (blk & 31));
-    if (flagged && p.masked_count) atomicAdd(p.masked_count, 1);
+    publish_flag(p, blk, flagged);
     if (p.res_scales && !flagged) p.res_scales[blk] = 0.0f;
   }
   // ---- RTN codes (kernels.cpp:24-40) ----
@@ -1131,6 +1150,33 @@ static cudaError_t opt_in_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// Launch with programmatic stream serialisation when the grid follows
+// fbq_zero_count_kernel (p.pdl): it may start while the zeroing grid drains.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+__global__ void fbq_zero_count_kernel(int* count) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) *count = 0;
+}
+cudaError_t launch_zero_count(int* count, cudaStream_t s) {
+  fbq_zero_count_kernel<<<1, 32, 0, s>>>(count);
+  return cudaGetLastError();
+}
+
 template <typename T, bool kVec, int kSR>
 static cudaError_t launch_k1_sr(const QuantParams& p, dim3 grid, cudaStream_t s) {
   const size_t smem = sizeof(T) * kTileElems;
@@ -1139,8 +1185,7 @@ static cudaError_t launch_k1_sr(const QuantParams& p, dim3 grid, cudaStream_t s)
     if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec, kSR>, smem)) return e;
     ready = true;
   }
-  fbq_quantize_block_kernel<T, kVec, kSR><<<grid, kQuantThreads, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_ex(fbq_quantize_block_kernel<T, kVec, kSR>, grid, dim3(kQuantThreads), smem, s, p.pdl, p);
 }
 template <typename T, bool kVec>
 static cudaError_t launch_k1(QuantParams p, dim3 grid, cudaStream_t s) {
@@ -1212,8 +1257,8 @@ static cudaError_t launch_k1_tma(const QuantParams& p, cudaStream_t s) {
   const int64_t nblk = (int64_t)gcols * ((p.rows + kBlock - 1) / kBlock);
   int64_t grid = (int64_t)num_sms() * ctas_per_sm;
   if (grid > nblk) grid = nblk;
-  fbq_quantize_tma_kernel<T, kSR, kQStages><<<(unsigned)grid, kQuantThreads, smem, s>>>(m, p, nblk, gcols);
-  return cudaGetLastError();
+  return launch_ex(fbq_quantize_tma_kernel<T, kSR, kQStages>, dim3((unsigned)grid), dim3(kQuantThreads), smem, s,
+                   p.pdl, m, p, nblk, gcols);
 }
 template <typename T, int kQStages, int kMinBlocks>
 static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
@@ -1244,8 +1289,8 @@ static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
   const int64_t nblk = (int64_t)gcols * ((p.rows + kBlock - 1) / kBlock);
   int64_t grid = (int64_t)num_sms() * ctas_per_sm;
   if (grid > nblk) grid = nblk;
-  fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks><<<(unsigned)grid, kQuantThreads, smem, s>>>(m, p, (int)nblk, gcols);
-  return cudaGetLastError();
+  return launch_ex(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks>, dim3((unsigned)grid), dim3(kQuantThreads),
+                   smem, s, p.pdl, m, p, (int)nblk, gcols);
 }
 
 template <typename T>
@@ -1283,9 +1328,8 @@ cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
       // 3 stages x 2 CTAs (latency hiding of the rounding passes matters more)
       return (g_quant_diag & 4) ? launch_k1_tma_reg<__nv_bfloat16, 3, 2>(p, s)
                                 : launch_k1_tma_reg<__nv_bfloat16, 2, 3>(p, s);
-    if (bf16) fbq_quantize_reg_kernel<__nv_bfloat16><<<grid, kQuantThreads, 0, s>>>(p);
-    else fbq_quantize_reg_kernel<float><<<grid, kQuantThreads, 0, s>>>(p);
-    return cudaGetLastError();
+    if (bf16) return launch_ex(fbq_quantize_reg_kernel<__nv_bfloat16>, grid, dim3(kQuantThreads), 0, s, p.pdl, p);
+    return launch_ex(fbq_quantize_reg_kernel<float>, grid, dim3(kQuantThreads), 0, s, p.pdl, p);
   }
   if (vec && (g_quant_diag & 2) && nblk >= 2 * num_sms() && p.rows < (1ll << 31) &&
       p.cols < (1ll << 31))
@@ -1302,11 +1346,11 @@ cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf
   if (bf16) {
     const size_t smem = 2 * sizeof(__nv_bfloat16) * kTileElems;  // a|b rows, then h (fp32) in place
     if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16>, smem)) return e;
-    fbq_glu_forward_kernel<__nv_bfloat16><<<grid, kQuantThreads, smem, s>>>(g, p);
+    return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
   } else {
     const size_t smem = 2 * sizeof(float) * kTileElems;
     if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<float>, smem)) return e;
-    fbq_glu_forward_kernel<float><<<grid, kQuantThreads, smem, s>>>(g, p);
+    return launch_ex(fbq_glu_forward_kernel<float>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
   }
   return cudaGetLastError();
 }

@@ -15,12 +15,13 @@ struct QuantParams {
   int mask_mode;
   double theta;
   const double* theta_dev;  // if non-null, the threshold is read on device (controller state)
-  uint32_t* mask_bits;     // in (given) / out (threshold, pre-zeroed)
+  uint32_t* mask_bits;     // in (given) / out (threshold: every bit written, no pre-zeroing)
   int8_t* codes;           // may be null (SR-only launch)
   float* scales;           // may be null
   int8_t* res_codes;       // may be null
   float* res_scales;       // may be null
-  int* masked_count;       // may be null (pre-zeroed)
+  int* masked_count;       // may be null; zeroed by launch_zero_count right before the grid
+  int pdl;                 // 1: launched as a programmatic dependent of launch_zero_count
   float* amax_out;         // may be null
   int8_t* sr_codes;        // may be null
   uint64_t sr_seed;
@@ -88,6 +89,7 @@ cudaError_t launch_topk(const float* scores, int64_t n, int64_t k, uint32_t* mas
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
 cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s);
+cudaError_t launch_zero_count(int* count, cudaStream_t s);
 cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,
                               double r_min, double r_max, double alpha, double* last_rate,
                               cudaStream_t s);

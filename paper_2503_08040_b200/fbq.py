@@ -218,12 +218,12 @@ def fallback_quantize(x: torch.Tensor, mask: torch.Tensor | None = None, *,
         if not theta > 0.0:
             raise ValueError("threshold must be > 0")  # policy.cpp:74
         mode, th = K.FBQ_MASK_THRESHOLD, float(theta)
-        bits_t = torch.zeros(cdiv(max(gr * gc, 1), 32), dtype=torch.int32, device=dev)
+        bits_t = torch.empty(cdiv(max(gr * gc, 1), 32), dtype=torch.int32, device=dev)  # all bits written
     else:
         raise ValueError("fallback_quantize needs a mask or a threshold")
     codes, scales = _alloc_codes(r, c, dev), _alloc_grid(r, c, dev)
     res_codes, res_scales = _alloc_codes(r, c, dev), _alloc_grid(r, c, dev)
-    count = torch.zeros(1, dtype=torch.int32, device=dev)
+    count = torch.empty(1, dtype=torch.int32, device=dev)  # zeroed in-stream by the call
     sr = _alloc_codes(r, c, dev) if sr_seed is not None else None
     K.call("fbq_cuda_quantize_fallback", x.data_ptr(), _dtype_code(x), r, c, x.stride(0), mode,
            th, bits_t.data_ptr(), codes.data_ptr(), codes.stride(0), scales.data_ptr(),

@@ -72,6 +72,44 @@ def test_fallback_quantize_threshold(F, orc, shape):
     assert np.array_equal(host(F.score_blocks(dev(x))), scores)
 
 
+@pytest.mark.parametrize("shape", [(300, 270), (640, 1152), (8192, 512)])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_threshold_mask_needs_no_zeroing(F, orc, shape, dtype):
+    """THRESHOLD mode writes every bitmap bit (tail bits of the last word
+    cleared) and zeroes the count in-stream: dirty buffers give the oracle's
+    mask, and back-to-back calls on the same buffers agree."""
+    import torch
+    from paper_2503_08040_b200 import _capi as K
+    x = outlier_matrix(*shape, seed=11, channels=[1], tokens=[min(9, shape[0] - 1)], occasional=7)
+    if dtype == "bf16":
+        x = bf16_round(x)
+    xt = dev(x).to(torch.bfloat16) if dtype == "bf16" else dev(x)
+    scores = orc.score_blocks_absmax(x)
+    theta = float(np.median(scores))
+    mask = orc.mask_threshold(scores, theta)
+    r, c = shape
+    nb = mask.size
+    words = (nb + 31) // 32
+    bits = torch.full((words,), -1, dtype=torch.int32, device="cuda")
+    count = torch.full((1,), 12345, dtype=torch.int32, device="cuda")
+    codes = torch.empty((r, (c + 15) // 16 * 16), dtype=torch.int8, device="cuda")
+    res = torch.empty_like(codes)
+    sc = torch.empty(nb, dtype=torch.float32, device="cuda")
+    rsc = torch.empty_like(sc)
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        K.call("fbq_cuda_quantize_fallback", xt.data_ptr(), K.FBQ_BF16 if dtype == "bf16" else K.FBQ_F32,
+               r, c, c, K.FBQ_MASK_THRESHOLD, theta, bits.data_ptr(), codes.data_ptr(), codes.stride(0),
+               sc.data_ptr(), res.data_ptr(), rsc.data_ptr(), count.data_ptr(), None, None, 0, 0, stream)
+        torch.cuda.synchronize()
+        want = np.zeros(words * 32, dtype=np.uint8)
+        want[:nb] = mask.reshape(-1)
+        want_words = (want.reshape(-1, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)).sum(1)
+        got = host(bits).view(np.uint32)
+        assert np.array_equal(got, want_words.astype(np.uint32))
+        assert int(count.item()) == int(mask.sum())
+
+
 def test_fallback_quantize_given_mask(F, orc):
     x = outlier_matrix(512, 384, seed=3, channels=[10, 200], occasional=20)
     scores = orc.score_blocks_absmax(x)
