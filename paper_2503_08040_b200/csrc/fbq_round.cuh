@@ -125,6 +125,26 @@ __device__ __forceinline__ float rtn_window(float level) { return 0.5f - level *
 template <int V>
 __device__ __forceinline__ bool rtn_fast_vec(const float (&x)[V], float inv_a, float window,
                                              uint32_t (&w)[V]) {
+  if constexpr (V % 2 == 0) {
+    // element pairs on the packed FP32 pipe (FMUL2 / FADD2 / FFMA2): q, m,
+    // n = m - M (exact), d = q - n (exact, |d| <= 1/2) -- 4 instructions per
+    // pair -- and one 3-input max of |d| per pair for the boundary test
+    const float2 inv2 = make_float2(inv_a, inv_a);
+    const float2 mag = make_float2(kMagic, kMagic), nmag = make_float2(-kMagic, -kMagic);
+    const float2 neg1 = make_float2(-1.0f, -1.0f);
+    float dm = 0.0f;
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const float2 q = __fmul2_rn(make_float2(x[i], x[i + 1]), inv2);
+      const float2 m = __fadd2_rn(q, mag);
+      const float2 n = __fadd2_rn(m, nmag);
+      const float2 d = __ffma2_rn(n, neg1, q);
+      dm = fmaxf(dm, fmaxf(fabsf(d.x), fabsf(d.y)));
+      w[i] = __float_as_uint(m.x);
+      w[i + 1] = __float_as_uint(m.y);
+    }
+    return dm > window;
+  }
   bool near = false;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -163,6 +183,30 @@ __device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
 template <int V>
 __device__ __forceinline__ bool sr_fast_vec(const float (&x)[V], float inv_a, uint64_t z,
                                             uint32_t (&w)[V]) {
+  if constexpr (V % 2 == 0) {
+    // the float part on element pairs (FADD2 / FMUL2 / FFMA2, 3-input max)
+    const float2 inv2 = make_float2(inv_a, inv_a);
+    const float2 mag = make_float2(kMagic, kMagic), nmag = make_float2(-kMagic, -kMagic);
+    const float2 neg1 = make_float2(-1.0f, -1.0f), c15 = make_float2(1.5f, 1.5f);
+    float dm = 0.0f, tm = 0.0f;
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const uint32_t h0 = mix64_hi(z);
+      const uint32_t h1 = mix64_hi(z + kGolden);
+      z += 2 * kGolden;
+      const float2 u = make_float2(__uint_as_float(0x3F800000u | (h0 >> 9)),
+                                   __uint_as_float(0x3F800000u | (h1 >> 9)));
+      const float2 half_u = __ffma2_rn(u, neg1, c15);  // 1.5 - u, exact
+      const float2 t = __fadd2_rn(__fmul2_rn(make_float2(x[i], x[i + 1]), inv2), half_u);
+      const float2 m = __fadd2_rn(t, mag);
+      const float2 d = __ffma2_rn(__fadd2_rn(m, nmag), neg1, t);
+      dm = fmaxf(dm, fmaxf(fabsf(d.x), fabsf(d.y)));
+      tm = fmaxf(tm, fmaxf(fabsf(t.x), fabsf(t.y)));
+      w[i] = __float_as_uint(m.x);
+      w[i + 1] = __float_as_uint(m.y);
+    }
+    return (dm > 0.5f - 0x1p-13f) | (tm > 127.25f);
+  }
   bool near = false;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
