@@ -418,7 +418,7 @@ __device__ __forceinline__ float code_of(const uint2& c, int i) {
 
 // One block's work given its raw values in registers (all threads; contains
 // CTA barriers).
-template <typename T>
+template <typename T, int kSR = 0>
 __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t bi, int64_t bj,
                                                    int64_t blk, const uint4 (&raw)[Tiling<T>::NP],
                                                    float* red) {
@@ -481,6 +481,32 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
       else __stcs(reinterpret_cast<unsigned int*>(dst), code[ps].x);
     }
   }
+  // ---- stochastic context planes (quant.cpp:55-84): RNG index (row_offset + r) * cols + c ----
+  if constexpr (kSR >= 1) {
+    if (col_ok) {
+      const uint64_t lin1 = (uint64_t)((p.row_offset + r0) * p.cols + cc + 1);
+      const uint64_t row_step = (uint64_t)RPP * (uint64_t)p.cols * kGolden;
+      uint64_t z1 = p.sr_seed + lin1 * kGolden;
+      uint64_t z2 = kSR >= 2 ? p.sr_seed2 + lin1 * kGolden : 0;
+#pragma unroll 1
+      for (int ps = 0; ps < nrow; ++ps) {
+        float v[V];
+        unpack<T>(raw[ps], v);
+        uint32_t w[V];
+        const int64_t off = (r0 + (int64_t)ps * RPP) * p.ldq + cc;
+        sr_vec<V>(v, a, inv_a, mode, z1, w);
+        if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(p.sr_codes + off), make_uint2(pack4_lo8(w), pack4_lo8(w + 4)));
+        else __stcs(reinterpret_cast<unsigned int*>(p.sr_codes + off), pack4_lo8(w));
+        if constexpr (kSR >= 2) {
+          sr_vec<V>(v, a, inv_a, mode, z2, w);
+          if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(p.sr_codes2 + off), make_uint2(pack4_lo8(w), pack4_lo8(w + 4)));
+          else __stcs(reinterpret_cast<unsigned int*>(p.sr_codes2 + off), pack4_lo8(w));
+        }
+        z1 += row_step;
+        z2 += row_step;
+      }
+    }
+  }
   if (!flagged) return;  // block-uniform
   // ---- fallback residual (quant.cpp:146-172): res = fl(x - fl(c * a)) ----
   float rm = 0.0f;
@@ -531,19 +557,19 @@ __device__ __forceinline__ void load_block_reg(const QuantParams& p, int64_t bi,
 
 // One 128 x 128 block per CTA (fp32 inputs: 64 registers of raw values per
 // thread leave no room for a register double buffer).
-template <typename T>
+template <typename T, int kSR>
 __global__ void __launch_bounds__(kQuantThreads, 2)
 fbq_quantize_reg_kernel(QuantParams p) {
   __shared__ float red[kQuantThreads / 32];
   uint4 raw[Tiling<T>::NP];
   load_block_reg<T>(p, blockIdx.y, blockIdx.x, raw);
-  quantize_block_reg<T>(p, blockIdx.y, blockIdx.x, (int64_t)blockIdx.y * gridDim.x + blockIdx.x, raw, red);
+  quantize_block_reg<T, kSR>(p, blockIdx.y, blockIdx.x, (int64_t)blockIdx.y * gridDim.x + blockIdx.x, raw, red);
 }
 
 // Persistent + TMA ring + register compute (bf16): tiles land in a kQStages
 // shared-memory ring by TMA while the CTA quantizes the current tile from
 // registers; a slot is handed back to TMA as soon as its values are in registers.
-template <typename T, int kQStages, int kMinBlocks>
+template <typename T, int kQStages, int kMinBlocks, int kSR>
 __global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantParams p, int nblk,
                             int gcols) {
@@ -589,7 +615,7 @@ fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantPara
     }
     if (++s == kQStages) { s = 0; phase ^= 1; }
     const int bi = b / gcols;
-    quantize_block_reg<T>(p, bi, b - bi * gcols, b, raw, red);
+    quantize_block_reg<T, kSR>(p, bi, b - bi * gcols, b, raw, red);
   }
 }
 
@@ -1260,14 +1286,14 @@ static cudaError_t launch_k1_tma(const QuantParams& p, cudaStream_t s) {
   return launch_ex(fbq_quantize_tma_kernel<T, kSR, kQStages>, dim3((unsigned)grid), dim3(kQuantThreads), smem, s,
                    p.pdl, m, p, nblk, gcols);
 }
-template <typename T, int kQStages, int kMinBlocks>
+template <typename T, int kQStages, int kMinBlocks, int kSR>
 static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
   const size_t smem = (size_t)kQStages * sizeof(T) * kTileElems;
   static int ctas_per_sm = 0;
   if (!ctas_per_sm) {
-    if (cudaError_t e = opt_in_smem(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks>, smem)) return e;
+    if (cudaError_t e = opt_in_smem(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, smem)) return e;
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>,
                                                       kQuantThreads, smem) != cudaSuccess || n < 1)
       n = 1;
     ctas_per_sm = n;
@@ -1289,7 +1315,7 @@ static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
   const int64_t nblk = (int64_t)gcols * ((p.rows + kBlock - 1) / kBlock);
   int64_t grid = (int64_t)num_sms() * ctas_per_sm;
   if (grid > nblk) grid = nblk;
-  return launch_ex(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks>, dim3((unsigned)grid), dim3(kQuantThreads),
+  return launch_ex(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, dim3((unsigned)grid), dim3(kQuantThreads),
                    smem, s, p.pdl, m, p, (int)nblk, gcols);
 }
 
@@ -1308,7 +1334,11 @@ static cudaError_t launch_k1_tma_any(QuantParams p, cudaStream_t s) {
 
 // diagnostics: 1 = force the smem-staged one-block-per-CTA K1, 2 = the
 // persistent TMA-pipelined K1 for SR launches, 4 = bf16 TMA ring 3 stages x
-// 2 CTAs per SM (A/B comparisons; results are identical)
+// 2 CTAs per SM, 8 = SR launches on the register-resident K1 instead of the
+// smem-staged one (A/B comparisons; results are identical.  Measured on B200:
+// the register-resident SR variant is 25-45 % SLOWER -- with the RNG's ~17
+// integer instructions per element it needs 128 registers, i.e. 16 warps per
+// SM, too few to hide its latency; scripts/sr_ab.py)
 int g_quant_diag = 0;
 
 cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
@@ -1322,14 +1352,31 @@ cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
   const int64_t nblk = (int64_t)grid.x * grid.y;
   // register-resident K1: RTN / fallback detect with 8-byte aligned code planes
   const bool sr = p.sr_codes || p.sr_codes2;
-  if (vec && !sr && !(g_quant_diag & 1) && p.vec_store) {
-    if (bf16 && nblk >= 2 * num_sms() && p.rows < (1ll << 31) && p.cols < (1ll << 31))
+  if (vec && !(g_quant_diag & 1) && p.vec_store && (!sr || (g_quant_diag & 8))) {
+    QuantParams q = p;  // compact the stochastic planes into kSR = 0, 1, 2
+    if (!q.sr_codes && q.sr_codes2) {
+      q.sr_codes = q.sr_codes2;
+      q.sr_seed = q.sr_seed2;
+      q.sr_codes2 = nullptr;
+    }
+    const int nsr = q.sr_codes2 ? 2 : (q.sr_codes ? 1 : 0);
+    if (bf16 && nblk >= 2 * num_sms() && p.rows < (1ll << 31) && p.cols < (1ll << 31)) {
       // 2-stage ring, three CTAs (24 warps) per SM: measured faster than
       // 3 stages x 2 CTAs (latency hiding of the rounding passes matters more)
-      return (g_quant_diag & 4) ? launch_k1_tma_reg<__nv_bfloat16, 3, 2>(p, s)
-                                : launch_k1_tma_reg<__nv_bfloat16, 2, 3>(p, s);
-    if (bf16) return launch_ex(fbq_quantize_reg_kernel<__nv_bfloat16>, grid, dim3(kQuantThreads), 0, s, p.pdl, p);
-    return launch_ex(fbq_quantize_reg_kernel<float>, grid, dim3(kQuantThreads), 0, s, p.pdl, p);
+      if (nsr == 2) return launch_k1_tma_reg<__nv_bfloat16, 3, 2, 2>(q, s);
+      if (nsr == 1) return launch_k1_tma_reg<__nv_bfloat16, 3, 2, 1>(q, s);
+      return (g_quant_diag & 4) ? launch_k1_tma_reg<__nv_bfloat16, 3, 2, 0>(q, s)
+                                : launch_k1_tma_reg<__nv_bfloat16, 2, 3, 0>(q, s);
+    }
+    const dim3 b(kQuantThreads);
+    if (bf16) {
+      if (nsr == 2) return launch_ex(fbq_quantize_reg_kernel<__nv_bfloat16, 2>, grid, b, 0, s, q.pdl, q);
+      if (nsr == 1) return launch_ex(fbq_quantize_reg_kernel<__nv_bfloat16, 1>, grid, b, 0, s, q.pdl, q);
+      return launch_ex(fbq_quantize_reg_kernel<__nv_bfloat16, 0>, grid, b, 0, s, q.pdl, q);
+    }
+    if (nsr == 2) return launch_ex(fbq_quantize_reg_kernel<float, 2>, grid, b, 0, s, q.pdl, q);
+    if (nsr == 1) return launch_ex(fbq_quantize_reg_kernel<float, 1>, grid, b, 0, s, q.pdl, q);
+    return launch_ex(fbq_quantize_reg_kernel<float, 0>, grid, b, 0, s, q.pdl, q);
   }
   if (vec && (g_quant_diag & 2) && nblk >= 2 * num_sms() && p.rows < (1ll << 31) &&
       p.cols < (1ll << 31))
