@@ -229,7 +229,10 @@ int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
                         int64_t ldo, fbq_stream_t stream);
 
 /* Rounding probes for exhaustive tests: out_rtn[i] = RTN code of x[i]/a[i]
- * (kernels.cpp:24-40), out_sr[i] = SR code with RNG bits[i] (quant.cpp:69-77). */
+ * (kernels.cpp:24-40), out_sr[i] = SR code with RNG bits[i] (quant.cpp:69-77).
+ * path 0: scalar functions, 1: the kernels' vector paths (V = 1), 2: 10-bit
+ * context RTN (int16 out), 3: the 8-wide packed RTN path (n % 8 == 0, one
+ * scale per 8-element vector = a[8g]). */
 int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
                          int8_t* out_sr, int64_t n, int path, fbq_stream_t stream);
 

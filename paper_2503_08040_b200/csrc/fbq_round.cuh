@@ -156,6 +156,29 @@ __device__ __forceinline__ bool rtn_fast_vec(const float (&x)[V], float inv_a, f
   }
   return near;
 }
+// Exact correction of rtn_fast_vec's words in place, for vectors whose
+// boundary test fired (~20 % of bf16 vectors: a bf16 value sitting near a
+// tie repeats many times in a block).  Same arithmetic as rtn_code_fast --
+// n = m - M, exact remainder r = x - n a, step toward r when 2|r| > a or on
+// an exact tie with n odd -- on element pairs and inline (no call frame): the
+// code is the low byte / halfword of m + step.  |x| <= amax keeps the result
+// inside +-level, so no clamp is needed.
+template <int V>
+__device__ __forceinline__ void rtn_fix_vec(const float (&x)[V], float a, uint32_t (&w)[V]) {
+  static_assert(V % 2 == 0, "pairs");
+  const float2 nmag = make_float2(-kMagic, -kMagic), na = make_float2(-a, -a);
+#pragma unroll
+  for (int i = 0; i < V; i += 2) {
+    const float2 n = __fadd2_rn(make_float2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), nmag);
+    const float2 r = __ffma2_rn(n, na, make_float2(x[i], x[i + 1]));  // exact
+    const float2 r2 = __fadd2_rn(r, r);                                // exact
+    const float t0 = fabsf(r2.x), t1 = fabsf(r2.y);
+    const bool s0 = (t0 > a) | ((t0 == a) & ((w[i] & 1u) != 0));
+    const bool s1 = (t1 > a) | ((t1 == a) & ((w[i + 1] & 1u) != 0));
+    w[i] += s0 ? (r2.x > 0.0f ? 1u : 0xFFFFFFFFu) : 0u;
+    w[i + 1] += s1 ? (r2.y > 0.0f ? 1u : 0xFFFFFFFFu) : 0u;
+  }
+}
 template <int V>
 __device__ __forceinline__ void rtn_exact_vec(const float (&x)[V], float a, float inv_a,
                                               float level, uint32_t (&w)[V]) {

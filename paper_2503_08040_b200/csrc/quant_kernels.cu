@@ -176,7 +176,10 @@ template <int V>
 __device__ __forceinline__ void rtn_vec(const float (&v)[V], float a, float inv_a, int mode,
                                         uint32_t (&w)[V]) {
   if (mode == 2) {
-    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) rtn_exact_vec<V>(v, a, inv_a, 127.0f, w);
+    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) {
+      if constexpr (V % 2 == 0) rtn_fix_vec<V>(v, a, w);
+      else rtn_exact_vec<V>(v, a, inv_a, 127.0f, w);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < V; ++i) w[i] = mode == 0 ? 0u : (uint32_t)rtn_code_slow(v[i], a, 127.0f);
@@ -367,19 +370,6 @@ __device__ __forceinline__ void unpack(const uint4& raw, float (&v)[16 / sizeof(
     v[3] = __uint_as_float(raw.w);
   }
 }
-// exact RTN of one vector (out of line: taken with probability ~2^-12 per element)
-template <typename T>
-__device__ __noinline__ uint2 rtn_exact_raw(uint4 raw, float a, float inv_a, float level) {
-  constexpr int V = 16 / sizeof(T);
-  float v[V];
-  unpack<T>(raw, v);
-  uint32_t w[V];
-  rtn_exact_vec<V>(v, a, inv_a, level, w);
-  uint2 out;
-  out.x = pack4_lo8(w);
-  out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
-  return out;
-}
 template <typename T>
 __device__ __noinline__ uint2 rtn_slow_raw(uint4 raw, float a, float level) {
   constexpr int V = 16 / sizeof(T);
@@ -388,6 +378,22 @@ __device__ __noinline__ uint2 rtn_slow_raw(uint4 raw, float a, float level) {
   uint32_t w[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) w[i] = (uint32_t)rtn_code_slow(v[i], a, level);
+  uint2 out;
+  out.x = pack4_lo8(w);
+  out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
+  return out;
+}
+// A vector whose boundary test fired (~20 % of bf16 vectors): fast path again
+// plus the exact packed correction, out of line so the 8x-unrolled main path
+// of the 80-register persistent variant stays spill-free.
+template <typename T>
+__device__ __noinline__ uint2 rtn_fix_raw(uint4 raw, float a, float inv_a) {
+  constexpr int V = 16 / sizeof(T);
+  float v[V];
+  unpack<T>(raw, v);
+  uint32_t w[V];
+  rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w);
+  rtn_fix_vec<V>(v, a, w);
   uint2 out;
   out.x = pack4_lo8(w);
   out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
@@ -402,7 +408,7 @@ __device__ __forceinline__ uint2 rtn_raw(const uint4& raw, float a, float inv_a,
     float v[V];
     unpack<T>(raw, v);
     uint32_t w[V];
-    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) return rtn_exact_raw<T>(raw, a, inv_a, 127.0f);
+    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) return rtn_fix_raw<T>(raw, a, inv_a);
     uint2 out;
     out.x = pack4_lo8(w);
     out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
@@ -410,6 +416,12 @@ __device__ __forceinline__ uint2 rtn_raw(const uint4& raw, float a, float inv_a,
   }
   if (mode == 1) return rtn_slow_raw<T>(raw, a, 127.0f);
   return make_uint2(0u, 0u);
+}
+// the same, out of line: the fallback residual of flagged blocks recomputes
+// the primary codes through this (keeps the unrolled main path small)
+template <typename T>
+__device__ __noinline__ uint2 rtn_raw_call(uint4 raw, float a, float inv_a, int mode) {
+  return rtn_raw<T>(raw, a, inv_a, mode);
 }
 __device__ __forceinline__ float code_of(const uint2& c, int i) {
   const uint32_t w = i < 4 ? c.x : c.y;
@@ -470,15 +482,16 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
     if (p.res_scales && !flagged) p.res_scales[blk] = 0.0f;
   }
   // ---- RTN codes (kernels.cpp:24-40) ----
-  uint2 code[NP];
+  // (the codes are not kept in registers: the fallback residual below -- 5-20 %
+  // of blocks -- recomputes them, which keeps this variant inside 80 registers)
   int8_t* cp = p.codes ? p.codes + r0 * p.ldq + cc : nullptr;
 #pragma unroll
   for (int ps = 0; ps < NP; ++ps) {
-    code[ps] = rtn_raw<T>(raw[ps], a, inv_a, mode);
+    const uint2 code = rtn_raw<T>(raw[ps], a, inv_a, mode);
     if (cp && col_ok && ps < nrow) {
       int8_t* dst = cp + (int64_t)ps * RPP * p.ldq;
-      if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), code[ps]);
-      else __stcs(reinterpret_cast<unsigned int*>(dst), code[ps].x);
+      if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), code);
+      else __stcs(reinterpret_cast<unsigned int*>(dst), code.x);
     }
   }
   // ---- stochastic context planes (quant.cpp:55-84): RNG index (row_offset + r) * cols + c ----
@@ -514,8 +527,9 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   for (int ps = 0; ps < NP; ++ps) {
     float v[V];
     unpack<T>(raw[ps], v);
+    const uint2 code = rtn_raw_call<T>(raw[ps], a, inv_a, mode);
 #pragma unroll
-    for (int i = 0; i < V; ++i) rm = fmaxf(rm, fabsf(__fsub_rn(v[i], __fmul_rn(code_of(code[ps], i), a))));
+    for (int i = 0; i < V; ++i) rm = fmaxf(rm, fabsf(__fsub_rn(v[i], __fmul_rn(code_of(code, i), a))));
   }
   const float ra = block_scale(block_max(rm, red));
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
@@ -528,8 +542,9 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
     if (ps >= nrow) break;
     float v[V];
     unpack<T>(raw[ps], v);
+    const uint2 code = rtn_raw_call<T>(raw[ps], a, inv_a, mode);
 #pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn(code_of(code[ps], i), a));
+    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn(code_of(code, i), a));
     uint32_t w[V];
     rtn_vec<V>(v, ra, inv_ra, rmode, w);
     int8_t* dst = rp + (int64_t)ps * RPP * p.ldq;
@@ -711,7 +726,10 @@ __device__ __forceinline__ float group_rtn(const float (&x)[V], uint32_t (&w)[V]
   const float s = m > 0.0f ? __fdiv_rn(m, level) : 0.0f;
   const float inv = s > 0.0f ? __frcp_rn(s) : 0.0f;
   if (s >= kTinyScale) {
-    if (rtn_fast_vec<V>(x, inv, rtn_window(level), w)) rtn_exact_vec<V>(x, s, inv, level, w);
+    if (rtn_fast_vec<V>(x, inv, rtn_window(level), w)) {
+      if constexpr (V % 2 == 0) rtn_fix_vec<V>(x, s, w);
+      else rtn_exact_vec<V>(x, s, inv, level, w);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < V; ++i) w[i] = s > 0.0f ? (uint32_t)rtn_code_slow(x[i], s, level) : 0u;
@@ -1137,6 +1155,23 @@ __global__ void fbq_dequantize_kernel(DequantParams p) {
 // context RTN (group_rtn's path, level 511, |x| <= 511 a; out_rtn holds n int16).
 __global__ void fbq_round_probe_kernel(const float* x, const float* a, const uint64_t* bits,
                                        int8_t* out_rtn, int8_t* out_sr, int64_t n, int path) {
+  if (path == 3) {
+    // the 8-wide packed RTN fast path with its two-level boundary test, one
+    // vector per thread with the scale of the vector's first element
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n / 8;
+         g += (int64_t)gridDim.x * blockDim.x) {
+      const float ai = a[8 * g];
+      const float inv = ai > 0.0f ? __frcp_rn(ai) : 0.0f;
+      float v[8];
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = x[8 * g + j];
+      rtn_vec<8>(v, ai, inv, round_mode(ai), w);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out_rtn[8 * g + j] = (int8_t)(uint8_t)w[j];
+    }
+    return;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float ai = a[i];

@@ -90,6 +90,28 @@ def test_rtn_near_ties_all_scale_binades(path):
     assert np.array_equal(got, ref_rtn(x, a))
 
 
+def test_rtn_packed_vector_path_near_ties():
+    """Path 3: the 8-wide packed fast path (FMUL2/FADD2/FFMA2, 3-input |d|
+    max) with its exact fallback, on vectors sharing one scale: near-ties,
+    exact ties, repeated values and tiny scales."""
+    rng = np.random.default_rng(5)
+    n = 1 << 21
+    g = n // 8
+    e = rng.integers(-140, 60, g)
+    a = np.repeat((rng.uniform(1, 2, g) * 2.0 ** e).astype(np.float32), 8)
+    k = rng.integers(-127, 128, n)
+    half = 0.5 * rng.choice([-1, 1, 0], n)
+    base = ((k + half) * a.astype(np.float64)).astype(np.float32)
+    jit = rng.integers(-3, 4, n).astype(np.int32)
+    x = (base.view(np.int32) + jit).view(np.float32)
+    x[::5] = np.repeat(x[::40], 8)[: x[::5].size]  # repeated values across vectors
+    amax = 127 * a.astype(np.float64)
+    x = np.where(np.abs(x.astype(np.float64)) <= amax, x, (np.sign(x) * amax).astype(np.float32))
+    x = np.where(np.isfinite(x), x, 0).astype(np.float32)
+    got, _ = probe(x, a, path=3)
+    assert np.array_equal(got, ref_rtn(x, a))
+
+
 def test_rtn10_context_path():
     rng = np.random.default_rng(3)
     x, a = near_tie_inputs(rng, 1 << 22, 511)
