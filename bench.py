@@ -388,7 +388,7 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     from paper_2503_08040_b200 import fbq, linear
-    from paper_2503_08040_b200.dist import allreduce_grads, max_over_ranks
+    from paper_2503_08040_b200.dist import allreduce_mlp_grads_overlapped, max_over_ranks
 
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -422,13 +422,16 @@ def run_ours(args, rank, world, local):
 
     stream = torch.cuda.current_stream()
 
+    comm = torch.cuda.Stream() if world > 1 else None
+
     def step(i):
         mlp.zero_grad()
         mlp.forward(x, i, row_offset, out=y)
         mlp.backward(gy, i, row_offset, out=gx)
-        mlp.controller_step()
         if world > 1:
-            allreduce_grads([d_grad, gu_grad])
+            # dW_down's all-reduce overlaps the GLU backward + gate/up GEMMs
+            allreduce_mlp_grads_overlapped(mlp, gu_grad, d_grad, comm)
+        mlp.controller_step()
 
     clk = ClockSampler(local)
     clk.__enter__()  # sample from the first warm-up step through the timed region

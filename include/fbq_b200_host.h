@@ -91,6 +91,12 @@ int64_t fbq_mlp_launch_count(void* mlp);
  * all-reduce): which = 0 gate (d_ff x d_model), 1 up, 2 down (d_model x d_ff).
  * gate and up are contiguous ([gate; up]). */
 void* fbq_mlp_grad_ptr(void* mlp, int which);
+/* Make `stream` wait until gradient `which` (0/1: dW_gate|dW_up, final at the
+ * end of backward; 2: dW_down, final right after its GEMM, i.e. while the GLU
+ * backward and the gate/up GEMMs are still running) of the LAST enqueued
+ * backward is complete: data-parallel callers all-reduce dW_down on a side
+ * stream overlapped with the rest of the backward. */
+int fbq_mlp_wait_grad(void* mlp, int which, fbq_stream_t stream);
 /* Copy gradients / fallback statistics to the host (synchronises). */
 int fbq_mlp_get_grads(void* mlp, float* g_gate, float* g_up, float* g_down);
 /* rates[2] = last fallback rate of gate/up and down; thresholds[2] likewise */

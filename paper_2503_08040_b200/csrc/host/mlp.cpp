@@ -100,6 +100,7 @@ struct Mlp {
   DevBuf hx, hgy, hy, hgx;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_x = nullptr, ev_gy = nullptr, ev_fwd = nullptr, ev_bwd = nullptr;
+  cudaEvent_t ev_grad[2] = {nullptr, nullptr};  // [0] dW_gate|up final, [1] dW_down final
 
   Mlp(const fbq_mlp_config& cfg, const float* wg, const float* wu, const float* wd) : c(cfg) {
     D = c.d_model;
@@ -163,6 +164,7 @@ struct Mlp {
     CU_TRY(cudaEventCreateWithFlags(&ev_gy, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_bwd, cudaEventDisableTiming));
+    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1]}) CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
 
   ~Mlp() {
@@ -173,7 +175,7 @@ struct Mlp {
     async_free();
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
-    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd})
+    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1]})
       if (e) cudaEventDestroy(e);
   }
 
@@ -270,6 +272,9 @@ struct Mlp {
     gemm([&] { return fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_MN_MAJOR,
                           ctx_h.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
                           nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, 1, c.epilogue, s); }, s);
+    // dW_d is final for this step: data-parallel callers start its all-reduce
+    // on a side stream here, overlapped with the rest of the backward
+    CU_TRY(cudaEventRecord(ev_grad[1], s));
     // GLU backward fused with SR(ga), SR(gb)
     FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.as<int16_t>(),
                                   ctx_b.as<int16_t>(), ldF, ctx_a_s.as<float>(),
@@ -281,14 +286,25 @@ struct Mlp {
     const int64_t lds_gq = 2 * gF;
     int8_t* gqc = gq.as<int8_t>();
     float* gqs = gq_scales.as<float>();
-    gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_K_MAJOR, wgu_codes.as<int8_t>(), ldD,
-                             wgu_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr,
-                             tok, D, F, gx, c.act_dtype, D, 0,
-                             c.epilogue, s); }, s);
-    gemm([&] { return fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_K_MAJOR,
-                             wgu_codes.as<int8_t>() + F * ldD, ldD,
-                             wgu_scales.as<float>() + gF * gD, gD, FBQ_MN_MAJOR, nullptr, nullptr,
-                             nullptr, tok, D, F, gx, c.act_dtype, D, 1, c.epilogue, s); }, s);
+    if (c.epilogue == FBQ_EPI_EXACT) {
+      // the reference's order: fl(bqg(ga, W_g) + bqg(gb, W_u)), two GEMMs
+      gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_K_MAJOR, wgu_codes.as<int8_t>(), ldD,
+                               wgu_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr,
+                               tok, D, F, gx, c.act_dtype, D, 0,
+                               c.epilogue, s); }, s);
+      gemm([&] { return fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_K_MAJOR,
+                               wgu_codes.as<int8_t>() + F * ldD, ldD,
+                               wgu_scales.as<float>() + gF * gD, gD, FBQ_MN_MAJOR, nullptr, nullptr,
+                               nullptr, tok, D, F, gx, c.act_dtype, D, 1, c.epilogue, s); }, s);
+    } else {
+      // FMA epilogue (tolerance mode): ONE GEMM over K = 2 d_ff -- [ga | gb]
+      // and [W_g; W_u] are already laid out as one operand each (codes and
+      // scale grids), so the two products sum in the fp32 accumulator instead
+      // of a second GEMM re-reading and re-writing dX
+      gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_K_MAJOR, wgu_codes.as<int8_t>(), ldD,
+                               wgu_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr,
+                               tok, D, 2 * F, gx, c.act_dtype, D, 0, c.epilogue, s); }, s);
+    }
     // dW_g += bqg(ga^T, ctx_g) ; dW_u += bqg(gb^T, ctx_u)
     gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_MN_MAJOR, ctx_g.as<int8_t>(), ldD,
                              x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr, F,
@@ -297,6 +313,7 @@ struct Mlp {
                              ldD, x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr,
                              nullptr, F, D, tok, g_gu.as<float>() + F * D, FBQ_F32, D, 1,
                              c.epilogue, s); }, s);
+    CU_TRY(cudaEventRecord(ev_grad[0], s));
   }
 
   void controller(cudaStream_t s) {
@@ -666,6 +683,14 @@ int fbq_mlp_gemm_time(void* m, double* total_ms, int64_t* n_gemms) {
 }
 
 int64_t fbq_mlp_launch_count(void* m) { return m ? static_cast<Mlp*>(m)->launches : 0; }
+
+int fbq_mlp_wait_grad(void* m, int which, fbq_stream_t stream) {
+  if (!m || which < 0 || which > 2) return FBQ_ERR_ARG;
+  auto* mlp = static_cast<Mlp*>(m);
+  cudaEvent_t e = mlp->ev_grad[which == 2 ? 1 : 0];
+  return cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), e, 0) == cudaSuccess ? FBQ_OK
+                                                                                          : FBQ_ERR_CUDA;
+}
 
 void* fbq_mlp_grad_ptr(void* m, int which) {
   if (!m) return nullptr;

@@ -34,6 +34,23 @@ def allreduce_grads(tensors, group=None, async_op=False):
     return works if async_op else []
 
 
+def allreduce_mlp_grads_overlapped(mlp, gu_grad, d_grad, comm_stream, group=None):
+    """The dW all-reduce of one fallback-quantized MLP step, overlapped with
+    its backward: call right after ``mlp.backward(...)`` was enqueued.  dW_down
+    is final as soon as its GEMM ends (``fbq_mlp_wait_grad``), so its NCCL
+    all-reduce runs on ``comm_stream`` while the GLU backward and the gate/up
+    GEMMs still occupy the compute stream; dW_gate|up follows the backward.
+    On return the current stream is ordered after both reductions."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return
+    with torch.cuda.stream(comm_stream):
+        mlp.wait_grad(2, comm_stream)
+        w_down = dist.all_reduce(d_grad, op=dist.ReduceOp.SUM, group=group, async_op=True)
+    w_gu = dist.all_reduce(gu_grad, op=dist.ReduceOp.SUM, group=group, async_op=True)
+    w_down.wait()
+    w_gu.wait()
+
+
 def max_over_ranks(value: float, device=None) -> float:
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return value

@@ -44,6 +44,7 @@ _sigs = {
                                           C.c_void_p, C.c_void_p, C.c_int]),
     "fbq_mlp_host_sync": (C.c_int, [C.c_void_p]),
     "fbq_mlp_grad_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "fbq_mlp_wait_grad": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "fbq_mlp_get_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fbq_mlp_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "fbq_host_last_error": (C.c_char_p, []),
@@ -157,6 +158,11 @@ class GluMlp:
 
     def zero_grad(self):
         _check(lib.fbq_mlp_zero_grad(self._h, _stream()), "zero_grad")
+
+    def wait_grad(self, which: int, stream) -> None:
+        """Make `stream` wait until gradient `which` (0/1 gate/up, 2 down) of the
+        last enqueued backward is final (dW_down: right after its GEMM)."""
+        _check(lib.fbq_mlp_wait_grad(self._h, which, stream.cuda_stream), "wait_grad")
 
     def grad_tensors(self):
         """Device fp32 views (gate+up contiguous, down) for the DP all-reduce."""

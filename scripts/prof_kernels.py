@@ -37,7 +37,14 @@ if what == "mlp":
     mlp = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.bfloat16, mid_dtype=torch.bfloat16, exact=False)
     x = bench.make_activations(T, bench.D_MODEL, 1000, "cuda", torch.bfloat16)
     gy = bench.make_grads(T, bench.D_MODEL, 2000, "cuda", torch.bfloat16)
-    mlp.set_thresholds(4.0, 1.0)
+    # the bench's calibration: 85th percentile of the block AbsMax of X and of h
+    th_gu = float(torch.quantile(fbq.score_blocks(x).flatten(), 0.85))
+    with torch.no_grad():
+        xs = x[:1024].float()
+        h = torch.nn.functional.silu(xs @ torch.from_numpy(wg).cuda().t()) * (xs @ torch.from_numpy(wu).cuda().t())
+        th_d = float(torch.quantile(fbq.score_blocks(h).flatten(), 0.85))
+        del xs, h
+    mlp.set_thresholds(th_gu, th_d)
     for i in range(2):
         mlp.zero_grad(); mlp.forward(x, i); mlp.backward(gy, i); mlp.controller_step()
     torch.cuda.synchronize()

@@ -171,3 +171,53 @@ def test_mlp_pipelined_host_api_matches_sync(mods):
     for a, b in zip(m1.grads_host(), m2.grads_host()):
         assert np.array_equal(a, b)
     assert m1.controller_state() == m2.controller_state()
+
+
+def test_mlp_fma_epilogue_fp32_close_to_reference(mods):
+    """fp32 activations, FMA epilogue: dX comes from ONE GEMM over K = 2 d_ff
+    ([ga | gb] x [W_g; W_u]) instead of the reference's two products added;
+    outputs and gradients stay close to the reference (the codes of later
+    layers may flip where an FMA-rounded value crosses a rounding boundary)."""
+    import torch
+    linear, RefMlp = mods
+    wg, wu, wd = weights(15)
+    x, gy = inputs(16)
+    ref = RefMlp(wg, wu, wd, threshold=4.0)
+    y_r, gx_r = ref.step(x, gy, 0)
+    m = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.float32, exact=False,
+                      threshold_init=4.0)
+    y = m.forward(_dev(x), 0).cpu().numpy()
+    gx = m.backward(_dev(gy), 0).cpu().numpy()
+    assert rel_fro(y, y_r) < 1e-3
+    assert rel_fro(gx, gx_r) < 1e-2
+    for g, g_r in zip(m.grads_host(), ref.grads()):
+        assert rel_fro(g, g_r) < 1e-2
+
+
+def test_mlp_grad_ready_events():
+    """fbq_mlp_wait_grad: a side stream ordered after dW_down's event sees the
+    final dW_down while the rest of the backward may still run (the hook the
+    data-parallel all-reduce overlaps on); likewise dW_gate|up at the end."""
+    import torch
+    from paper_2503_08040_b200 import linear
+    d, f, t = 1024, 2048, 2048
+    wg, wu, wd = weights(21, d, f)
+    x, gy = inputs(22, t, d)
+    m = linear.GluMlp(wg, wu, wd, t, threshold_init=4.0)
+    gu, gd = m.grad_tensors()
+    side = torch.cuda.Stream()
+    xs, gys = _dev(x, torch.bfloat16), _dev(gy, torch.bfloat16)
+    for step in range(2):
+        m.zero_grad()
+        m.forward(xs, step)
+        m.backward(gys, step)
+        m.wait_grad(2, side)
+        with torch.cuda.stream(side):
+            early_d = gd.clone()
+        m.wait_grad(0, side)
+        with torch.cuda.stream(side):
+            early_gu = gu.clone()
+        torch.cuda.synchronize()
+        assert torch.equal(early_d, gd)
+        assert torch.equal(early_gu, gu)
+        assert float(gd.abs().sum()) > 0
