@@ -179,6 +179,38 @@ def cpu_reference(tokens, steps, warmup):
             "s_per_step": dt}
 
 
+def cpu_reference_c1(rate=0.10):
+    """BASELINE configs[0] on the reference's own CPU path, timed on this box's
+    host cores beside the GPU sweep: one fallback-quantized linear forward
+    Y = X W^T, M = N = K = 4096, block 128, topk mask at `rate`
+    (fallback_quantize single-threaded as shipped, fallback_gemm with
+    set_gemm_threads(nproc), AVX2 backend)."""
+    import numpy as np
+    from oracle.oracle import REF_oracle
+    ref = REF_oracle()
+    if ref is None:
+        raise FileNotFoundError("oracle/_ref/libfbq_ref.so not built")
+    cores = os.cpu_count() or 1
+    ref.set_gemm_threads(cores)
+    n = 4096
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, n), dtype=np.float32)
+    x[:, ::512] *= 100.0  # outlier channels
+    w = (rng.standard_normal((n, n), dtype=np.float32) * 0.02)
+    t0 = time.perf_counter()
+    mask = ref.mask_topk(ref.score_blocks_absmax(x), rate)
+    c, sc, rc, rs = ref.fallback_quantize(x, mask)
+    t_q = time.perf_counter() - t0
+    wc, ws = ref.quantize_rtn(np.ascontiguousarray(w.T))
+    t0 = time.perf_counter()
+    ref.block_gemm(c, sc, wc, ws, mask=mask, res_codes=rc, res_scales=rs)
+    t_g = time.perf_counter() - t0
+    return {"workload": f"C1 fallback linear forward 4096^3, {rate:.0%} fallback blocks (topk)",
+            "cores": cores, "kind": "reference", "fallback_gemm_s": round(t_g, 3),
+            "fallback_gemm_GOPS": round(2 * n ** 3 / t_g / 1e9, 1),
+            "score+mask+fallback_quantize_s": round(t_q, 3)}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return  # rank 0 alone runs and prints the CPU reference
@@ -539,6 +571,11 @@ def run_ours(args, rank, world, local):
                 c4 = {"error": str(ex)[:200]}
 
         cpu = None
+        if not args.no_cpu_baseline and world == 1 and not args.no_sweep and isinstance(sweep, dict):
+            try:
+                sweep["C1 cpu reference (same box)"] = cpu_reference_c1()
+            except Exception as ex:  # pragma: no cover
+                sweep["C1 cpu reference (same box)"] = {"error": str(ex)[:200]}
         if not args.no_cpu_baseline and world == 1:
             try:
                 cb = cpu_reference(REF_SAMPLE_TOKENS, 1, 0)
