@@ -804,7 +804,11 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
 // staged dH and 10-bit contexts; one pass for both block absmaxes, one pass
 // stochastic-rounding both into [q(ga) | q(gb)] with their own RNG streams
 // (quant.cpp:55-84).
-template <typename T>
+// kStaged: dH and both contexts staged in shared memory (96 KiB for bf16:
+// two CTAs per SM); otherwise every pass reads them straight from global
+// memory (the second pass hits L2) with three CTAs per SM -- more warps for
+// an issue-bound kernel.
+template <typename T, bool kStaged>
 __global__ void __launch_bounds__(kQuantThreads)
 fbq_glu_backward_kernel(GluBwdParams g) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -818,9 +822,11 @@ fbq_glu_backward_kernel(GluBwdParams g) {
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
-  stage_tile<T, true>(tg, reinterpret_cast<const T*>(g.gh), g.ld_gh, g.rows, g.cols, r0, c0);
-  stage_tile<int16_t, true>(tca, g.ctx_a, g.ld_ctx, g.rows, g.cols, r0, c0);
-  stage_tile<int16_t, true>(tcb, g.ctx_b, g.ld_ctx, g.rows, g.cols, r0, c0);
+  if constexpr (kStaged) {
+    stage_tile<T, true>(tg, reinterpret_cast<const T*>(g.gh), g.ld_gh, g.rows, g.cols, r0, c0);
+    stage_tile<int16_t, true>(tca, g.ctx_a, g.ld_ctx, g.rows, g.cols, r0, c0);
+    stage_tile<int16_t, true>(tcb, g.ctx_b, g.ld_ctx, g.rows, g.cols, r0, c0);
+  }
   if (threadIdx.x < kBlock) {
     const int64_t r = r0 + threadIdx.x;
     sa_row[threadIdx.x] = r < g.rows ? g.ctx_a_scales[r * gcols + bj] : 0.0f;
@@ -829,18 +835,36 @@ fbq_glu_backward_kernel(GluBwdParams g) {
   __syncthreads();
   // dequantized contexts: fl(code * scale) (quant.cpp:86-104); a zero scale
   // has all-zero codes, so no special case is needed
-  auto deq = [&](const int16_t* t, float s, int rb, int cb, float (&v)[V]) {
+  auto deq = [&](const int16_t* t, const int16_t* gt, float s, int rb, int cb, float (&v)[V]) {
     int16_t c[V];
-    if constexpr (V == 8) *reinterpret_cast<uint4*>(c) = *reinterpret_cast<const uint4*>(t + rb * kBlock + cb);
-    else *reinterpret_cast<uint2*>(c) = *reinterpret_cast<const uint2*>(t + rb * kBlock + cb);
+    if constexpr (kStaged) {
+      if constexpr (V == 8) *reinterpret_cast<uint4*>(c) = *reinterpret_cast<const uint4*>(t + rb * kBlock + cb);
+      else *reinterpret_cast<uint2*>(c) = *reinterpret_cast<const uint2*>(t + rb * kBlock + cb);
+    } else {
+      const int64_t r = r0 + rb, cc = c0 + cb;
+      const bool ok = r < g.rows && cc < g.cols;
+      const int16_t* src = gt + r * g.ld_ctx + cc;
+      if constexpr (V == 8) *reinterpret_cast<uint4*>(c) = ok ? *reinterpret_cast<const uint4*>(src) : make_uint4(0, 0, 0, 0);
+      else *reinterpret_cast<uint2*>(c) = ok ? *reinterpret_cast<const uint2*>(src) : make_uint2(0, 0);
+    }
 #pragma unroll
     for (int i = 0; i < V; ++i) v[i] = __fmul_rn((float)c[i], s);
   };
   auto eval = [&](int rb, int cb, float (&ga)[V], float (&gb)[V]) {
     float a[V], b[V];
-    load_vec<T, V>(tg + rb * kBlock + cb, ga);
-    deq(tca, sa_row[rb], rb, cb, a);
-    deq(tcb, sb_row[rb], rb, cb, b);
+    if constexpr (kStaged) {
+      load_vec<T, V>(tg + rb * kBlock + cb, ga);
+    } else {
+      const int64_t r = r0 + rb, cc = c0 + cb;
+      if (r < g.rows && cc < g.cols) {
+        load_vec<T, V>(reinterpret_cast<const T*>(g.gh) + r * g.ld_gh + cc, ga);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) ga[i] = 0.0f;
+      }
+    }
+    deq(tca, g.ctx_a, sa_row[rb], rb, cb, a);
+    deq(tcb, g.ctx_b, sb_row[rb], rb, cb, b);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const float gy = ga[i];
@@ -1440,14 +1464,23 @@ cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s) {
   const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
                   (unsigned)((g.rows + kBlock - 1) / kBlock));
+  const bool staged = (g_quant_diag & 32) != 0;  // diagnostics: the smem-staged variant
   if (bf16) {
+    if (!staged) {
+      fbq_glu_backward_kernel<__nv_bfloat16, false><<<grid, kQuantThreads, 0, s>>>(g);
+      return cudaGetLastError();
+    }
     const size_t smem = (sizeof(__nv_bfloat16) + 2 * sizeof(int16_t)) * kTileElems;
-    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<__nv_bfloat16>, smem)) return e;
-    fbq_glu_backward_kernel<__nv_bfloat16><<<grid, kQuantThreads, smem, s>>>(g);
+    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<__nv_bfloat16, true>, smem)) return e;
+    fbq_glu_backward_kernel<__nv_bfloat16, true><<<grid, kQuantThreads, smem, s>>>(g);
   } else {
+    if (!staged) {
+      fbq_glu_backward_kernel<float, false><<<grid, kQuantThreads, 0, s>>>(g);
+      return cudaGetLastError();
+    }
     const size_t smem = (sizeof(float) + 2 * sizeof(int16_t)) * kTileElems;
-    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<float>, smem)) return e;
-    fbq_glu_backward_kernel<float><<<grid, kQuantThreads, smem, s>>>(g);
+    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<float, true>, smem)) return e;
+    fbq_glu_backward_kernel<float, true><<<grid, kQuantThreads, smem, s>>>(g);
   }
   return cudaGetLastError();
 }
