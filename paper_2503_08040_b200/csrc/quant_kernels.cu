@@ -332,8 +332,8 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   }
 }
 
-template <typename T, bool kVec, int kSR>
-__global__ void __launch_bounds__(kQuantThreads)
+template <typename T, bool kVec, int kSR, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_quantize_block_kernel(QuantParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   T* tile = reinterpret_cast<T*>(dsm);
@@ -808,8 +808,8 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
 // two CTAs per SM); otherwise every pass reads them straight from global
 // memory (the second pass hits L2) with three CTAs per SM -- more warps for
 // an issue-bound kernel.
-template <typename T, bool kStaged>
-__global__ void __launch_bounds__(kQuantThreads)
+template <typename T, bool kStaged, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_glu_backward_kernel(GluBwdParams g) {
   extern __shared__ __align__(16) uint8_t dsm[];
   T* tg = reinterpret_cast<T*>(dsm);
@@ -1267,10 +1267,14 @@ static cudaError_t launch_k1_sr(const QuantParams& p, dim3 grid, cudaStream_t s)
   const size_t smem = sizeof(T) * kTileElems;
   static bool ready = false;
   if (!ready) {
-    if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec, kSR>, smem)) return e;
+    if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec, kSR, sizeof(T) == 2 ? 4 : 1>, smem)) return e;
     ready = true;
   }
-  return launch_ex(fbq_quantize_block_kernel<T, kVec, kSR>, grid, dim3(kQuantThreads), smem, s, p.pdl, p);
+  // bf16 tiles (32 KiB): four CTAs per SM at 64 registers (measured 7 % faster
+  // than three at 76-82 registers for the two-plane SR launch); fp32 tiles
+  // (64 KiB) are shared-memory bound at three CTAs anyway
+  constexpr int kMinB = sizeof(T) == 2 ? 4 : 1;
+  return launch_ex(fbq_quantize_block_kernel<T, kVec, kSR, kMinB>, grid, dim3(kQuantThreads), smem, s, p.pdl, p);
 }
 template <typename T, bool kVec>
 static cudaError_t launch_k1(QuantParams p, dim3 grid, cudaStream_t s) {
@@ -1467,7 +1471,9 @@ cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s
   const bool staged = (g_quant_diag & 32) != 0;  // diagnostics: the smem-staged variant
   if (bf16) {
     if (!staged) {
-      fbq_glu_backward_kernel<__nv_bfloat16, false><<<grid, kQuantThreads, 0, s>>>(g);
+      // four CTAs (32 warps) per SM: 64 registers; measured 484 us vs 590 us
+      // at 82 registers / three CTAs (a few spilled bytes notwithstanding)
+      fbq_glu_backward_kernel<__nv_bfloat16, false, 4><<<grid, kQuantThreads, 0, s>>>(g);
       return cudaGetLastError();
     }
     const size_t smem = (sizeof(__nv_bfloat16) + 2 * sizeof(int16_t)) * kTileElems;
@@ -1475,7 +1481,7 @@ cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s
     fbq_glu_backward_kernel<__nv_bfloat16, true><<<grid, kQuantThreads, smem, s>>>(g);
   } else {
     if (!staged) {
-      fbq_glu_backward_kernel<float, false><<<grid, kQuantThreads, 0, s>>>(g);
+      fbq_glu_backward_kernel<float, false, 3><<<grid, kQuantThreads, 0, s>>>(g);
       return cudaGetLastError();
     }
     const size_t smem = (sizeof(float) + 2 * sizeof(int16_t)) * kTileElems;
