@@ -1397,7 +1397,9 @@ static cudaError_t launch_k1_tma_any(QuantParams p, cudaStream_t s) {
 
 // diagnostics: 1 = force the smem-staged one-block-per-CTA K1, 2 = the
 // persistent TMA-pipelined K1 for SR launches, 4 = bf16 TMA ring 3 stages x
-// 2 CTAs per SM, 8 = SR launches on the register-resident K1 instead of the
+// 2 CTAs per SM, 128 = bf16 RTN on the one-block-per-CTA register kernel
+// instead of the persistent TMA one (8192x14336: 99 vs 79 us), 8 = SR
+// launches on the register-resident K1 instead of the
 // smem-staged one (A/B comparisons; results are identical.  Measured on B200:
 // the register-resident SR variant is 25-45 % SLOWER -- with the RNG's ~17
 // integer instructions per element it needs 128 registers, i.e. 16 warps per
@@ -1423,7 +1425,8 @@ cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
       q.sr_codes2 = nullptr;
     }
     const int nsr = q.sr_codes2 ? 2 : (q.sr_codes ? 1 : 0);
-    if (bf16 && nblk >= 2 * num_sms() && p.rows < (1ll << 31) && p.cols < (1ll << 31)) {
+    if (bf16 && nblk >= 2 * num_sms() && p.rows < (1ll << 31) && p.cols < (1ll << 31) &&
+        !(g_quant_diag & 128)) {
       // 2-stage ring, three CTAs (24 warps) per SM: measured faster than
       // 3 stages x 2 CTAs (latency hiding of the rounding passes matters more)
       if (nsr == 2) return launch_k1_tma_reg<__nv_bfloat16, 3, 2, 2>(q, s);
