@@ -742,8 +742,8 @@ __device__ __forceinline__ float group_rtn(const float (&x)[V], uint32_t (&w)[V]
 // in the row; only the VPR threads of that row -- one warp or half-warp --
 // touch it, so a __syncwarp orders their reads before their writes).  h is
 // thus evaluated once and never reaches HBM.
-template <typename T>
-__global__ void __launch_bounds__(kQuantThreads)
+template <typename T, bool kStaged, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_glu_forward_kernel(GluParams g, QuantParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   constexpr int kRow = 2 * kBlock;                      // T per smem row
@@ -756,12 +756,40 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
   const T* ab = reinterpret_cast<const T*>(g.ab);
-  stage_tile<T, true>(tab, ab, g.ld_ab, g.rows, g.cols, r0, c0, kRow);
-  stage_tile<T, true>(tab + kBlock, ab + g.cols, g.ld_ab, g.rows, g.cols, r0, c0, kRow);
-  __syncthreads();
+  if constexpr (kStaged) {
+    stage_tile<T, true>(tab, ab, g.ld_ab, g.rows, g.cols, r0, c0, kRow);
+    stage_tile<T, true>(tab + kBlock, ab + g.cols, g.ld_ab, g.rows, g.cols, r0, c0, kRow);
+    __syncthreads();
+  }
   const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
   const int64_t cc = c0 + lc;
+  // a and b of (row rb, this thread's V columns): staged tile or global memory
+  // (zero outside the tensor: silu(0) * 0 = 0, like the staged zero fill)
+  auto load_ab = [&](int rb, int cb, float (&va)[V], float (&vb)[V]) {
+    if constexpr (kStaged) {
+      load_vec<T, V>(tab + rb * kRow + cb, va);
+      load_vec<T, V>(tab + rb * kRow + kBlock + cb, vb);
+    } else {
+      const int64_t r = r0 + rb, c = c0 + cb;
+      if (r < g.rows && c < g.cols) {
+        load_vec<T, V>(ab + r * g.ld_ab + c, va);
+        load_vec<T, V>(ab + r * g.ld_ab + g.cols + c, vb);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) va[i] = vb[i] = 0.0f;
+      }
+    }
+  };
+  // h = fl(silu(a) * b) (trainsim.cpp:230), deterministic: the direct variant
+  // re-evaluates it in every pass instead of keeping a 64 KiB fp32 tile
+  auto hval = [&](const float (&va)[V], const float (&vb)[V], float (&vh)[V]) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float sa = g.exact_math ? silu_ref(va[i]) : silu_fast(va[i]);
+      vh[i] = __fmul_rn(sa, vb[i]);
+    }
+  };
   // 10-bit contexts of a and b (trainsim.cpp:240-243), h and its absmax
   float m = 0.0f;
 #pragma unroll 1
@@ -770,8 +798,7 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
     const int64_t r = r0 + rb;
     const bool ok = r < g.rows && cc < g.cols;  // cols % 8 == 0: uniform per row group
     float va[V], vb[V];
-    load_vec<T, V>(tab + rb * kRow + lc, va);
-    load_vec<T, V>(tab + rb * kRow + kBlock + lc, vb);
+    load_ab(rb, lc, va, vb);
     uint32_t code[V];
     float s = group_rtn<V, VPR>(va, code, g.ctx_level);
     if (ok && g.ctx_a) store_codes16<V>(g.ctx_a + r * g.ld_ctx + cc, code);
@@ -779,24 +806,36 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
     s = group_rtn<V, VPR>(vb, code, g.ctx_level);
     if (ok && g.ctx_b) store_codes16<V>(g.ctx_b + r * g.ld_ctx + cc, code);
     if (ok && g.ctx_b_scales && lc == 0) g.ctx_b_scales[r * gcols + bj] = s;
-    // h = fl(silu(a) * b) (trainsim.cpp:230); zero-filled lanes: silu(0) * 0 = 0
+    float vh[V];
+    hval(va, vb, vh);
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float sa = g.exact_math ? silu_ref(va[i]) : silu_fast(va[i]);
-      va[i] = __fmul_rn(sa, vb[i]);
-      m = fmaxf(m, fabsf(va[i]));
-    }
+    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(vh[i]));
     if (ok && g.h_out) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) g.h_out[r * g.ld_h + cc + i] = va[i];
+      for (int i = 0; i < V; ++i) g.h_out[r * g.ld_h + cc + i] = vh[i];
     }
-    __syncwarp();
-    store_f32<V>(th + rb * kRowF + lc, va);
+    if constexpr (kStaged) {
+      // h as 128 fp32 IN PLACE of the row's [a | b] (512 bytes; only the VPR
+      // threads of that row touch it, so a __syncwarp orders reads before writes)
+      __syncwarp();
+      store_f32<V>(th + rb * kRowF + lc, vh);
+    }
   }
   // h quantized like a linear input (K1, fused)
-  quantize_block<V, 1>(
-      p, bi * gridDim.x + bj, r0, c0, red,
-      [&](int rb, int cb, float (&v)[V]) { load_vec<float, V>(th + rb * kRowF + cb, v); }, true, m);
+  if constexpr (kStaged) {
+    quantize_block<V, 1>(
+        p, bi * gridDim.x + bj, r0, c0, red,
+        [&](int rb, int cb, float (&v)[V]) { load_vec<float, V>(th + rb * kRowF + cb, v); }, true, m);
+  } else {
+    quantize_block<V, 1>(
+        p, bi * gridDim.x + bj, r0, c0, red,
+        [&](int rb, int cb, float (&v)[V]) {
+          float va[V], vb[V];
+          load_ab(rb, cb, va, vb);
+          hval(va, vb, v);
+        },
+        true, m);
+  }
 }
 
 // GluCombine backward (trainsim.cpp:248-263) fused with the two dY
@@ -1456,14 +1495,20 @@ cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf
                                cudaStream_t s) {
   const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
                   (unsigned)((g.rows + kBlock - 1) / kBlock));
+  // staged (default): h computed once into shared memory, three CTAs per SM
+  // (442 us on the C3 shape); diagnostics 256 = the direct variant that re-reads
+  // a|b from L2 and re-evaluates h per pass at four CTAs per SM (505 us)
   if (bf16) {
+    if (g_quant_diag & 256)
+      return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16, false, 4>, grid, dim3(kQuantThreads), 0, s,
+                       p.pdl, g, p);
     const size_t smem = 2 * sizeof(__nv_bfloat16) * kTileElems;  // a|b rows, then h (fp32) in place
-    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16>, smem)) return e;
-    return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
+    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16, true, 3>, smem)) return e;
+    return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16, true, 3>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
   } else {
     const size_t smem = 2 * sizeof(float) * kTileElems;
-    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<float>, smem)) return e;
-    return launch_ex(fbq_glu_forward_kernel<float>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
+    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<float, true>, smem)) return e;
+    return launch_ex(fbq_glu_forward_kernel<float, true>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
   }
   return cudaGetLastError();
 }
