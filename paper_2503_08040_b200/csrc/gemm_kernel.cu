@@ -69,16 +69,29 @@ constexpr size_t kSmemBytes =
     1024 + (size_t)kStages * kStageBytes + (size_t)kEpiWarps * kOutChunk + 2 * sizeof(ScalePage) + 256;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
-// Grouped rasterisation: tiles walk kGroupM block-rows at a time (bm fastest),
-// so the ~148 CTAs resident at once share kGroupM A row-panels and ~148/kGroupM
-// B column-panels in L2 instead of re-streaming all of B for every block-row
-// (row-major order read the gate/up B operand ~30x from DRAM).
+// Tile rasterisation, chosen per launch so that one operand stays resident in
+// the 126 MB L2 while the other streams once:
+//  * A small (<= 48 MiB) and B large (> 96 MiB): group_m = MB -- bm fastest over ALL block-rows, so
+//    the ~148 resident CTAs share a couple of B column panels and A is re-read
+//    from L2 only (e.g. the gate/up forward: X codes 32 MiB, W 112 MiB);
+//  * B small and A large: n_fastest -- every bn of one block-row before the next,
+//    B re-read from L2 only (e.g. dW_gate/up: the X context 32 MiB);
+//  * else groups of kGroupM block-rows (bm fastest), sharing kGroupM A
+//    row-panels and ~148/kGroupM B column-panels in L2.
+// With kGroupM groups everywhere the gate/up forward re-read all of B once per
+// group (1.03 GB of DRAM reads for 0.15 GB of operands, ncu).
 constexpr int kGroupM = 8;
-__device__ __forceinline__ void tile_coords(int tile, int MB, int NT, int& bm, int& bn2) {
-  const int per_group = kGroupM * NT;
+__device__ __forceinline__ void tile_coords(int tile, int MB, int NT, int group_m, int n_fastest,
+                                            int& bm, int& bn2) {
+  if (n_fastest) {
+    bm = tile / NT;
+    bn2 = tile - bm * NT;
+    return;
+  }
+  const int per_group = group_m * NT;
   const int group = tile / per_group;
-  const int first = group * kGroupM;
-  const int rows = min(kGroupM, MB - first);
+  const int first = group * group_m;
+  const int rows = min(group_m, MB - first);
   const int in = tile - group * per_group;
   bm = first + in % rows;
   bn2 = in / rows;
@@ -134,7 +147,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
   uint32_t tw = 0, tl = 0, tpre = 0, tpost = 0, t0 = 0, t1 = 0, t2 = 0, t3 = 0;
   for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
     int bm, bn2;
-    tile_coords(tile, p.MB, NT, bm, bn2);
+    tile_coords(tile, p.MB, NT, p.group_m, p.n_fastest, bm, bn2);
     const int bn = bn2 * 2 + h;
     float2 acc[64];
 #pragma unroll
@@ -441,7 +454,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       uint32_t phase = 0, pc = 0;
       for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         int bm, bn2;
-        tile_coords(tile, p.MB, NT, bm, bn2);
+        tile_coords(tile, p.MB, NT, p.group_m, p.n_fastest, bm, bn2);
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
           mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
@@ -537,7 +550,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     uint32_t pc = 0;
     for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       int bm, bn2;
-      tile_coords(tile, p.MB, NT, bm, bn2);
+      tile_coords(tile, p.MB, NT, p.group_m, p.n_fastest, bm, bn2);
       const int bn0 = 2 * bn2, bn1 = 2 * bn2 + 1;
       for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
         ScalePage& sp = pages[pc & 1];
@@ -676,6 +689,19 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
       p.tma_store = p.accumulate ? 2 : ((p.diag & 16384) ? 3 : 1);
   }
   p.num_tiles = p.MB * ((p.NB + 1) / 2);
+  {
+    // only when the other operand does not fit: with both small, or both
+    // large, the kGroupM groups were as fast or faster (C1 -4 %, C5 -1 %;
+    // gate/up forward +4.5 %, dW_gate/up +5 %: scripts/gemm_raster_ab.py)
+    constexpr double kResident = 48.0 * (1 << 20), kStreamed = 96.0 * (1 << 20);
+    const double a_bytes = (double)p.M * (double)p.K, b_bytes = (double)p.N * (double)p.K;
+    p.group_m = kGroupM;
+    p.n_fastest = 0;
+    if (!(p.diag & (1 << 18))) {  // diagnostics: 1 << 18 = always kGroupM groups
+      if (a_bytes <= kResident && b_bytes > kStreamed) p.group_m = p.MB;
+      else if (b_bytes <= kResident && a_bytes > kStreamed) p.n_fastest = 1;
+    }
+  }
   const int grid = p.num_tiles < gemm_num_sms() ? p.num_tiles : gemm_num_sms();
   switch (epi) {
     case kEpiExact: return launch_typed<kEpiExact>(ma, mr, mb, mo, p, grid, s);

@@ -32,6 +32,8 @@ struct GemmParams {
   int32_t* dump;            // kEpiDump: [MB][NB][KB][128][128] primary, then residual
   int64_t dump_res_offset;  // element offset of the residual products
   int num_tiles;
+  int group_m;    // tile raster: block-rows per group (bm fastest inside a group)
+  int n_fastest;  // 1: bn fastest over the whole N (B stays L2-resident)
   float one;  // 1.0f (runtime constant for the exact epilogue)
   int diag;   // perf diagnostics: 1 = skip epilogue math, 2 = skip TMA loads
   long long* prof;  // perf diagnostics: 16 int64 per CTA (MMA-warp cycles, epilogue timeline) or null
