@@ -697,7 +697,9 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
     const double a_bytes = (double)p.M * (double)p.K, b_bytes = (double)p.N * (double)p.K;
     p.group_m = kGroupM;
     p.n_fastest = 0;
-    if (!(p.diag & (1 << 18))) {  // diagnostics: 1 << 18 = always kGroupM groups
+    if (p.diag & (1 << 19)) p.group_m = p.MB;          // diagnostics/tests: force each raster
+    else if (p.diag & (1 << 20)) p.n_fastest = 1;
+    else if (!(p.diag & (1 << 18))) {  // diagnostics: 1 << 18 = always kGroupM groups
       if (a_bytes <= kResident && b_bytes > kStreamed) p.group_m = p.MB;
       else if (b_bytes <= kResident && a_bytes > kStreamed) p.n_fastest = 1;
     }

@@ -278,6 +278,32 @@ def test_gemm_many_tiles_odd_pairs(F, orc):
     assert rel_fro(host(y2), want) <= FMA_TOL
 
 
+@pytest.mark.parametrize("raster", [1 << 18, 1 << 19, 1 << 20])
+def test_gemm_tile_rasters(F, orc, raster):
+    """Every tile rasterisation the launcher may pick (kGroupM groups, bm over
+    all block-rows, bn fastest) covers each tile exactly once: bit-exact on a
+    ragged multi-wave shape with fallback blocks, plain and accumulating."""
+    lib = F.K.lib
+    lib.fbq_debug_set_gemm_diag.argtypes = [F.K.cint]
+    m, n, k = 2200, 1400, 520
+    a, b, mask = _quant_pair(orc, m, n, k, seed=43, rate=0.2)
+    w = np.ascontiguousarray(b.T)
+    wq = F.quantize_rtn(dev(w))
+    wc, ws = orc.quantize_rtn(w)
+    bc, bs = orc.transpose_qt(wc, ws)
+    fa = F.fallback_quantize(dev(a), dev(mask))
+    ac, as_, rc, rs = orc.fallback_quantize(a, mask)
+    want = orc.block_gemm(ac, as_, bc, bs, mask=mask, res_codes=rc, res_scales=rs)
+    try:
+        lib.fbq_debug_set_gemm_diag(raster)
+        y = F.fallback_gemm(fa, F.transpose(wq))
+        assert np.array_equal(host(y).view(np.int32), want.view(np.int32))
+        y2 = F.fallback_gemm(fa, F.transpose(wq), exact=False)
+        assert rel_fro(host(y2), want) <= FMA_TOL
+    finally:
+        lib.fbq_debug_set_gemm_diag(0)
+
+
 @pytest.mark.parametrize("rate", [0.0, 1e-4, 0.05, 0.2, 0.5, 1.0])
 def test_mask_topk_device_matches_reference(F, orc, rate):
     """mask_topk (policy.cpp:56-71) on the device: exactly ceil(rate*n) blocks,
