@@ -63,6 +63,8 @@ struct ScalePage {
   float prim[2][kPage];  // fl(sA * sB) for the two 128-column halves
   float res[2][kPage];   // fl(rA * sB) (flagged k-blocks only)
   uint8_t flag[kPage];   // fallback bit u(bm, bk)
+  int tile;              // the tile this page belongs to; -1: no more tiles (all roles exit)
+  int pg;                // first k-block of the page
 };
 
 constexpr size_t kSmemBytes =
@@ -145,7 +147,12 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
 
   uint32_t item = 0, pc = 0;
   uint32_t tw = 0, tl = 0, tpre = 0, tpost = 0, t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-  for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+  // tiles arrive through the scale pages (the scale-loader warp is the
+  // scheduler): the first page of each tile carries its index, -1 ends
+  for (;;) {
+    mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+    const int tile = pages[pc & 1].tile;
+    if (tile < 0) break;
     int bm, bn2;
     tile_coords(tile, p.MB, NT, p.group_m, p.n_fastest, bm, bn2);
     const int bn = bn2 * 2 + h;
@@ -154,7 +161,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
     for (int i = 0; i < 64; ++i) acc[i] = make_float2(0.0f, 0.0f);
     for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
       const ScalePage& sp = pages[pc & 1];
-      mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+      if (pg > 0) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
       const int nk = min(kPage, p.KB - pg);
       for (int j = 0; j < nk; ++j) {
         const bool masked = sp.flag[j];
@@ -452,12 +459,15 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint64_t pol = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0, pc = 0;
-      for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (;;) {
+        mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+        const int tile = pages[pc & 1].tile;
+        if (tile < 0) break;
         int bm, bn2;
         tile_coords(tile, p.MB, NT, p.group_m, p.n_fastest, bm, bn2);
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
-          mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+          if (pg > 0) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
           const int nk = min(kPage, p.KB - pg);
           for (int j = 0; j < nk; ++j) {
             const int bk = pg + j;
@@ -511,10 +521,17 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       int stage = 0;
       uint32_t phase = 0, item = 0, pc = 0;
       const long long t_start = p.prof ? clock64() : 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      // diag 512 (bare MMA loop, no scale pages): the static tile schedule
+      for (int tile = blockIdx.x;; tile += gridDim.x) {
+        if (p.diag & 512) {
+          if (tile >= p.num_tiles) break;
+        } else {
+          mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+          if (pages[pc & 1].tile < 0) break;
+        }
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
-          if (!(p.diag & 512)) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+          if (!(p.diag & 512) && pg > 0) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
           const int nk = min(kPage, p.KB - pg);
           for (int j = 0; j < nk; ++j) {
             const int n_items = (!(p.diag & 512) && sp.flag[j]) ? 2 : 1;
@@ -547,14 +564,33 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
   } else if (warp == 2) {
     // ===================== scale loader =====================
+    // The tile scheduler: the first tile is blockIdx.x, every further one is
+    // claimed from the launch's counter (p.tile_ctr, zeroed in-stream before
+    // the launch) -- CTAs that drew cheap tiles (few fallback blocks) take
+    // more, so the last wave is balanced; without a counter the static
+    // schedule tile += gridDim.x.  Each tile's pages carry its index to the
+    // other roles; a page with tile = -1 tells them to exit.
     uint32_t pc = 0;
-    for (int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x;
+    for (;;) {
+      if (tile >= p.num_tiles) {
+        ScalePage& sp = pages[pc & 1];
+        mbar_wait_sleep(sempty + (pc & 1), ((pc >> 1) & 1) ^ 1);
+        if (lane == 0) sp.tile = -1;
+        __syncwarp();
+        mbar_arrive(sfull + (pc & 1));
+        break;
+      }
       int bm, bn2;
       tile_coords(tile, p.MB, NT, p.group_m, p.n_fastest, bm, bn2);
       const int bn0 = 2 * bn2, bn1 = 2 * bn2 + 1;
       for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
         ScalePage& sp = pages[pc & 1];
         mbar_wait_sleep(sempty + (pc & 1), ((pc >> 1) & 1) ^ 1);
+        if (lane == 0) {
+          sp.tile = tile;
+          sp.pg = pg;
+        }
         const int nk = min(kPage, p.KB - pg);
         for (int j = lane; j < nk; j += 32) {
           const int bk = pg + j;
@@ -576,6 +612,9 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         __syncwarp();
         mbar_arrive(sfull + (pc & 1));
       }
+      int next = 0;
+      if (lane == 0) next = p.tile_ctr ? atomicAdd(p.tile_ctr, 1) + (int)gridDim.x : tile + (int)gridDim.x;
+      tile = __shfl_sync(0xffffffffu, next, 0);
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
@@ -689,6 +728,22 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
       p.tma_store = p.accumulate ? 2 : ((p.diag & 16384) ? 3 : 1);
   }
   p.num_tiles = p.MB * ((p.NB + 1) / 2);
+  // dynamic tile counter: a slot of a per-device ring, zeroed in-stream
+  p.tile_ctr = nullptr;
+  if (!(p.diag & (1 << 21)) && !(p.diag & 512)) {  // diagnostics: 1 << 21 = static schedule
+    static int* ring[64] = {};
+    static unsigned next_slot[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+      constexpr int kSlots = 256;
+      if (!ring[dev] && cudaMalloc(&ring[dev], kSlots * 128) != cudaSuccess) ring[dev] = nullptr;
+      if (ring[dev]) {
+        int* ctr = ring[dev] + (next_slot[dev]++ % kSlots) * 32;  // one 128-byte line per slot
+        if (cudaMemsetAsync(ctr, 0, sizeof(int), s) == cudaSuccess) p.tile_ctr = ctr;
+      }
+    }
+  }
   {
     // only when the other operand does not fit: with both small, or both
     // large, the kGroupM groups were as fast or faster (C1 -4 %, C5 -1 %;

@@ -34,6 +34,7 @@ struct GemmParams {
   int num_tiles;
   int group_m;    // tile raster: block-rows per group (bm fastest inside a group)
   int n_fastest;  // 1: bn fastest over the whole N (B stays L2-resident)
+  int* tile_ctr;  // dynamic tile counter (zeroed before the launch) or null: static schedule
   float one;  // 1.0f (runtime constant for the exact epilogue)
   int diag;   // perf diagnostics: 1 = skip epilogue math, 2 = skip TMA loads
   long long* prof;  // perf diagnostics: 16 int64 per CTA (MMA-warp cycles, epilogue timeline) or null
