@@ -58,6 +58,11 @@ int fbq_mlp_backward_device(void* mlp, const void* gy, int64_t tokens, int64_t r
                             int step, void* gx, fbq_stream_t stream);
 /* controller_step of every layer (trainsim.cpp:129-133) from the last forward */
 int fbq_mlp_controller_step(void* mlp, fbq_stream_t stream);
+/* zero_grad is deferred: the next backward's dW GEMMs write instead of
+ * accumulate (bit-identical to adding into zeroed buffers, no 0.7 GB memset
+ * per step).  fbq_mlp_get_grads / fbq_mlp_grad_ptr materialise pending zeros;
+ * a device view of the gradients obtained earlier shows the zeros only once
+ * the next backward has run. */
 int fbq_mlp_zero_grad(void* mlp, fbq_stream_t stream);
 
 /* Host API: one fwd+bwd step over host fp32 buffers (synchronous, like the
