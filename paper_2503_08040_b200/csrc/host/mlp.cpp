@@ -21,6 +21,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../../include/fbq_b200_host.h"
@@ -101,6 +102,11 @@ struct Mlp {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_x = nullptr, ev_gy = nullptr, ev_fwd = nullptr, ev_bwd = nullptr;
   cudaEvent_t ev_grad[2] = {nullptr, nullptr};  // [0] dW_gate|up final, [1] dW_down final
+  // backward side stream: the dW GEMMs run there, so each GEMM's last-wave
+  // tail (up to one 224-k-block tile on the long-K dX) is filled by the next
+  // independent grid's CTAs instead of idling SMs
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join = nullptr;
 
   Mlp(const fbq_mlp_config& cfg, const float* wg, const float* wu, const float* wd) : c(cfg) {
     D = c.d_model;
@@ -164,7 +170,9 @@ struct Mlp {
     CU_TRY(cudaEventCreateWithFlags(&ev_gy, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_bwd, cudaEventDisableTiming));
-    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1]}) CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_fork[0], &ev_fork[1], &ev_join})
+      CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CU_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   }
 
   ~Mlp() {
@@ -175,7 +183,8 @@ struct Mlp {
     async_free();
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
-    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1]})
+    if (side) cudaStreamDestroy(side);
+    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1], ev_fork[0], ev_fork[1], ev_join})
       if (e) cudaEventDestroy(e);
   }
 
@@ -203,13 +212,28 @@ struct Mlp {
     if (profiling) CU_TRY(cudaEventRecord(next_event(), s));
     ++launches;
   }
+  // GEMM busy time: the union of the [start, end] intervals (GEMMs on the
+  // backward side stream overlap the main stream's), relative to the first event
   double gemm_ms_and_reset() {
-    double total = 0.0;
+    std::vector<std::pair<float, float>> iv;
     for (size_t i = 0; i + 1 < ev_used; i += 2) {
-      float ms = 0.f;
-      CU_TRY(cudaEventElapsedTime(&ms, ev_pool[i], ev_pool[i + 1]));
-      total += ms;
+      float a = 0.f, b = 0.f;
+      CU_TRY(cudaEventElapsedTime(&a, ev_pool[0], ev_pool[i]));
+      CU_TRY(cudaEventElapsedTime(&b, ev_pool[0], ev_pool[i + 1]));
+      iv.emplace_back(a, b);
     }
+    std::sort(iv.begin(), iv.end());
+    double total = 0.0, cs = -1e30, ce = -1e30;
+    for (auto& [a, b] : iv) {
+      if (a > ce) {
+        if (ce > cs) total += ce - cs;
+        cs = a;
+        ce = b;
+      } else if (b > ce) {
+        ce = b;
+      }
+    }
+    if (ce > cs) total += ce - cs;
     ev_used = 0;
     return total;
   }
@@ -265,18 +289,21 @@ struct Mlp {
     FBQ_TRY(fbq_cuda_quantize_stochastic(gy, c.act_dtype, tok, D, D,
                                          layer_seed(c.seed, layer(2), 1, step), row_off,
                                          gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), s));
+    CU_TRY(cudaEventRecord(ev_fork[0], s));
+    CU_TRY(cudaStreamWaitEvent(side, ev_fork[0], 0));
     // dH = bqg(dY, W_d): B = W_d codes (D x F) read MN-major (trainsim.cpp:121-122)
     gemm([&] { return fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_K_MAJOR,
                           wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_MN_MAJOR,
                           nullptr, nullptr, nullptr, tok, F, D, gh.p, c.mid_dtype, F, 0,
                           c.epilogue, s); }, s);
-    // dW_d += bqg(dY^T, ctx_h) (trainsim.cpp:124-125)
+    // dW_d += bqg(dY^T, ctx_h) (trainsim.cpp:124-125), on the side stream
+    cudaStream_t b = side;
     gemm([&] { return fbq_cuda_gemm(gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), FBQ_MN_MAJOR,
                           ctx_h.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
-                          nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, acc_w, c.epilogue, s); }, s);
+                          nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, acc_w, c.epilogue, b); }, b);
     // dW_d is final for this step: data-parallel callers start its all-reduce
     // on a side stream here, overlapped with the rest of the backward
-    CU_TRY(cudaEventRecord(ev_grad[1], s));
+    CU_TRY(cudaEventRecord(ev_grad[1], b));
     // GLU backward fused with SR(ga), SR(gb)
     FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.as<int16_t>(),
                                   ctx_b.as<int16_t>(), ldF, ctx_a_s.as<float>(),
@@ -284,6 +311,8 @@ struct Mlp {
                                   gq_scales.as<float>(), layer_seed(c.seed, layer(0), 1, step),
                                   layer_seed(c.seed, layer(1), 1, step), row_off, nullptr,
                                   exact_math(), s));
+    CU_TRY(cudaEventRecord(ev_fork[1], s));
+    CU_TRY(cudaStreamWaitEvent(side, ev_fork[1], 0));
     // dX = bqg(ga, W_g) + bqg(gb, W_u)   (the reference adds the two layers' dX)
     const int64_t lds_gq = 2 * gF;
     int8_t* gqc = gq.as<int8_t>();
@@ -307,14 +336,18 @@ struct Mlp {
                                wgu_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr,
                                tok, D, 2 * F, gx, c.act_dtype, D, 0, c.epilogue, s); }, s);
     }
-    // dW_g += bqg(ga^T, ctx_g) ; dW_u += bqg(gb^T, ctx_u)
+    // dW_g += bqg(ga^T, ctx_g) ; dW_u += bqg(gb^T, ctx_u)   (side stream)
     gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_MN_MAJOR, ctx_g.as<int8_t>(), ldD,
                              x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr, F,
-                             D, tok, g_gu.p, FBQ_F32, D, acc_w, c.epilogue, s); }, s);
+                             D, tok, g_gu.p, FBQ_F32, D, acc_w, c.epilogue, b); }, b);
     gemm([&] { return fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_MN_MAJOR, ctx_u.as<int8_t>(),
                              ldD, x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr,
                              nullptr, F, D, tok, g_gu.as<float>() + F * D, FBQ_F32, D, acc_w,
-                             c.epilogue, s); }, s);
+                             c.epilogue, b); }, b);
+    // join: everything after the backward (controller, next step, readers of
+    // dW) is ordered after the side stream's GEMMs
+    CU_TRY(cudaEventRecord(ev_join, side));
+    CU_TRY(cudaStreamWaitEvent(s, ev_join, 0));
     CU_TRY(cudaEventRecord(ev_grad[0], s));
   }
 
