@@ -107,6 +107,9 @@ struct Mlp {
   // independent grid's CTAs instead of idling SMs
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join = nullptr;
+  // forward: the weight quantizations run on the side stream, overlapping the
+  // (issue-bound) X quantizer, the gate/up GEMM's tail and the GLU forward
+  cudaEvent_t ev_ffork = nullptr, ev_wgu = nullptr, ev_wd = nullptr;
 
   Mlp(const fbq_mlp_config& cfg, const float* wg, const float* wu, const float* wd) : c(cfg) {
     D = c.d_model;
@@ -170,7 +173,7 @@ struct Mlp {
     CU_TRY(cudaEventCreateWithFlags(&ev_gy, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_bwd, cudaEventDisableTiming));
-    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_fork[0], &ev_fork[1], &ev_join})
+    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_fork[0], &ev_fork[1], &ev_join, &ev_ffork, &ev_wgu, &ev_wd})
       CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CU_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   }
@@ -184,7 +187,8 @@ struct Mlp {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (side) cudaStreamDestroy(side);
-    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1], ev_fork[0], ev_fork[1], ev_join})
+    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1], ev_fork[0], ev_fork[1], ev_join,
+                          ev_ffork, ev_wgu, ev_wd})
       if (e) cudaEventDestroy(e);
   }
 
@@ -247,10 +251,16 @@ struct Mlp {
     // weights: one RTN quantization serves forward (K-major) and dgrad (MN-major);
     // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97, 121)
     launches += 5;  // 2 x RTN(W), K1(X), GLU forward (+ the 2 GEMMs counted in gemm())
+    // side stream: RTN(W_gate|up) then RTN(W_down), joined right before the
+    // GEMM that consumes each
+    CU_TRY(cudaEventRecord(ev_ffork, s));
+    CU_TRY(cudaStreamWaitEvent(side, ev_ffork, 0));
     FBQ_TRY(fbq_cuda_quantize_rtn(w_gu.p, FBQ_F32, 2 * F, D, D, wgu_codes.as<int8_t>(), ldD,
-                                  wgu_scales.as<float>(), s));
+                                  wgu_scales.as<float>(), side));
+    CU_TRY(cudaEventRecord(ev_wgu, side));
     FBQ_TRY(fbq_cuda_quantize_rtn(w_d.p, FBQ_F32, D, F, F, wd_codes.as<int8_t>(), ldF,
-                                  wd_scales.as<float>(), s));
+                                  wd_scales.as<float>(), side));
+    CU_TRY(cudaEventRecord(ev_wd, side));
     // X: score + threshold mask + fallback codes + gate/up contexts (trainsim.cpp:80-102)
     FBQ_TRY(fbq_cuda_quantize_linear_input(
         x, c.act_dtype, tok, D, D, FBQ_MASK_THRESHOLD, c.threshold_init, th,
@@ -259,6 +269,7 @@ struct Mlp {
         layer_seed(c.seed, layer(0), 0, step), ctx_u.as<int8_t>(),
         layer_seed(c.seed, layer(1), 0, step), row_off, s));
     // [a | b] = fallback_gemm(X, [W_g; W_u]^T)
+    CU_TRY(cudaStreamWaitEvent(s, ev_wgu, 0));
     gemm([&] { return fbq_cuda_gemm(x_codes.as<int8_t>(), ldD, x_scales.as<float>(), FBQ_K_MAJOR,
                           wgu_codes.as<int8_t>(), ldD, wgu_scales.as<float>(), FBQ_K_MAJOR,
                           x_mask.as<uint32_t>(), x_res.as<int8_t>(), x_res_scales.as<float>(),
@@ -271,6 +282,7 @@ struct Mlp {
         h_res.as<int8_t>(), h_res_scales.as<float>(), cnt + 1, ctx_h.as<int8_t>(),
         layer_seed(c.seed, layer(2), 0, step), row_off, nullptr, 0, s));
     // y = fallback_gemm(h, W_d^T)
+    CU_TRY(cudaStreamWaitEvent(s, ev_wd, 0));
     gemm([&] { return fbq_cuda_gemm(h_codes.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_K_MAJOR,
                           wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_K_MAJOR,
                           h_mask.as<uint32_t>(), h_res.as<int8_t>(), h_res_scales.as<float>(),
