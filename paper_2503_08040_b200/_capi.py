@@ -10,6 +10,8 @@ import ctypes as C
 import os
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfbq_b200.so")
+# diagnostics only (A/B of two builds in one session): an explicit alternative build
+_LIB_PATH = os.environ.get("FBQ_B200_LIB_OVERRIDE", _LIB_PATH)
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
