@@ -446,14 +446,20 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   if constexpr (sizeof(T) == 2) {
     // |bf16| orders like its low 15 bits as an unsigned integer: packed 16x2
     // integer max on the raw words, no unpacking (LOP3 + VIMNMX3.U16x2)
-    uint32_t mm = 0;
+    // No masking per word: the SIGNED 16-bit max (from 0) picks the largest
+    // non-negative value, the UNSIGNED max the largest-magnitude negative one
+    // (if any; sign-magnitude orders like the raw bits), so
+    // max|x| = max(smax, umax & 0x7FFF) -- one 3-input VIMNMX3 per two words
+    // per accumulator instead of a LOP3 per word.
+    uint32_t ms = 0, mu = 0;
 #pragma unroll
     for (int ps = 0; ps < NP; ++ps) {
-      mm = __vmaxu2(mm, raw[ps].x & 0x7FFF7FFFu);
-      mm = __vmaxu2(mm, raw[ps].y & 0x7FFF7FFFu);
-      mm = __vmaxu2(mm, raw[ps].z & 0x7FFF7FFFu);
-      mm = __vmaxu2(mm, raw[ps].w & 0x7FFF7FFFu);
+      ms = __vimax3_s16x2(ms, raw[ps].x, raw[ps].y);
+      ms = __vimax3_s16x2(ms, raw[ps].z, raw[ps].w);
+      mu = __vimax3_u16x2(mu, raw[ps].x, raw[ps].y);
+      mu = __vimax3_u16x2(mu, raw[ps].z, raw[ps].w);
     }
+    const uint32_t mm = __vmaxu2(ms, mu & 0x7FFF7FFFu);
     m = __uint_as_float(max(mm >> 16, mm & 0xFFFFu) << 16);
   } else {
 #pragma unroll
