@@ -913,20 +913,41 @@ fbq_glu_backward_kernel(GluBwdParams g) {
     }
     deq(tca, g.ctx_a, sa_row[rb], rb, cb, a);
     deq(tcb, g.ctx_b, sb_row[rb], rb, cb, b);
+    if (g.exact_math) {
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float gy = ga[i];
-      float sg, sl;
-      if (g.exact_math) {
-        sg = silu_grad_ref(a[i]);
-        sl = silu_ref(a[i]);
-      } else {
-        const float sig = sigmoid_fast(a[i]);
-        sg = sig * (1.0f + a[i] * (1.0f - sig));
-        sl = a[i] * sig;
+      for (int i = 0; i < V; ++i) {
+        const float gy = ga[i];
+        const float sg = silu_grad_ref(a[i]), sl = silu_ref(a[i]);
+        ga[i] = __fmul_rn(__fmul_rn(gy, b[i]), sg);
+        gb[i] = __fmul_rn(gy, sl);
       }
-      ga[i] = __fmul_rn(__fmul_rn(gy, b[i]), sg);
-      gb[i] = __fmul_rn(gy, sl);
+    } else {
+      // the fast path on element pairs (FMUL2 / FFMA2; ex2 / rcp stay scalar
+      // MUFU): sig = 1 / (1 + 2^(-a log2 e)), sg = sig (1 + a (1 - sig)),
+      // sl = a sig, ga = fl(fl(gy b) sg), gb = fl(gy sl) -- the same roundings
+      // as the scalar sigmoid_fast / silu_grad_fast sequence
+      const float2 one2 = make_float2(1.0f, 1.0f), neg1 = make_float2(-1.0f, -1.0f);
+      const float2 nl2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const float2 x2 = make_float2(a[i], a[i + 1]);
+        const float2 t = __fmul2_rn(x2, nl2e);
+        float e0, e1, r0, r1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t.y));
+        const float2 d = __fadd2_rn(make_float2(e0, e1), one2);
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+        const float2 sig = make_float2(r0, r1);
+        const float2 om = __ffma2_rn(sig, neg1, one2);   // 1 - sig
+        const float2 sg = __fmul2_rn(sig, __ffma2_rn(x2, om, one2));
+        const float2 sl = __fmul2_rn(x2, sig);
+        const float2 gy = make_float2(ga[i], ga[i + 1]);
+        const float2 g1 = __fmul2_rn(__fmul2_rn(gy, make_float2(b[i], b[i + 1])), sg);
+        const float2 g2 = __fmul2_rn(gy, sl);
+        ga[i] = g1.x; ga[i + 1] = g1.y;
+        gb[i] = g2.x; gb[i + 1] = g2.y;
+      }
     }
   };
   const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
