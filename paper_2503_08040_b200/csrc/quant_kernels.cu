@@ -793,10 +793,27 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
   // h = fl(silu(a) * b) (trainsim.cpp:230), deterministic: the direct variant
   // re-evaluates it in every pass instead of keeping a 64 KiB fp32 tile
   auto hval = [&](const float (&va)[V], const float (&vb)[V], float (&vh)[V]) {
+    if (g.exact_math) {
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float sa = g.exact_math ? silu_ref(va[i]) : silu_fast(va[i]);
-      vh[i] = __fmul_rn(sa, vb[i]);
+      for (int i = 0; i < V; ++i) vh[i] = __fmul_rn(silu_ref(va[i]), vb[i]);
+    } else {
+      // silu_fast on element pairs: the same roundings, FP32 ops packed
+      const float2 one2 = make_float2(1.0f, 1.0f);
+      const float2 nl2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const float2 x2 = make_float2(va[i], va[i + 1]);
+        const float2 t = __fmul2_rn(x2, nl2e);
+        float e0, e1, r0, r1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t.y));
+        const float2 d = __fadd2_rn(make_float2(e0, e1), one2);
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+        const float2 h2 = __fmul2_rn(__fmul2_rn(x2, make_float2(r0, r1)), make_float2(vb[i], vb[i + 1]));
+        vh[i] = h2.x;
+        vh[i + 1] = h2.y;
+      }
     }
   };
   // 10-bit contexts of a and b (trainsim.cpp:240-243), h and its absmax
