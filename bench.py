@@ -288,7 +288,8 @@ def quant_sweep(device, hbm_peak):
 # ----------------------------------------------------------------- C4: Qwen-2.5-7B block linears
 def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
     """BASELINE configs[3] on one GPU: the Qwen-2.5-7B transformer-block linears
-    (q, k, v, o: 3584 -> 3584/512/512/3584 as QuantLinear; gate/up/down
+    (q, k, v, o: 3584 -> 3584/512/512/3584 as QuantLinear, q/k/v on three
+    streams; gate/up/down
     3584 -> 18944 -> 3584 as the fused SwiGLU driver) fwd+bwd with the
     compressed (int8 stochastic) activation contexts, 8192 tokens, bf16
     activations, synthetic inputs with outlier channels; the attention core
@@ -313,14 +314,29 @@ def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
     outs = {H: torch.empty(tokens, H, device=device, dtype=torch.bfloat16),
             KV: torch.empty(tokens, KV, device=device, dtype=torch.bfloat16)}
     gx = torch.empty(tokens, H, device=device, dtype=torch.bfloat16)
+    # q, k and v read the same X and are independent layers (own thresholds,
+    # masks, contexts): they run on three streams so the small k/v GEMMs
+    # (N = 512: 128 tiles, < one wave of 148 SMs) share the machine with q
+    qkv_streams = [torch.cuda.Stream() for _ in range(3)]
+    qkv_out = [torch.empty(tokens, o, device=device, dtype=torch.bfloat16) for o in (H, KV, KV)]
+    qkv_gx = [torch.empty(tokens, H, device=device, dtype=torch.bfloat16) for _ in range(3)]
 
     def step(i):
-        for n, l in enumerate(qkvo):
-            l.zero_grad()
-            o = l.out_features
-            l.forward(attn if n == 3 else x, i, out=outs[o])
-            l.backward(gys[o], i, out=gx)
-            l.controller_step()
+        main = torch.cuda.current_stream()
+        for n, (l, st) in enumerate(zip(qkvo[:3], qkv_streams)):
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                l.zero_grad()
+                l.forward(x, i, out=qkv_out[n])
+                l.backward(gys[l.out_features], i, out=qkv_gx[n])
+                l.controller_step()
+        for st in qkv_streams:
+            main.wait_stream(st)
+        l = qkvo[3]
+        l.zero_grad()
+        l.forward(attn, i, out=outs[H])
+        l.backward(gys[H], i, out=gx)
+        l.controller_step()
         mlp.zero_grad()
         mlp.forward(x, i, 0, out=outs[H])
         mlp.backward(gys[H], i, 0, out=gx)
