@@ -135,6 +135,9 @@ int fbq_linear_forward_device(void* linear, const void* x, int64_t tokens, int64
 int fbq_linear_backward_device(void* linear, const void* gy, int64_t tokens, int64_t row_offset,
                                int step, void* gx, fbq_stream_t stream);
 int fbq_linear_controller_step(void* linear, fbq_stream_t stream);
+/* zero_grad is deferred like fbq_mlp_zero_grad: the next backward's dW GEMM
+ * writes instead of accumulating; fbq_linear_grad_ptr materialises a pending
+ * zero before returning the pointer. */
 int fbq_linear_zero_grad(void* linear, fbq_stream_t stream);
 float* fbq_linear_grad_ptr(void* linear);
 /* last observed fallback rate and the current threshold (synchronous read) */

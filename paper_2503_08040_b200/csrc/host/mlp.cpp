@@ -595,11 +595,15 @@ struct QuantLinear {
     FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldOut, gy_scales.as<float>(), FBQ_K_MAJOR,
                           w_codes.as<int8_t>(), ldIn, w_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
                           nullptr, nullptr, tok, In, Out, gx, c.act_dtype, In, 0, c.epilogue, s));
-    // grad_w += bqg(q(dY)^T, ctx) (trainsim.cpp:124-125)
+    // grad_w += bqg(q(dY)^T, ctx) (trainsim.cpp:124-125); after a (deferred)
+    // zero_grad the GEMM writes instead of reduce-adding into zeros
+    const int acc_w = grad_zero_pending ? 0 : 1;
+    grad_zero_pending = false;
     FBQ_TRY(fbq_cuda_gemm(gy_codes.as<int8_t>(), ldOut, gy_scales.as<float>(), FBQ_MN_MAJOR,
                           ctx.as<int8_t>(), ldIn, x_scales.as<float>(), FBQ_MN_MAJOR, nullptr,
-                          nullptr, nullptr, Out, In, tok, g.p, FBQ_F32, In, 1, c.epilogue, s));
+                          nullptr, nullptr, Out, In, tok, g.p, FBQ_F32, In, acc_w, c.epilogue, s));
   }
+  bool grad_zero_pending = false;
 
   void controller(cudaStream_t s) {
     if (c.fallback_mode != 0) return;  // trainsim.cpp:129-133: Threshold mode only
@@ -844,12 +848,21 @@ int fbq_linear_controller_step(void* l, fbq_stream_t stream) {
 }
 int fbq_linear_zero_grad(void* l, fbq_stream_t stream) {
   if (!l) return FBQ_ERR_ARG;
-  return guarded([&] {
-    auto* q = static_cast<QuantLinear*>(l);
-    CU_TRY(cudaMemsetAsync(q->g.p, 0, q->Out * q->In * 4, reinterpret_cast<cudaStream_t>(stream)));
-  });
+  (void)stream;
+  static_cast<QuantLinear*>(l)->grad_zero_pending = true;  // deferred (see backward)
+  return FBQ_OK;
 }
-float* fbq_linear_grad_ptr(void* l) { return l ? static_cast<QuantLinear*>(l)->g.as<float>() : nullptr; }
+float* fbq_linear_grad_ptr(void* l) {
+  if (!l) return nullptr;
+  auto* q = static_cast<QuantLinear*>(l);
+  if (q->grad_zero_pending) {  // materialise the pending zero for a reader
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemset(q->g.p, 0, q->Out * q->In * 4) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      return nullptr;
+    q->grad_zero_pending = false;
+  }
+  return q->g.as<float>();
+}
 int fbq_linear_get_controller(void* l, double* last_rate, double* threshold) {
   if (!l || !last_rate || !threshold) return FBQ_ERR_ARG;
   return guarded([&] {
