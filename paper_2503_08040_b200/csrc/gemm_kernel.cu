@@ -613,7 +613,20 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         mbar_arrive(sfull + (pc & 1));
       }
       int next = 0;
-      if (lane == 0) next = p.tile_ctr ? atomicAdd(p.tile_ctr, 1) + (int)gridDim.x : tile + (int)gridDim.x;
+      if (lane == 0) {
+        if (p.tile_ctr) {
+          next = atomicAdd(p.tile_ctr, 1) + (int)gridDim.x;
+          // Each CTA's last claim is the one past the end; once all gridDim.x
+          // of those are in, nobody reads the counter again: the last CTA
+          // resets it (and the arrival count) for the slot's next launch.
+          if (next >= p.num_tiles && atomicAdd(p.tile_ctr + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(p.tile_ctr, 0);
+            atomicExch(p.tile_ctr + 1, 0);
+          }
+        } else {
+          next = tile + (int)gridDim.x;
+        }
+      }
       tile = __shfl_sync(0xffffffffu, next, 0);
     }
   } else if (warp >= 4) {
@@ -728,7 +741,9 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
       p.tma_store = p.accumulate ? 2 : ((p.diag & 16384) ? 3 : 1);
   }
   p.num_tiles = p.MB * ((p.NB + 1) / 2);
-  // dynamic tile counter: a slot of a per-device ring, zeroed in-stream
+  // dynamic tile counter: a slot of a per-device ring (zeroed once at
+  // allocation; every launch leaves its slot at zero again -- the last CTA to
+  // make its final claim resets it), so no memset node per launch
   p.tile_ctr = nullptr;
   if (!(p.diag & (1 << 21)) && !(p.diag & 512)) {  // diagnostics: 1 << 21 = static schedule
     static int* ring[64] = {};
@@ -737,11 +752,16 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64) {
       constexpr int kSlots = 256;
-      if (!ring[dev] && cudaMalloc(&ring[dev], kSlots * 128) != cudaSuccess) ring[dev] = nullptr;
-      if (ring[dev]) {
-        int* ctr = ring[dev] + (next_slot[dev]++ % kSlots) * 32;  // one 128-byte line per slot
-        if (cudaMemsetAsync(ctr, 0, sizeof(int), s) == cudaSuccess) p.tile_ctr = ctr;
+      if (!ring[dev]) {
+        int* r = nullptr;
+        if (cudaMalloc(&r, kSlots * 128) == cudaSuccess) {
+          if (cudaMemset(r, 0, kSlots * 128) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess)
+            ring[dev] = r;
+          else
+            cudaFree(r);
+        }
       }
+      if (ring[dev]) p.tile_ctr = ring[dev] + (next_slot[dev]++ % kSlots) * 32;  // one 128 B line per slot
     }
   }
   {
