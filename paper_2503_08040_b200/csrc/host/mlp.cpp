@@ -173,7 +173,8 @@ struct Mlp {
     CU_TRY(cudaEventCreateWithFlags(&ev_gy, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_bwd, cudaEventDisableTiming));
-    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_fork[0], &ev_fork[1], &ev_join, &ev_ffork, &ev_wgu, &ev_wd})
+    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_fork[0], &ev_fork[1], &ev_join, &ev_ffork, &ev_wgu, &ev_wd,
+                           &ev_gyq})
       CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CU_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   }
@@ -188,7 +189,7 @@ struct Mlp {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (side) cudaStreamDestroy(side);
     for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1], ev_fork[0], ev_fork[1], ev_join,
-                          ev_ffork, ev_wgu, ev_wd})
+                          ev_ffork, ev_wgu, ev_wd, ev_gyq})
       if (e) cudaEventDestroy(e);
   }
 
@@ -290,17 +291,32 @@ struct Mlp {
     (void)gTt;
   }
 
+  // SR(dY) for the down layer (trainsim.cpp:117-119).  The host-buffer step
+  // APIs have dY before the forward runs, so they quantize it on the side
+  // stream right after the forward's weight quantizations (it then overlaps
+  // the forward) and the backward only waits for it (gy_ready).
+  cudaEvent_t ev_gyq = nullptr;
+  void quantize_gy(const void* gy, int64_t tok, int64_t row_off, int step, cudaStream_t s) {
+    FBQ_TRY(fbq_cuda_quantize_stochastic(gy, c.act_dtype, tok, D, D,
+                                         layer_seed(c.seed, layer(2), 1, step), row_off,
+                                         gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), s));
+  }
+  void quantize_gy_early(const void* gy, int64_t tok, int64_t row_off, int step) {
+    if (tok <= 0) return;
+    quantize_gy(gy, tok, row_off, step, side);
+    CU_TRY(cudaEventRecord(ev_gyq, side));
+  }
+
   void backward(const void* gy, int64_t tok, int64_t row_off, int step, void* gx,
-                cudaStream_t s) {
+                cudaStream_t s, bool gy_ready = false) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
     if (tok == 0) return;
     launches += 2;  // K2(dY), GLU backward (+ 6 GEMMs counted in gemm())
     const int acc_w = grad_zero_pending ? 0 : 1;  // dW: write (deferred zero_grad) or accumulate
     grad_zero_pending = false;
     // down: SR(dY) (trainsim.cpp:117-119)
-    FBQ_TRY(fbq_cuda_quantize_stochastic(gy, c.act_dtype, tok, D, D,
-                                         layer_seed(c.seed, layer(2), 1, step), row_off,
-                                         gy_codes.as<int8_t>(), ldD, gy_scales.as<float>(), s));
+    if (gy_ready) CU_TRY(cudaStreamWaitEvent(s, ev_gyq, 0));
+    else quantize_gy(gy, tok, row_off, step, s);
     CU_TRY(cudaEventRecord(ev_fork[0], s));
     CU_TRY(cudaStreamWaitEvent(side, ev_fork[0], 0));
     // dH = bqg(dY, W_d): B = W_d codes (D x F) read MN-major (trainsim.cpp:121-122)
@@ -394,11 +410,14 @@ struct Mlp {
     c.act_dtype = FBQ_F32;  // the host API is fp32 like the reference
     try {
       forward(hx.p, tok, 0, step, hy.p, s);
+      // SR(dY) on the side stream once dY has landed, overlapping the forward
+      CU_TRY(cudaStreamWaitEvent(side, ev_gy, 0));
+      quantize_gy_early(hgy.p, tok, 0, step);
       CU_TRY(cudaEventRecord(ev_fwd, s));
       CU_TRY(cudaStreamWaitEvent(copy_stream, ev_fwd, 0));
       CU_TRY(cudaMemcpyAsync(y, hy.p, bytes, cudaMemcpyDeviceToHost, copy_stream));
       CU_TRY(cudaStreamWaitEvent(s, ev_gy, 0));
-      backward(hgy.p, tok, 0, step, hgx.p, s);
+      backward(hgy.p, tok, 0, step, hgx.p, s, /*gy_ready=*/true);
       CU_TRY(cudaMemcpyAsync(gx, hgx.p, bytes, cudaMemcpyDeviceToHost, s));
     } catch (...) {
       c.act_dtype = saved;
@@ -476,8 +495,11 @@ struct Mlp {
     try {
       if (flags & FBQ_STEP_ZERO_GRAD) zero_grad(a_cs);
       forward(ax[slot].p, tok, 0, step, ay[slot].p, a_cs);
+      // SR(dY) on the side stream (ordered after this slot's H2D through the
+      // forward's fork), overlapping the forward
+      quantize_gy_early(agy[slot].p, tok, 0, step);
       CU_TRY(cudaEventRecord(a_fwd[slot], a_cs));
-      backward(agy[slot].p, tok, 0, step, agx[slot].p, a_cs);
+      backward(agy[slot].p, tok, 0, step, agx[slot].p, a_cs, /*gy_ready=*/true);
       if (flags & FBQ_STEP_CONTROLLER) controller(a_cs);
       CU_TRY(cudaEventRecord(a_done[slot], a_cs));
     } catch (...) {
