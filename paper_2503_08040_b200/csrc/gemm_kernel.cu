@@ -456,7 +456,13 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         tma_prefetch(&map_b);
         if (has_res) tma_prefetch(&map_r);
       }
-      const uint64_t pol = l2_policy_evict_last();
+      // L2 policy per operand: with a resident-operand raster the streamed
+      // operand is read by the ~148 concurrent tiles within a short window and
+      // then dead, so it is marked evict-first (diag 1 << 23: all evict-last)
+      const uint64_t pol_keep = l2_policy_evict_last();
+      const bool split_pol = !(p.diag & (1 << 23));
+      const uint64_t pol_a = (split_pol && p.n_fastest) ? l2_policy_evict_first() : pol_keep;
+      const uint64_t pol_b = (split_pol && p.group_m == p.MB && p.group_m > 8) ? l2_policy_evict_first() : pol_keep;
       int stage = 0;
       uint32_t phase = 0, pc = 0;
       for (;;) {
@@ -483,17 +489,17 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
                 const int k0 = bk * kBK, m0 = bm * kBM, n0 = bn2 * kBN;
                 if (p.a_major == 0) {
-                  tma_load_2d(sa, &map_a, full + stage, k0, m0, pol);
-                  if (masked) tma_load_2d(sr, &map_r, full + stage, k0, m0, pol);
+                  tma_load_2d(sa, &map_a, full + stage, k0, m0, pol_a);
+                  if (masked) tma_load_2d(sr, &map_r, full + stage, k0, m0, pol_a);
                 } else {
-                  tma_load_2d(sa, &map_a, full + stage, m0, k0, pol);
-                  if (masked) tma_load_2d(sr, &map_r, full + stage, m0, k0, pol);
+                  tma_load_2d(sa, &map_a, full + stage, m0, k0, pol_a);
+                  if (masked) tma_load_2d(sr, &map_r, full + stage, m0, k0, pol_a);
                 }
                 if (p.b_major == 0) {
-                  tma_load_2d(sb, &map_b, full + stage, k0, n0, pol);
+                  tma_load_2d(sb, &map_b, full + stage, k0, n0, pol_b);
                 } else {
-                  tma_load_2d(sb, &map_b, full + stage, n0, k0, pol);
-                  tma_load_2d(sb + kTileA, &map_b, full + stage, n0 + 128, k0, pol);
+                  tma_load_2d(sb, &map_b, full + stage, n0, k0, pol_b);
+                  tma_load_2d(sb + kTileA, &map_b, full + stage, n0 + 128, k0, pol_b);
                 }
               }
             }

@@ -1,4 +1,4 @@
-"""Same-process A/B of quantizer-kernel variants inside the C3 MLP step
+"""Same-process A/B of kernel variants inside the C3 MLP step (K1 diag flags, or GEMM diag flags with AB_GEMM=1)
 (Llama-3.1-8B SwiGLU, 8192 tokens, bf16, bench thresholds): K1 diag flags from
 the command line, interleaved; outputs must be bit-identical across flags."""
 import sys, os
@@ -8,6 +8,8 @@ import bench
 from paper_2503_08040_b200 import fbq, linear
 lib = fbq.K.lib
 lib.fbq_debug_set_quant_diag.argtypes = [fbq.K.cint]
+lib.fbq_debug_set_gemm_diag.argtypes = [fbq.K.cint]
+SET = lib.fbq_debug_set_gemm_diag if os.environ.get("AB_GEMM") else lib.fbq_debug_set_quant_diag
 diags = [int(a) for a in sys.argv[1:]] or [0, 32]
 T = 8192
 wg, wu, wd = bench.make_weights()
@@ -33,7 +35,7 @@ def step(i):
 res, outs = {d: [] for d in diags}, {}
 for rnd in range(3):
     for d in diags:
-        lib.fbq_debug_set_quant_diag(d)
+        SET(d)
         mlp.set_thresholds(th_gu, th_d)
         for i in range(2):
             step(i)
@@ -49,7 +51,7 @@ for rnd in range(3):
         step(0)
         torch.cuda.synchronize()
         outs[d] = (y.clone(), gx.clone(), [g.clone() for g in mlp.grad_tensors()])
-lib.fbq_debug_set_quant_diag(0)
+SET(0)
 for d in diags:
     print(f"diag={d:3d}: ms/step {' '.join(f'{v:.3f}' for v in res[d])}  best {T/min(res[d])*1e3/1e6:.4f}M tokens/s")
 ref = outs[diags[0]]
