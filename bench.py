@@ -179,6 +179,16 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- reference arm
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference(tokens, steps, warmup):
     """The reference's own CPU path (oracle/_ref: QuantLinearLayer x3 + GluCombine,
     block 128, set_gemm_threads(nproc)) on a bounded token sample."""
@@ -202,6 +212,7 @@ def cpu_reference(tokens, steps, warmup):
         m.step(x, gy, warmup + i)
     dt = (time.perf_counter() - t0) / max(steps, 1)
     return {"value": tokens / dt, "unit": "tokens/s", "cores": cores, "kind": "reference",
+            "cpu_model": cpu_model(),
             "sample": f"{tokens} tokens x d_model {D_MODEL} x d_ff {D_FF} per step (of {TOKENS}); "
                       f"{steps} timed step(s); reference fbq_core (oracle/_ref, AVX2, "
                       f"set_gemm_threads({cores})); quantizers single-threaded as shipped",
@@ -235,7 +246,7 @@ def cpu_reference_c1(rate=0.10):
     ref.block_gemm(c, sc, wc, ws, mask=mask, res_codes=rc, res_scales=rs)
     t_g = time.perf_counter() - t0
     return {"workload": f"C1 fallback linear forward 4096^3, {rate:.0%} fallback blocks (topk)",
-            "cores": cores, "kind": "reference", "fallback_gemm_s": round(t_g, 3),
+            "cores": cores, "cpu_model": cpu_model(), "kind": "reference", "fallback_gemm_s": round(t_g, 3),
             "fallback_gemm_GOPS": round(2 * n ** 3 / t_g / 1e9, 1),
             "score+mask+fallback_quantize_s": round(t_q, 3)}
 
@@ -253,7 +264,7 @@ def run_reference_arm(args, rank, world):
         "data": "synthetic", "impl": "reference",
         "config": {"workload": WORKLOAD + " -- CPU reference sample", "tokens": REF_SAMPLE_TOKENS,
                    "d_model": D_MODEL, "d_ff": D_FF, "block": 128},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")},
         "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -624,7 +635,7 @@ def run_ours(args, rank, world, local):
         if not args.no_cpu_baseline and world == 1:
             try:
                 cb = cpu_reference(REF_SAMPLE_TOKENS, 1, 0)
-                cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
             except Exception as ex:
                 cpu = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
