@@ -394,7 +394,7 @@ def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
     t = e0.elapsed_time(e1) / steps * 1e-3
     ops = 2 * tokens * (2 * H * H + 2 * H * KV + 3 * H * F) * 3
     rates = {f"{n}": round(l.controller_state()[0], 4) for n, l in zip("qkvo", qkvo)}
-    return {"workload": "Qwen-2.5-7B block linears q/k/v/o + SwiGLU MLP, fwd+bwd, 8192 tokens, 1 GPU",
+    return {"workload": f"Qwen-2.5-7B block linears q/k/v/o + SwiGLU MLP, fwd+bwd, {tokens} tokens, 1 GPU",
             "tokens_per_s": round(tokens / t, 1), "ms_per_step": round(t * 1e3, 3),
             "gemm_TOPS_effective": round(ops / t / 1e12, 1), "fallback_rates_qkvo": rates}
 
@@ -623,6 +623,10 @@ def run_ours(args, rank, world, local):
                 sweep = {"error": str(ex)[:200]}
             try:
                 c4 = qwen_block_linears(device)
+                # the strong-scaling base of SURVEY 8d (T = 32768 on one GPU)
+                c4_32k = qwen_block_linears(device, tokens=32768, steps=3, warmup=1)
+                c4["tokens_32768"] = {k: c4_32k[k] for k in ("tokens_per_s", "ms_per_step",
+                                                            "gemm_TOPS_effective")}
             except Exception as ex:  # pragma: no cover
                 c4 = {"error": str(ex)[:200]}
 
