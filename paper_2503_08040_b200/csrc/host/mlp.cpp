@@ -468,10 +468,14 @@ struct Mlp {
   // memset per step.  Readers of the gradient buffers flush it first.
   bool grad_zero_pending = false;
   void zero_grad(cudaStream_t) { grad_zero_pending = true; }
-  void flush_grad_zero(cudaStream_t s) {
+  // (device-wide: an earlier backward may still be writing dW on a
+  // non-blocking stream, so wait for it before clearing)
+  void flush_grad_zero() {
     if (!grad_zero_pending) return;
-    CU_TRY(cudaMemsetAsync(g_gu.p, 0, 2 * F * D * 4, s));
-    CU_TRY(cudaMemsetAsync(g_d.p, 0, D * F * 4, s));
+    CU_TRY(cudaDeviceSynchronize());
+    CU_TRY(cudaMemset(g_gu.p, 0, 2 * F * D * 4));
+    CU_TRY(cudaMemset(g_d.p, 0, D * F * 4));
+    CU_TRY(cudaDeviceSynchronize());
     grad_zero_pending = false;
   }
 
@@ -777,7 +781,7 @@ void* fbq_mlp_grad_ptr(void* m, int which) {
   if (!m) return nullptr;
   auto* mlp = static_cast<Mlp*>(m);
   try {
-    mlp->flush_grad_zero(nullptr);
+    mlp->flush_grad_zero();
     if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
   } catch (...) {
     return nullptr;
@@ -792,7 +796,7 @@ int fbq_mlp_get_grads(void* m, float* g_gate, float* g_up, float* g_down) {
   if (!m) return FBQ_ERR_ARG;
   return guarded([&] {
     auto* mlp = static_cast<Mlp*>(m);
-    mlp->flush_grad_zero(nullptr);
+    mlp->flush_grad_zero();
     CU_TRY(cudaDeviceSynchronize());
     const size_t n = mlp->F * mlp->D * 4;
     if (g_gate) CU_TRY(cudaMemcpy(g_gate, mlp->g_gu.p, n, cudaMemcpyDeviceToHost));
