@@ -172,11 +172,16 @@ __device__ __forceinline__ void rtn_fix_vec(const float (&x)[V], float a, uint32
     const float2 n = __fadd2_rn(make_float2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), nmag);
     const float2 r = __ffma2_rn(n, na, make_float2(x[i], x[i + 1]));  // exact
     const float2 r2 = __fadd2_rn(r, r);                                // exact
-    const float t0 = fabsf(r2.x), t1 = fabsf(r2.y);
-    const bool s0 = (t0 > a) | ((t0 == a) & ((w[i] & 1u) != 0));
-    const bool s1 = (t1 > a) | ((t1 == a) & ((w[i + 1] & 1u) != 0));
-    w[i] += s0 ? (r2.x > 0.0f ? 1u : 0xFFFFFFFFu) : 0u;
-    w[i + 1] += s1 ? (r2.y > 0.0f ? 1u : 0xFFFFFFFFu) : 0u;
+    // step toward r iff 2|r| > a, or 2|r| == a with n odd: t = 2|r| - a is
+    // exact (Sterbenz; |2r| <= a (1 + 2^-15)) or, when 2|r| < a/2, still
+    // negative with |t| >= 2^-144 (a >= kTinyScale); adding the denormal
+    // 2^-149 * (n & 1) turns the tie into "> 0" exactly when n is odd.
+    const float t0 = __fadd_rn(__fadd_rn(fabsf(r2.x), -a), __uint_as_float(w[i] & 1u));
+    const float t1 = __fadd_rn(__fadd_rn(fabsf(r2.y), -a), __uint_as_float(w[i + 1] & 1u));
+    const uint32_t sg0 = (__float_as_uint(r2.x) >> 31) ? 0xFFFFFFFFu : 1u;  // sign(r) as +-1
+    const uint32_t sg1 = (__float_as_uint(r2.y) >> 31) ? 0xFFFFFFFFu : 1u;
+    w[i] += t0 > 0.0f ? sg0 : 0u;
+    w[i + 1] += t1 > 0.0f ? sg1 : 0u;
   }
 }
 template <int V>
