@@ -110,48 +110,50 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run_nvml(self):
-        """In-process NVML sampling every 10 ms (an nvidia-smi call takes
-        ~0.1-0.5 s, i.e. one or two samples over a ~130 ms timed region).
-        Rows mirror the nvidia-smi fields."""
-        import pynvml
-        pynvml.nvmlInit()
+    def _nvml_open(self):
+        """NVML handle, opened BEFORE the sampling thread starts (the first
+        nvmlInit on a fresh box can take longer than the whole timed region)."""
         try:
+            import pynvml
+            pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            flags = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                     pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                try:
-                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except Exception:
-                    r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
-                self.rows.append([str(sm), str(mx), f"{pw:.1f}", hex(r)] +
-                                 ["Active" if r & f else "Not Active" for f in flags])
-                self._stop.wait(0.01)
-        finally:
-            pynvml.nvmlShutdown()
+            return pynvml, h, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return None
+
+    def _sample_nvml(self):
+        pynvml, h, mx = self._nvml
+        flags = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                 pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+        self.rows.append([str(sm), str(mx), f"{pw:.1f}", hex(r)] +
+                         ["Active" if r & f else "Not Active" for f in flags])
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        if out:
+            self.rows.append([v.strip() for v in out.split(",")])
 
     def _run(self):
-        try:
-            self._run_nvml()
-            return
-        except Exception:
-            pass  # no NVML: nvidia-smi subprocess sampling
+        # in-process NVML every 10 ms (an nvidia-smi call takes ~0.1-0.5 s,
+        # i.e. one or two samples over a ~130 ms timed region); rows mirror
+        # the nvidia-smi fields
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.01 if self._nvml else 0.1)
 
     def __enter__(self):
+        self._nvml = self._nvml_open()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -160,6 +162,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if not self.rows:  # always report at least the state right after the timed region
+            try:
+                self._sample_nvml() if self._nvml else self._sample_smi()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
