@@ -33,7 +33,8 @@ sys.path.insert(0, ROOT)
 D_MODEL, D_FF, TOKENS = 4096, 14336, 8192
 METRIC = "GLU-MLP fwd+bwd tokens/sec"
 WORKLOAD = "Llama-3.1-8B SwiGLU MLP 4096->14336->4096 fwd+bwd, fallback-quantized (config 3)"
-REF_SAMPLE_TOKENS = 256  # bounded CPU sample (tokens per reference step)
+REF_SAMPLE_TOKENS = 1024  # bounded CPU sample (tokens per reference step; the reference's
+# fixed per-step weight quantization is amortised over >= 1024 tokens)
 
 
 def parse():
@@ -68,7 +69,10 @@ def make_weights(seed=2):
 
 def make_activations(tokens, cols, seed, device, dtype, row_offset=0):
     """N(0,1) body + outlier channels (~123.5), token outliers (~605.8), rare
-    occasional outliers (~150.9) -- PAPER.md Table 1, Llama-3.1-8B row."""
+    occasional outliers (~150.9) -- PAPER.md Table 1, Llama-3.1-8B row.  The
+    outlier magnitudes drift smoothly by +-15 % across tokens and channels
+    (real outlier channels are not constant), which keeps block AbsMax scores
+    distinct so a threshold realises a requested fallback rate."""
     import torch
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -83,6 +87,10 @@ def make_activations(tokens, cols, seed, device, dtype, row_offset=0):
     r = torch.randint(0, tokens, (n_occ,), device=device, generator=g)
     c = torch.randint(0, cols, (n_occ,), device=device, generator=g)
     x[r, c] = 150.9
+    rr = torch.arange(row_offset, row_offset + tokens, device=device, dtype=torch.float32)[:, None]
+    cc = torch.arange(cols, device=device, dtype=torch.float32)[None, :]
+    big = x.abs() > 50
+    x = torch.where(big, x * (1.0 + 0.15 * torch.sin(rr * 0.0015 + cc * 0.0007)), x)
     return x.to(dtype)
 
 
@@ -199,7 +207,7 @@ def cpu_model() -> str:
 def cpu_reference(tokens, steps, warmup):
     """The reference's own CPU path (oracle/_ref: QuantLinearLayer x3 + GluCombine,
     block 128, set_gemm_threads(nproc)) on a bounded token sample."""
-    import numpy as np
+    import torch
     from oracle.oracle import REF_oracle, RefMlp
     ref = REF_oracle()
     if ref is None:
@@ -208,10 +216,9 @@ def cpu_reference(tokens, steps, warmup):
     ref.set_gemm_threads(cores)
     wg, wu, wd = make_weights()
     m = RefMlp(wg, wu, wd, threshold=8.0)
-    rng = np.random.default_rng(7)
-    x = rng.standard_normal((tokens, D_MODEL), dtype=np.float32)
-    x[:, :: 512] = 123.5
-    gy = (rng.standard_normal((tokens, D_MODEL), dtype=np.float32) * 1e-3)
+    # the GPU arm's synthetic recipe (same generator, CPU device) on a token sample
+    x = make_activations(tokens, D_MODEL, 1000, "cpu", torch.float32).numpy()
+    gy = make_grads(tokens, D_MODEL, 2000, "cpu", torch.float32).numpy()
     for i in range(warmup):
         m.step(x, gy, i)
     t0 = time.perf_counter()
@@ -220,9 +227,11 @@ def cpu_reference(tokens, steps, warmup):
     dt = (time.perf_counter() - t0) / max(steps, 1)
     return {"value": tokens / dt, "unit": "tokens/s", "cores": cores, "kind": "reference",
             "cpu_model": cpu_model(),
-            "sample": f"{tokens} tokens x d_model {D_MODEL} x d_ff {D_FF} per step (of {TOKENS}); "
-                      f"{steps} timed step(s); reference fbq_core (oracle/_ref, AVX2, "
-                      f"set_gemm_threads({cores})); quantizers single-threaded as shipped",
+            "sample": f"{tokens} tokens x d_model {D_MODEL} x d_ff {D_FF} per step (of {TOKENS}; the "
+                      f"GPU arm's synthetic recipe); {steps} timed step(s); reference fbq_core "
+                      f"(oracle/_ref, AVX2, set_gemm_threads({cores})); quantizers single-threaded "
+                      f"as shipped; tokens/s is per-token comparable (>= 1024 tokens amortise the "
+                      f"per-step weight quantization)",
             "s_per_step": dt}
 
 
@@ -261,7 +270,7 @@ def cpu_reference_c1(rate=0.10):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return  # rank 0 alone runs and prints the CPU reference
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 2))
     warm = 1 if args.warmup > 0 else 0
     cb = cpu_reference(REF_SAMPLE_TOKENS, steps, warm)
     line = {
@@ -302,10 +311,11 @@ def quant_sweep(device, hbm_peak):
         count = torch.zeros(1, dtype=torch.int32, device=device)
         for dt in (torch.bfloat16, torch.float32):
             x = make_activations(R, C, 5, device, dt)
-            sc = fbq.score_blocks(x).flatten().sort(descending=True).values
+            sc = fbq.score_blocks(x).cpu().numpy()
             for rate in (0.0, 0.05, 0.20):
-                k = int(round(rate * nb))
-                theta = float(sc[k].item()) if rate > 0 else float(sc[0].item()) * 2.0
+                # theta just below the ceil(rate*n)-th score (strict >, policy.cpp:77):
+                # the realised rate is reported as "flagged"
+                theta, _ = fbq.theta_for_rate(sc, rate)
 
                 def run():
                     K.call("fbq_cuda_quantize_fallback", x.data_ptr(), K.FBQ_BF16 if dt == torch.bfloat16 else K.FBQ_F32,
@@ -476,6 +486,103 @@ def gemm_sweep(device):
             "c5_m_sweep_28672x8192_rate_0.05": msweep}
 
 
+# ----------------------------------------------------------------- C3 comparators
+def _event_time(fn, steps, warmup):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def bf16_mlp_comparator(device, T=TOKENS, steps=10, warmup=3):
+    """SURVEY 8d's comparator for C3: the same SwiGLU MLP fwd+bwd, unquantized,
+    with cuBLAS bf16 GEMMs (fp32 accumulation; bf16 outputs, dW included) and
+    torch elementwise SiLU-GLU, same shapes and synthetic data -- the paper's
+    BF16 baseline.  Also the six GEMMs alone."""
+    import torch
+    import torch.nn.functional as Fn
+    wg, wu, wd = make_weights()
+    wgu = torch.cat([torch.from_numpy(wg), torch.from_numpy(wu)]).to(device, torch.bfloat16)
+    wdd = torch.from_numpy(wd).to(device, torch.bfloat16)
+    x = make_activations(T, D_MODEL, 1000, device, torch.bfloat16)
+    gy = make_grads(T, D_MODEL, 2000, device, torch.bfloat16)
+    F = D_FF
+
+    def step():
+        ab = x @ wgu.t()
+        a, b = ab[:, :F], ab[:, F:]
+        sa = Fn.silu(a)
+        h = sa * b
+        y = h @ wdd.t()
+        dh = gy @ wdd
+        g_d = gy.t() @ h
+        sg = torch.sigmoid(a)
+        ga = dh * b * (sg * (1 + a * (1 - sg)))
+        gb = dh * sa
+        dgu = torch.cat([ga, gb], dim=1)
+        dx = dgu @ wgu
+        g_gu = dgu.t() @ x
+        return y, dx, g_d, g_gu
+
+    ms = _event_time(step, steps, warmup)
+    ab = x @ wgu.t()
+    h = ab[:, :F].contiguous()
+    dgu = ab.contiguous()
+
+    def gemms():
+        x @ wgu.t()
+        h @ wdd.t()
+        gy @ wdd
+        gy.t() @ h
+        dgu @ wgu
+        dgu.t() @ x
+
+    ms_g = _event_time(gemms, steps, warmup)
+    flops = 18 * T * D_MODEL * F
+    out = {"workload": "C3 MLP fwd+bwd, cuBLAS bf16 (unquantized), same shapes and data",
+           "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms, "gemm_only_ms": ms_g,
+           "gemm_TFLOPS": flops / (ms_g * 1e-3) / 1e12}
+    del wgu, wdd, x, gy, ab, h, dgu
+    torch.cuda.empty_cache()
+    return out
+
+
+def exact_mode_rate(device, T=TOKENS, steps=5, warmup=2):
+    """C3 in the bit-exact configuration (fp32 activations and intermediates,
+    EXACT epilogue: fl(acc + fl(s * P)) as gemm.cpp:163-175, reference-exact
+    SiLU) -- the mode the parity tests hold bit-for-bit against the reference."""
+    import torch
+    from paper_2503_08040_b200 import linear
+    wg, wu, wd = make_weights()
+    m = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.float32, exact=True,
+                      threshold_init=8.0)
+    x = make_activations(T, D_MODEL, 1000, device, torch.float32)
+    gy = make_grads(T, D_MODEL, 2000, device, torch.float32)
+    y, gx = torch.empty_like(x), torch.empty_like(x)
+    i = [0]
+
+    def step():
+        m.zero_grad()
+        m.forward(x, i[0], out=y)
+        m.backward(gy, i[0], out=gx)
+        m.controller_step()
+        i[0] += 1
+
+    ms = _event_time(step, steps, warmup)
+    del m, x, gy, y, gx
+    torch.cuda.empty_cache()
+    return {"workload": "C3 MLP fwd+bwd, bit-exact mode (fp32 activations/intermediates, exact "
+                        "epilogue, reference-exact SiLU)", "tokens_per_s": T / (ms * 1e-3),
+            "ms_per_step": ms}
+
+
 # ----------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     import numpy as np
@@ -483,7 +590,8 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     from paper_2503_08040_b200 import fbq, linear
-    from paper_2503_08040_b200.dist import allreduce_mlp_grads_overlapped, max_over_ranks
+    from paper_2503_08040_b200.dist import (allreduce_mlp_grads_overlapped, controller_step_global,
+                                            global_quantile, max_over_ranks)
 
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -503,14 +611,15 @@ def run_ours(args, rank, world, local):
     # Thresholds: start the delay-threshold controller inside its target band
     # (the reference starts at 1.0 and walks there by x1.3 per step): the
     # 85th percentile of the block AbsMax scores of X and of a bf16 estimate of h.
+    # (pooled over ranks: every rank starts from the same thresholds)
     sc = fbq.score_blocks(x).flatten()
-    th_gu = float(torch.quantile(sc, 0.85))
+    th_gu = global_quantile(sc, 0.85)
     with torch.no_grad():
         xs = x[:1024].float()
         a = xs @ torch.from_numpy(wg).to(device).t()
         b = xs @ torch.from_numpy(wu).to(device).t()
         h = torch.nn.functional.silu(a) * b
-        th_d = float(torch.quantile(fbq.score_blocks(h).flatten(), 0.85))
+        th_d = global_quantile(fbq.score_blocks(h).flatten(), 0.85)
         del xs, a, b, h
     mlp.set_thresholds(th_gu, th_d)
     gu_grad, d_grad = mlp.grad_tensors()
@@ -526,7 +635,9 @@ def run_ours(args, rank, world, local):
         if world > 1:
             # dW_down's all-reduce overlaps the GLU backward + gate/up GEMMs
             allreduce_mlp_grads_overlapped(mlp, gu_grad, d_grad, comm)
-        mlp.controller_step()
+        # the controller sees the fallback rate of the whole batch (masked
+        # counts summed over ranks; trainsim.cpp:93,129-133)
+        controller_step_global(mlp, world * T)
 
     clk = ClockSampler(local)
     clk.__enter__()  # sample from the first warm-up step through the timed region
@@ -563,13 +674,33 @@ def run_ours(args, rank, world, local):
     gemm_ops_per_step = 18 * T * D_MODEL * D_FF  # 6 GEMM-equivalents x 2 flops x fwd+bwd(3x)
     gemm_ms_per_step = gemm_ms / args.steps
     achieved = gemm_ops_per_step / (gemm_ms_per_step * 1e-3) / 1e12
+    # cuBLAS plain int8 (torch._int_mm: no block scales, no fallback) on the
+    # step's largest GEMM shape (gate/up forward, T x 2 d_ff x d_model), same run
+    int8_ref = None
+    try:
+        xi = torch.randint(-127, 128, (T, D_MODEL), device=device, dtype=torch.int8)
+        wi = torch.randint(-127, 128, (D_MODEL, 2 * D_FF), device=device, dtype=torch.int8)
+        for _ in range(3):
+            torch._int_mm(xi, wi)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            torch._int_mm(xi, wi)
+        e1.record()
+        torch.cuda.synchronize()
+        int8_ref = round(2 * T * 2 * D_FF * D_MODEL / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e12, 1)
+        del xi, wi
+    except Exception:
+        int8_ref = None
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    bf16_sus = peaks.get("bf16_tflops_sustained")
-    peak = 2.0 * bf16_sus if bf16_sus else 2.0 * 1400.0
+    # dense int8 = 2 x dense bf16 on B200; the BURST cuBLAS bf16 figure (the
+    # timed region is ~0.1-0.2 s, not a seconds-long power-capped loop)
+    bf16_burst = peaks.get("bf16_tflops")
+    peak = 2.0 * bf16_burst if bf16_burst else 2.0 * 1590.0
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tr_path):
@@ -618,6 +749,17 @@ def run_ours(args, rank, world, local):
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
+        comparator = exact = None
+        if not args.no_sweep:
+            try:
+                comparator = bf16_mlp_comparator(device, T)
+                comparator["speedup_of_fbq"] = value / world / comparator["tokens_per_s"]
+            except Exception as ex:  # pragma: no cover
+                comparator = {"error": str(ex)[:200]}
+            try:
+                exact = exact_mode_rate(device, T)
+            except Exception as ex:  # pragma: no cover
+                exact = {"error": str(ex)[:200]}
         sweep = qsweep = c4 = None
         if not args.no_sweep:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
@@ -668,13 +810,16 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "tensor", "kernel": "fbq_gemm_kernel (tcgen05 kind::i8)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained "
-                                        "(dense int8 = 2x dense bf16 on B200)",
+                         "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst; dense int8 = "
+                                        "2x dense bf16 on B200)",
+                         "cublas_int8_same_shape_TOPS": int8_ref,
                          "frac_of_nominal_4500": achieved / 4500.0,
                          "gemm_share_of_step": gemm_ms_per_step / ms,
                          "gemm_launches_per_step": n_gemm / args.steps},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
+            "bf16_mlp_comparator": comparator,
+            "exact_mode": exact,
             "gemm_sweep": sweep,
             "quant_sweep": qsweep,
             "qwen_block_c4": c4,

@@ -58,6 +58,14 @@ enum fbq_epilogue {
 };
 
 const char* fbq_version(void);
+/* One-time setup of the CURRENT device (thread-safe, idempotent; allocates and
+ * synchronises once): the GEMM's dynamic tile-counter ring.  Call it once per
+ * device before capturing or timing work (the fbq_mlp_* / fbq_linear_*
+ * drivers call it at creation).  The fbq_cuda_* entry points work without it
+ * -- the GEMM then uses its static tile schedule -- and never allocate or
+ * synchronise themselves; every call is safe from concurrent host threads
+ * and under CUDA stream capture. */
+int fbq_cuda_init(void);
 const char* fbq_status_string(int status);
 int fbq_last_cuda_error(void); /* cudaError_t of the last FBQ_ERR_CUDA on this thread */
 int fbq_block_side(void);      /* 128 */

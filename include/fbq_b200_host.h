@@ -58,6 +58,13 @@ int fbq_mlp_backward_device(void* mlp, const void* gy, int64_t tokens, int64_t r
                             int step, void* gx, fbq_stream_t stream);
 /* controller_step of every layer (trainsim.cpp:129-133) from the last forward */
 int fbq_mlp_controller_step(void* mlp, fbq_stream_t stream);
+/* Data parallel (trainsim.cpp:93,129-133 / policy.cpp:97-109 on the global
+ * batch): the device int32[2] masked-block counters of the last forward
+ * (gate/up, down) -- sum them over ranks in place on `stream` -- and a
+ * controller step that divides by the GLOBAL block counts (0 = local). */
+int32_t* fbq_mlp_count_ptr(void* mlp);
+int fbq_mlp_controller_step_blocks(void* mlp, int64_t blocks_gate_up, int64_t blocks_down,
+                                   fbq_stream_t stream);
 /* zero_grad is deferred: the next backward's dW GEMMs write instead of
  * accumulate (bit-identical to adding into zeroed buffers, no 0.7 GB memset
  * per step).  fbq_mlp_get_grads / fbq_mlp_grad_ptr materialise pending zeros;
@@ -96,11 +103,11 @@ int64_t fbq_mlp_launch_count(void* mlp);
  * all-reduce): which = 0 gate (d_ff x d_model), 1 up, 2 down (d_model x d_ff).
  * gate and up are contiguous ([gate; up]). */
 void* fbq_mlp_grad_ptr(void* mlp, int which);
-/* Make `stream` wait until gradient `which` (0/1: dW_gate|dW_up, final at the
- * end of backward; 2: dW_down, final right after its GEMM, i.e. while the GLU
- * backward and the gate/up GEMMs are still running) of the LAST enqueued
- * backward is complete: data-parallel callers all-reduce dW_down on a side
- * stream overlapped with the rest of the backward. */
+/* Make `stream` wait until gradient `which` (0 dW_gate, 1 dW_up, 2 dW_down) of
+ * the LAST enqueued backward is complete.  Each is final right after its own
+ * GEMM (dW_down first, while the GLU backward and the gate/up GEMMs still run;
+ * dW_gate while dW_up is computed): data-parallel callers all-reduce each on a
+ * side stream overlapped with the rest of the backward. */
 int fbq_mlp_wait_grad(void* mlp, int which, fbq_stream_t stream);
 /* Copy gradients / fallback statistics to the host (synchronises). */
 int fbq_mlp_get_grads(void* mlp, float* g_gate, float* g_up, float* g_down);
@@ -135,6 +142,9 @@ int fbq_linear_forward_device(void* linear, const void* x, int64_t tokens, int64
 int fbq_linear_backward_device(void* linear, const void* gy, int64_t tokens, int64_t row_offset,
                                int step, void* gx, fbq_stream_t stream);
 int fbq_linear_controller_step(void* linear, fbq_stream_t stream);
+/* data parallel, as fbq_mlp_count_ptr / fbq_mlp_controller_step_blocks (int32[1]) */
+int32_t* fbq_linear_count_ptr(void* linear);
+int fbq_linear_controller_step_blocks(void* linear, int64_t blocks, fbq_stream_t stream);
 /* zero_grad is deferred like fbq_mlp_zero_grad: the next backward's dW GEMM
  * writes instead of accumulating; fbq_linear_grad_ptr materialises a pending
  * zero before returning the pointer. */

@@ -34,6 +34,7 @@ _SIGS = {
     "fbq_status_string": (C.c_char_p, [cint]),
     "fbq_last_cuda_error": (cint, []),
     "fbq_block_side": (cint, []),
+    "fbq_cuda_init": (cint, []),
     "fbq_cuda_block_absmax": (cint, [vp, cint, i64, i64, i64, vp, vp]),
     "fbq_cuda_mask_topk": (cint, [vp, i64, dbl, vp, vp, vp]),
     "fbq_cuda_rmsnorm_forward": (cint, [vp, cint, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp]),
@@ -80,5 +81,24 @@ def check(status: int, what: str) -> None:
     raise FbqError(status, what)
 
 
+_initialised = set()
+
+
+def ensure_init() -> None:
+    """fbq_cuda_init() once per CUDA device this process launches on (the GEMM's
+    tile-counter ring; one allocation + sync, never on the launch path)."""
+    import torch
+    dev = torch.cuda.current_device()
+    if dev not in _initialised:
+        check(lib.fbq_cuda_init(), "fbq_cuda_init")
+        _initialised.add(dev)
+
+
 def call(name: str, *args) -> None:
+    if name.startswith("fbq_cuda_") and not _initialised:
+        ensure_init()
+    elif name.startswith("fbq_cuda_"):
+        import torch
+        if torch.cuda.current_device() not in _initialised:
+            ensure_init()
     check(getattr(lib, name)(*args), name)

@@ -23,8 +23,15 @@ LIB = os.path.join(LIB_DIR, "libfbq_b200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+# -ftz=false / IEEE division: the bit-exact rounding in fbq_round.cuh (the
+# parity-denormal RTN fix, subnormal scales and products) needs
+# fp32 denormals preserved; nvcc defines no macro for -ftz, so the flags are
+# pinned here and checked below (never add --use_fast_math).
+CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ftz=false",
+                   "-prec-div=true", "-prec-sqrt=true",
                    "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+assert not any(f in CU_FLAGS for f in ("--use_fast_math", "-use_fast_math", "-ftz=true")), \
+    "fbq kernels require IEEE denormals (no FTZ / fast math)"
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 

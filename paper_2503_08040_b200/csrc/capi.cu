@@ -44,6 +44,8 @@ void fbq_debug_set_gemm_prof(long long* dev_buf) { g_gemm_prof = dev_buf; }
 void fbq_debug_set_quant_diag(int flags) { fbq::g_quant_diag = flags; }
 int fbq_block_side(void) { return 128; }
 
+int fbq_cuda_init(void) { return cuda_status(fbq::gemm_init()); }
+
 int fbq_malloc(void** ptr, size_t bytes) {
   if (!ptr) return FBQ_ERR_ARG;
   *ptr = nullptr;

@@ -37,7 +37,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "gemm_kernel.cuh"
 #include "sm100.cuh"
@@ -658,15 +660,14 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static PFN_encodeTiled get_encode() {
-  static PFN_encodeTiled fn = nullptr;
-  if (!fn) {
+  static const PFN_encodeTiled fn = [] {  // thread-safe one-time lookup
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled>(ptr);
-  }
+      return reinterpret_cast<PFN_encodeTiled>(ptr);
+    return (PFN_encodeTiled) nullptr;
+  }();
   return fn;
 }
 
@@ -685,34 +686,87 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t inner, int64_t ou
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int gemm_num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+// ---- per-device state (thread-safe; set up by gemm_init, never in a launch) ----
+constexpr int kMaxDevices = 64;
+// Dynamic tile counters: a ring of 128-byte slots per device, zeroed once at
+// gemm_init.  Every launch takes the next slot with an atomic fetch_add and
+// leaves it at zero again (the last CTA to make its final claim resets it),
+// so no memset node per launch and no allocation or synchronisation on the
+// launch path (safe under stream capture: a captured launch keeps its slot,
+// which every replay leaves reset).  kSlots concurrent launches per device
+// may be in flight before a slot is reused.
+constexpr int kCounterSlots = 4096;
+static std::atomic<int*> g_ring[kMaxDevices];
+static std::atomic<unsigned> g_next_slot[kMaxDevices];
+static std::once_flag g_init_once[kMaxDevices];
+static cudaError_t g_init_err[kMaxDevices] = {};
+static std::atomic<int> g_num_sms[kMaxDevices];
+
+static int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+  return dev;
+}
+
+// kernel attributes + SM count, once per device (no allocation, no sync: may
+// run on the launch path)
+static std::once_flag g_attr_once[kMaxDevices];
+static cudaError_t g_attr_err[kMaxDevices] = {};
+static cudaError_t gemm_attributes(int dev) {
+  std::call_once(g_attr_once[dev], [dev] {
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+    g_num_sms[dev].store(n > 0 ? n : 148);
+    for (cudaError_t e : {cudaFuncSetAttribute(fbq_gemm_kernel<kEpiExact>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+                          cudaFuncSetAttribute(fbq_gemm_kernel<kEpiFma>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+                          cudaFuncSetAttribute(fbq_gemm_kernel<kEpiDump>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)})
+      if (e != cudaSuccess && g_attr_err[dev] == cudaSuccess) g_attr_err[dev] = e;
+  });
+  return g_attr_err[dev];
+}
+
+cudaError_t gemm_init() {
+  const int dev = current_device();
+  if (dev < 0) return cudaErrorInvalidDevice;
+  if (cudaError_t e = gemm_attributes(dev)) return e;
+  std::call_once(g_init_once[dev], [dev] {
+    int* r = nullptr;
+    cudaError_t e = cudaMalloc(&r, (size_t)kCounterSlots * 128);
+    if (e == cudaSuccess) e = cudaMemset(r, 0, (size_t)kCounterSlots * 128);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      if (r) cudaFree(r);
+      g_init_err[dev] = e;
+      return;
+    }
+    g_ring[dev].store(r, std::memory_order_release);
+  });
+  return g_init_err[dev];
+}
+
+static bool gemm_ready(int dev) { return dev >= 0 && g_ring[dev].load(std::memory_order_acquire) != nullptr; }
+
+int gemm_num_sms() {
+  const int dev = current_device();
+  const int n = dev >= 0 ? g_num_sms[dev].load() : 0;
+  return n > 0 ? n : 148;
 }
 
 template <int kEpi>
 static cudaError_t launch_typed(const CUtensorMap& ma, const CUtensorMap& mr,
                                 const CUtensorMap& mb, const CUtensorMap& mo, const GemmParams& p,
                                 int grid, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fbq_gemm_kernel<kEpi>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   fbq_gemm_kernel<kEpi><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, mo, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s) {
+  const int dev = current_device();
+  if (dev < 0) return cudaErrorInvalidDevice;
+  if (cudaError_t e = gemm_attributes(dev)) return e;
   CUtensorMap ma, mr, mb;
   const int64_t M = p.M, N = p.N, K = p.K;
   bool ok = true;
@@ -747,28 +801,12 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
       p.tma_store = p.accumulate ? 2 : ((p.diag & 16384) ? 3 : 1);
   }
   p.num_tiles = p.MB * ((p.NB + 1) / 2);
-  // dynamic tile counter: a slot of a per-device ring (zeroed once at
-  // allocation; every launch leaves its slot at zero again -- the last CTA to
-  // make its final claim resets it), so no memset node per launch
+  // dynamic tile counter: the next slot of the device's ring (see gemm_init);
+  // before fbq_cuda_init() ran on this device, the static tile schedule
   p.tile_ctr = nullptr;
-  if (!(p.diag & (1 << 21)) && !(p.diag & 512)) {  // diagnostics: 1 << 21 = static schedule
-    static int* ring[64] = {};
-    static unsigned next_slot[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64) {
-      constexpr int kSlots = 256;
-      if (!ring[dev]) {
-        int* r = nullptr;
-        if (cudaMalloc(&r, kSlots * 128) == cudaSuccess) {
-          if (cudaMemset(r, 0, kSlots * 128) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess)
-            ring[dev] = r;
-          else
-            cudaFree(r);
-        }
-      }
-      if (ring[dev]) p.tile_ctr = ring[dev] + (next_slot[dev]++ % kSlots) * 32;  // one 128 B line per slot
-    }
+  if (gemm_ready(dev) && !(p.diag & (1 << 21)) && !(p.diag & 512)) {  // diag 1 << 21: static schedule
+    const unsigned slot = g_next_slot[dev].fetch_add(1, std::memory_order_relaxed) % kCounterSlots;
+    p.tile_ctr = g_ring[dev].load(std::memory_order_acquire) + (size_t)slot * 32;  // one 128 B line per slot
   }
   {
     // only when the other operand does not fit: with both small, or both

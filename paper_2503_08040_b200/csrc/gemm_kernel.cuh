@@ -40,6 +40,10 @@ struct GemmParams {
   long long* prof;  // perf diagnostics: 16 int64 per CTA (MMA-warp cycles, epilogue timeline) or null
 };
 
+// Per-device one-time setup (the dynamic tile-counter ring: one allocation
+// + zeroing + sync); thread-safe, idempotent.  Until it has run on the current
+// device launch_gemm uses the static tile schedule; it never allocates.
+cudaError_t gemm_init();
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s);
 int gemm_num_sms();
 

@@ -101,7 +101,7 @@ struct Mlp {
   DevBuf hx, hgy, hy, hgx;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_x = nullptr, ev_gy = nullptr, ev_fwd = nullptr, ev_bwd = nullptr;
-  cudaEvent_t ev_grad[2] = {nullptr, nullptr};  // [0] dW_gate|up final, [1] dW_down final
+  cudaEvent_t ev_grad[3] = {nullptr, nullptr, nullptr};  // dW_gate, dW_up, dW_down final
   // backward side stream: the dW GEMMs run there, so each GEMM's last-wave
   // tail (up to one 224-k-block tile on the long-K dX) is filled by the next
   // independent grid's CTAs instead of idling SMs
@@ -118,6 +118,7 @@ struct Mlp {
     if (D <= 0 || F <= 0 || T <= 0) throw CudaError(FBQ_ERR_SHAPE, "bad MLP shape");
     // d_ff % 128: the concatenated [gate; up] planes must not share a block
     if (D % 16 || F % 128) throw CudaError(FBQ_ERR_UNSUPPORTED, "need d_model % 16 == 0 and d_ff % 128 == 0");
+    FBQ_TRY(fbq_cuda_init());  // per-device setup (GEMM tile-counter ring) before any launch
     ldD = ld16(D);
     ldF = ld16(F);
     ldF2 = ld16(2 * F);
@@ -173,7 +174,7 @@ struct Mlp {
     CU_TRY(cudaEventCreateWithFlags(&ev_gy, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
     CU_TRY(cudaEventCreateWithFlags(&ev_bwd, cudaEventDisableTiming));
-    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_fork[0], &ev_fork[1], &ev_join, &ev_ffork, &ev_wgu, &ev_wd,
+    for (cudaEvent_t* e : {&ev_grad[0], &ev_grad[1], &ev_grad[2], &ev_fork[0], &ev_fork[1], &ev_join, &ev_ffork, &ev_wgu, &ev_wd,
                            &ev_gyq})
       CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CU_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -188,7 +189,7 @@ struct Mlp {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (side) cudaStreamDestroy(side);
-    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1], ev_fork[0], ev_fork[1], ev_join,
+    for (cudaEvent_t e : {ev_x, ev_gy, ev_fwd, ev_bwd, ev_grad[0], ev_grad[1], ev_grad[2], ev_fork[0], ev_fork[1], ev_join,
                           ev_ffork, ev_wgu, ev_wd, ev_gyq})
       if (e) cudaEventDestroy(e);
   }
@@ -331,7 +332,7 @@ struct Mlp {
                           nullptr, nullptr, D, F, tok, g_d.p, FBQ_F32, F, acc_w, c.epilogue, b); }, b);
     // dW_d is final for this step: data-parallel callers start its all-reduce
     // on a side stream here, overlapped with the rest of the backward
-    CU_TRY(cudaEventRecord(ev_grad[1], b));
+    CU_TRY(cudaEventRecord(ev_grad[2], b));
     // GLU backward fused with SR(ga), SR(gb)
     FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.as<int16_t>(),
                                   ctx_b.as<int16_t>(), ldF, ctx_a_s.as<float>(),
@@ -368,27 +369,35 @@ struct Mlp {
     gemm([&] { return fbq_cuda_gemm_ex(gqc, ldF2, gqs, lds_gq, FBQ_MN_MAJOR, ctx_g.as<int8_t>(), ldD,
                              x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr, nullptr, F,
                              D, tok, g_gu.p, FBQ_F32, D, acc_w, c.epilogue, b); }, b);
+    // dW_gate is final: its all-reduce overlaps the dW_up GEMM
+    CU_TRY(cudaEventRecord(ev_grad[0], b));
     gemm([&] { return fbq_cuda_gemm_ex(gqc + F, ldF2, gqs + gF, lds_gq, FBQ_MN_MAJOR, ctx_u.as<int8_t>(),
                              ldD, x_scales.as<float>(), gD, FBQ_MN_MAJOR, nullptr, nullptr,
                              nullptr, F, D, tok, g_gu.as<float>() + F * D, FBQ_F32, D, acc_w,
                              c.epilogue, b); }, b);
+    CU_TRY(cudaEventRecord(ev_grad[1], b));
     // join: everything after the backward (controller, next step, readers of
     // dW) is ordered after the side stream's GEMMs
     CU_TRY(cudaEventRecord(ev_join, side));
     CU_TRY(cudaStreamWaitEvent(s, ev_join, 0));
-    CU_TRY(cudaEventRecord(ev_grad[0], s));
   }
 
-  void controller(cudaStream_t s) {
+  // observed rate = masked blocks / blocks of the last forward (policy.cpp:82-87).
+  // Data parallel: the caller sums `counts` over ranks in place and passes the
+  // global block counts, so every rank updates theta with the rate of the whole
+  // batch (trainsim.cpp:93,129-133) and the thresholds stay identical.
+  void controller(cudaStream_t s, int64_t blocks_gu = 0, int64_t blocks_d = 0) {
     launches += 2;
-    // observed rate = masked blocks / blocks of the last forward (policy.cpp:82-87)
-    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), counts.as<int32_t>(), last_blocks[0],
+    ctl_blocks[0] = blocks_gu > 0 ? blocks_gu : last_blocks[0];
+    ctl_blocks[1] = blocks_d > 0 ? blocks_d : last_blocks[1];
+    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), counts.as<int32_t>(), ctl_blocks[0],
                                        c.r_min, c.r_max, c.alpha, rates.as<double>(), s));
     FBQ_TRY(fbq_cuda_controller_update(theta.as<double>() + 1, counts.as<int32_t>() + 1,
-                                       last_blocks[1], c.r_min, c.r_max, c.alpha,
+                                       ctl_blocks[1], c.r_min, c.r_max, c.alpha,
                                        rates.as<double>() + 1, s));
   }
   int64_t last_blocks[2] = {1, 1};
+  int64_t ctl_blocks[2] = {0, 0};  // blocks the last controller step divided by (0: none yet)
 
   void step_host(const float* x, const float* gy, int64_t tok, int step, float* y, float* gx) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
@@ -547,6 +556,7 @@ struct QuantLinear {
     T = c.max_tokens;
     if (In <= 0 || Out <= 0 || T <= 0) throw CudaError(FBQ_ERR_SHAPE, "bad linear shape");
     if (In % 16 || Out % 16) throw CudaError(FBQ_ERR_UNSUPPORTED, "need in/out features % 16 == 0");
+    FBQ_TRY(fbq_cuda_init());
     ldIn = ld16(In);
     ldOut = ld16(Out);
     gIn = cdiv(In, 128);
@@ -631,10 +641,11 @@ struct QuantLinear {
   }
   bool grad_zero_pending = false;
 
-  void controller(cudaStream_t s) {
+  void controller(cudaStream_t s, int64_t blocks = 0) {
     if (c.fallback_mode != 0) return;  // trainsim.cpp:129-133: Threshold mode only
-    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), count.as<int32_t>(), last_blocks,
-                                       c.r_min, c.r_max, c.alpha, rate.as<double>(), s));
+    FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), count.as<int32_t>(),
+                                       blocks > 0 ? blocks : last_blocks, c.r_min, c.r_max,
+                                       c.alpha, rate.as<double>(), s));
   }
 };
 
@@ -712,6 +723,16 @@ int fbq_mlp_controller_step(void* m, fbq_stream_t stream) {
   return guarded([&] { static_cast<Mlp*>(m)->controller(reinterpret_cast<cudaStream_t>(stream)); });
 }
 
+int fbq_mlp_controller_step_blocks(void* m, int64_t blocks_gate_up, int64_t blocks_down,
+                                   fbq_stream_t stream) {
+  if (!m || blocks_gate_up < 0 || blocks_down < 0) return FBQ_ERR_ARG;
+  return guarded([&] {
+    static_cast<Mlp*>(m)->controller(reinterpret_cast<cudaStream_t>(stream), blocks_gate_up, blocks_down);
+  });
+}
+
+int32_t* fbq_mlp_count_ptr(void* m) { return m ? static_cast<Mlp*>(m)->counts.as<int32_t>() : nullptr; }
+
 int fbq_mlp_zero_grad(void* m, fbq_stream_t stream) {
   if (!m) return FBQ_ERR_ARG;
   return guarded([&] {
@@ -772,7 +793,7 @@ int64_t fbq_mlp_launch_count(void* m) { return m ? static_cast<Mlp*>(m)->launche
 int fbq_mlp_wait_grad(void* m, int which, fbq_stream_t stream) {
   if (!m || which < 0 || which > 2) return FBQ_ERR_ARG;
   auto* mlp = static_cast<Mlp*>(m);
-  cudaEvent_t e = mlp->ev_grad[which == 2 ? 1 : 0];
+  cudaEvent_t e = mlp->ev_grad[which];
   return cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), e, 0) == cudaSuccess ? FBQ_OK
                                                                                           : FBQ_ERR_CUDA;
 }
@@ -815,8 +836,12 @@ int fbq_mlp_get_controller(void* m, double* rates, double* thresholds) {
       // last observed rate of the most recent forward (masked / blocks)
       int32_t cnt[2];
       CU_TRY(cudaMemcpy(cnt, mlp->counts.p, 8, cudaMemcpyDeviceToHost));
-      rates[0] = (double)cnt[0] / (double)mlp->last_blocks[0];
-      rates[1] = (double)cnt[1] / (double)mlp->last_blocks[1];
+      // counts are global after a data-parallel reduction: divide by the
+      // blocks the controller used (local blocks when no step ran yet)
+      for (int i = 0; i < 2; ++i) {
+        const int64_t b = mlp->ctl_blocks[i] > 0 ? mlp->ctl_blocks[i] : mlp->last_blocks[i];
+        rates[i] = (double)cnt[i] / (double)b;
+      }
     }
   });
 }
@@ -871,6 +896,15 @@ int fbq_linear_backward_device(void* l, const void* gy, int64_t tokens, int64_t 
 int fbq_linear_controller_step(void* l, fbq_stream_t stream) {
   if (!l) return FBQ_ERR_ARG;
   return guarded([&] { static_cast<QuantLinear*>(l)->controller(reinterpret_cast<cudaStream_t>(stream)); });
+}
+int fbq_linear_controller_step_blocks(void* l, int64_t blocks, fbq_stream_t stream) {
+  if (!l || blocks < 0) return FBQ_ERR_ARG;
+  return guarded([&] {
+    static_cast<QuantLinear*>(l)->controller(reinterpret_cast<cudaStream_t>(stream), blocks);
+  });
+}
+int32_t* fbq_linear_count_ptr(void* l) {
+  return l ? static_cast<QuantLinear*>(l)->count.as<int32_t>() : nullptr;
 }
 int fbq_linear_zero_grad(void* l, fbq_stream_t stream) {
   if (!l) return FBQ_ERR_ARG;

@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
 
 #include <cuda.h>
 
@@ -1321,6 +1322,24 @@ static cudaError_t opt_in_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// Per-device, thread-safe one-time setup of one kernel instance (shared-memory
+// opt-in, occupancy): function attributes are per device, and two host threads
+// may launch concurrently.  No allocation or synchronisation.
+constexpr int kMaxDev = 64;
+struct DevOnce {
+  std::once_flag flag[kMaxDev];
+  cudaError_t err[kMaxDev] = {};
+  int val[kMaxDev] = {};
+};
+template <class F>
+static cudaError_t dev_once(DevOnce& o, F&& f, int* val = nullptr) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  std::call_once(o.flag[dev], [&] { o.err[dev] = f(o.val[dev]); });
+  if (val) *val = o.val[dev];
+  return o.err[dev];
+}
+
 // Launch with programmatic stream serialisation when the grid follows
 // fbq_zero_count_kernel (p.pdl): it may start while the zeroing grid drains.
 template <typename... KArgs, typename... Args>
@@ -1351,11 +1370,11 @@ cudaError_t launch_zero_count(int* count, cudaStream_t s) {
 template <typename T, bool kVec, int kSR>
 static cudaError_t launch_k1_sr(const QuantParams& p, dim3 grid, cudaStream_t s) {
   const size_t smem = sizeof(T) * kTileElems;
-  static bool ready = false;
-  if (!ready) {
-    if (cudaError_t e = opt_in_smem(fbq_quantize_block_kernel<T, kVec, kSR, sizeof(T) == 2 ? 4 : 1>, smem)) return e;
-    ready = true;
-  }
+  static DevOnce once;
+  if (cudaError_t e = dev_once(once, [&](int&) {
+        return opt_in_smem(fbq_quantize_block_kernel<T, kVec, kSR, sizeof(T) == 2 ? 4 : 1>, smem);
+      }))
+    return e;
   // bf16 tiles (32 KiB): four CTAs per SM at 64 registers (measured 7 % faster
   // than three at 76-82 registers for the two-plane SR launch); fp32 tiles
   // (64 KiB) are shared-memory bound at three CTAs anyway
@@ -1380,41 +1399,44 @@ typedef CUresult (*PFN_encodeTiledQ)(CUtensorMap*, CUtensorMapDataType, cuuint32
                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static PFN_encodeTiledQ encode_fn() {
-  static PFN_encodeTiledQ fn = nullptr;
-  if (!fn) {
+  static const PFN_encodeTiledQ fn = [] {  // thread-safe one-time lookup
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiledQ>(ptr);
-  }
+      return reinterpret_cast<PFN_encodeTiledQ>(ptr);
+    return (PFN_encodeTiledQ) nullptr;
+  }();
   return fn;
 }
 
 static int num_sms() {
-  static int n = 0;
-  if (!n) {
+  static DevOnce once;
+  int n = 0;
+  dev_once(once, [](int& v) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    return cudaSuccess;
+  }, &n);
+  return n > 0 ? n : 148;
 }
 
 template <typename T, int kSR, int kQStages>
 static cudaError_t launch_k1_tma(const QuantParams& p, cudaStream_t s) {
   const size_t smem = (size_t)kQStages * sizeof(T) * kTileElems;
-  static int ctas_per_sm = 0;
-  if (!ctas_per_sm) {
-    if (cudaError_t e = opt_in_smem(fbq_quantize_tma_kernel<T, kSR, kQStages>, smem)) return e;
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_kernel<T, kSR, kQStages>,
-                                                      kQuantThreads, smem) != cudaSuccess || n < 1)
-      n = 1;
-    ctas_per_sm = n;
-  }
+  static DevOnce once;
+  int ctas_per_sm = 1;
+  if (cudaError_t e = dev_once(once, [&](int& v) {
+        if (cudaError_t e2 = opt_in_smem(fbq_quantize_tma_kernel<T, kSR, kQStages>, smem)) return e2;
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_kernel<T, kSR, kQStages>, kQuantThreads, smem) != cudaSuccess || n < 1)
+          n = 1;
+        v = n;
+        return cudaSuccess;
+      }, &ctas_per_sm))
+    return e;
   CUtensorMap m;
   PFN_encodeTiledQ enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -1438,15 +1460,17 @@ static cudaError_t launch_k1_tma(const QuantParams& p, cudaStream_t s) {
 template <typename T, int kQStages, int kMinBlocks, int kSR>
 static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
   const size_t smem = (size_t)kQStages * sizeof(T) * kTileElems;
-  static int ctas_per_sm = 0;
-  if (!ctas_per_sm) {
-    if (cudaError_t e = opt_in_smem(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, smem)) return e;
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>,
-                                                      kQuantThreads, smem) != cudaSuccess || n < 1)
-      n = 1;
-    ctas_per_sm = n;
-  }
+  static DevOnce once;
+  int ctas_per_sm = 1;
+  if (cudaError_t e = dev_once(once, [&](int& v) {
+        if (cudaError_t e2 = opt_in_smem(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, smem)) return e2;
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, kQuantThreads, smem) != cudaSuccess || n < 1)
+          n = 1;
+        v = n;
+        return cudaSuccess;
+      }, &ctas_per_sm))
+    return e;
   CUtensorMap m;
   PFN_encodeTiledQ enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;

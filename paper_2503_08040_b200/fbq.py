@@ -21,6 +21,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field, replace
 
+import numpy as np
 import torch
 
 from . import _capi as K
@@ -371,6 +372,37 @@ def mask_topk(scores: torch.Tensor, rate: float) -> torch.Tensor:
                _stream())
     gr, gc = (scores.shape if scores.dim() == 2 else (1, n))
     return bits_to_mask(bits, gr, gc).view(scores.shape)
+
+
+def theta_for_rate(scores, rate: float):
+    """A THRESHOLD-mode theta that flags ceil(rate*n) blocks under policy.cpp:77's
+    strict `score > theta` -- or, when that count splits a group of tied scores,
+    the nearest count at a tie boundary.  Returns (theta, flagged_fraction).
+    theta is a score value itself (strictly below the flagged ones), so the
+    strict compare makes the count exact; with no block flagged it is the
+    maximum score, with every block flagged it is below the minimum.  (Host
+    helper for benchmarks and tests: the fallback rate a threshold realises.)"""
+    s = np.sort(np.asarray(scores, dtype=np.float64).reshape(-1))[::-1]
+    n = s.size
+    if n == 0:
+        return 1.0, 0.0
+    k = min(n, math.ceil(rate * n))
+
+    def cut_ok(c):  # top c are strictly above the rest
+        return c == 0 or c == n or s[c - 1] > s[c]
+    lo, hi = k, k
+    while not cut_ok(lo):
+        lo -= 1
+    while not cut_ok(hi):
+        hi += 1
+    c = lo if (k - lo) <= (hi - k) else hi
+    if c == 0:
+        theta = float(s[0]) if s[0] > 0 else 1.0
+    elif c == n:
+        theta = float(s[-1]) * 0.5  # every positive score above it
+    else:
+        theta = float(s[c])
+    return theta, c / n
 
 
 def mask_rate(mask: torch.Tensor) -> float:

@@ -37,6 +37,8 @@ _sigs = {
     "fbq_mlp_backward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                           C.c_void_p, C.c_void_p]),
     "fbq_mlp_controller_step": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_mlp_controller_step_blocks": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
+    "fbq_mlp_count_ptr": (C.c_void_p, [C.c_void_p]),
     "fbq_mlp_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fbq_mlp_step_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
                                     C.c_void_p, C.c_void_p]),
@@ -76,6 +78,8 @@ for _name, (_res, _args) in {
     "fbq_linear_backward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                              C.c_void_p, C.c_void_p]),
     "fbq_linear_controller_step": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_linear_controller_step_blocks": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "fbq_linear_count_ptr": (C.c_void_p, [C.c_void_p]),
     "fbq_linear_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fbq_linear_grad_ptr": (C.c_void_p, [C.c_void_p]),
     "fbq_linear_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -90,13 +94,32 @@ def _check(st, what):
 
 
 class _DevArray:
-    """__cuda_array_interface__ view of a driver-owned fp32 buffer."""
+    """__cuda_array_interface__ view of a driver-owned device buffer."""
 
-    def __init__(self, ptr, shape):
+    def __init__(self, ptr, shape, typestr="<f4"):
+        if not ptr:
+            raise K.FbqError(K.FBQ_ERR_CUDA, f"null device pointer ({lib.fbq_host_last_error().decode()})")
         self.__cuda_array_interface__ = {
-            "shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False), "version": 3,
+            "shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False), "version": 3,
             "strides": None,
         }
+
+
+def _blocks(tokens: int, cols: int) -> int:
+    return -(-tokens // 128) * -(-cols // 128)
+
+
+def _check_act(t: torch.Tensor, dtype, cols: int, what: str):
+    if not t.is_cuda or t.dtype != dtype or t.dim() != 2 or t.shape[1] != cols:
+        raise ValueError(f"{what}: expected a CUDA {dtype} tensor of shape (tokens, {cols}), got "
+                         f"{t.device} {t.dtype} {tuple(t.shape)}")
+
+
+def _check_out(out, tokens: int, cols: int, dtype, what: str):
+    if out is not None and (not out.is_cuda or out.dtype != dtype or tuple(out.shape) != (tokens, cols)
+                            or not out.is_contiguous()):
+        raise ValueError(f"{what}: out must be a contiguous CUDA {dtype} tensor of shape "
+                         f"({tokens}, {cols}), got {out.device} {out.dtype} {tuple(out.shape)}")
 
 
 def _stream():
@@ -138,7 +161,8 @@ class GluMlp:
 
     # -- device API ----------------------------------------------------------
     def forward(self, x: torch.Tensor, step: int, row_offset: int = 0, out=None):
-        assert x.is_cuda and x.dtype == self.act_dtype and x.shape[1] == self.d_model
+        _check_act(x, self.act_dtype, self.d_model, "GluMlp.forward x")
+        _check_out(out, x.shape[0], self.d_model, self.act_dtype, "GluMlp.forward")
         x = x.contiguous()
         y = out if out is not None else torch.empty_like(x)
         _check(lib.fbq_mlp_forward_device(self._h, x.data_ptr(), x.shape[0], row_offset, step,
@@ -146,22 +170,35 @@ class GluMlp:
         return y
 
     def backward(self, gy: torch.Tensor, step: int, row_offset: int = 0, out=None):
-        assert gy.is_cuda and gy.dtype == self.act_dtype and gy.shape[1] == self.d_model
+        _check_act(gy, self.act_dtype, self.d_model, "GluMlp.backward dY")
+        _check_out(out, gy.shape[0], self.d_model, self.act_dtype, "GluMlp.backward")
         gy = gy.contiguous()
         gx = out if out is not None else torch.empty_like(gy)
         _check(lib.fbq_mlp_backward_device(self._h, gy.data_ptr(), gy.shape[0], row_offset, step,
                                            gx.data_ptr(), _stream()), "backward")
         return gx
 
-    def controller_step(self):
-        _check(lib.fbq_mlp_controller_step(self._h, _stream()), "controller_step")
+    def controller_step(self, global_tokens: int | None = None):
+        """controller_step (trainsim.cpp:129-133).  Data parallel: after the
+        masked counts (count_tensor) were summed over ranks, pass the global
+        token count so the rate is that of the whole batch."""
+        if global_tokens is None:
+            _check(lib.fbq_mlp_controller_step(self._h, _stream()), "controller_step")
+        else:
+            _check(lib.fbq_mlp_controller_step_blocks(
+                self._h, _blocks(global_tokens, self.d_model), _blocks(global_tokens, self.d_ff),
+                _stream()), "controller_step")
+
+    def count_tensor(self) -> torch.Tensor:
+        """Device int32[2]: masked blocks of the last forward (gate/up, down)."""
+        return torch.as_tensor(_DevArray(lib.fbq_mlp_count_ptr(self._h), (2,), "<i4"), device="cuda")
 
     def zero_grad(self):
         _check(lib.fbq_mlp_zero_grad(self._h, _stream()), "zero_grad")
 
     def wait_grad(self, which: int, stream) -> None:
-        """Make `stream` wait until gradient `which` (0/1 gate/up, 2 down) of the
-        last enqueued backward is final (dW_down: right after its GEMM)."""
+        """Make `stream` wait until gradient `which` (0 gate, 1 up, 2 down) of the
+        last enqueued backward is final (each right after its own GEMM)."""
         _check(lib.fbq_mlp_wait_grad(self._h, which, stream.cuda_stream), "wait_grad")
 
     def grad_tensors(self):
@@ -262,6 +299,10 @@ class QuantLinear:
             self._h = None
 
     def forward(self, x: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        _check_act(x, self.act_dtype, self.in_features, "QuantLinear.forward x")
+        _check_out(out, x.shape[0], self.out_features, self.act_dtype, "QuantLinear.forward")
+        if x.shape[0] > self.max_tokens:
+            raise ValueError(f"QuantLinear.forward: {x.shape[0]} tokens > max_tokens {self.max_tokens}")
         x = x.contiguous()
         y = out if out is not None else torch.empty(x.shape[0], self.out_features, device=x.device,
                                                     dtype=self.act_dtype)
@@ -270,6 +311,10 @@ class QuantLinear:
         return y
 
     def backward(self, gy: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        _check_act(gy, self.act_dtype, self.out_features, "QuantLinear.backward dY")
+        _check_out(out, gy.shape[0], self.in_features, self.act_dtype, "QuantLinear.backward")
+        if gy.shape[0] > self.max_tokens:
+            raise ValueError(f"QuantLinear.backward: {gy.shape[0]} tokens > max_tokens {self.max_tokens}")
         gy = gy.contiguous()
         gx = out if out is not None else torch.empty(gy.shape[0], self.in_features, device=gy.device,
                                                      dtype=self.act_dtype)
@@ -277,8 +322,16 @@ class QuantLinear:
                                               gx.data_ptr(), _stream()), "linear backward")
         return gx
 
-    def controller_step(self):
-        _check(lib.fbq_linear_controller_step(self._h, _stream()), "linear controller_step")
+    def controller_step(self, global_tokens: int | None = None):
+        if global_tokens is None:
+            _check(lib.fbq_linear_controller_step(self._h, _stream()), "linear controller_step")
+        else:
+            _check(lib.fbq_linear_controller_step_blocks(
+                self._h, _blocks(global_tokens, self.in_features), _stream()), "linear controller_step")
+
+    def count_tensor(self) -> torch.Tensor:
+        """Device int32[1]: masked blocks of the last forward (Threshold mode)."""
+        return torch.as_tensor(_DevArray(lib.fbq_linear_count_ptr(self._h), (1,), "<i4"), device="cuda")
 
     def zero_grad(self):
         _check(lib.fbq_linear_zero_grad(self._h, _stream()), "linear zero_grad")

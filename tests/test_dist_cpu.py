@@ -89,3 +89,74 @@ def test_sharded_semantics_on_oracle(orc):
         ctc, cts = orc.transpose_qt(cg, sg)
         dw_sum += orc.block_gemm(ctc, cts, cx, sx)
     assert rel_fro(dw_sum, dw_full) < 1e-6
+
+
+def _ctl_worker(rank, world, port, out):
+    """Global-rate controller semantics with gloo: each rank's local masked
+    count, summed in place, over the global block count drives the same theta
+    update on every rank as the one-process run on the whole batch."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_08040_b200 import fbq
+    from paper_2503_08040_b200.dist import controller_step_global, global_quantile
+
+    class FakeLayer:  # the module protocol controller_step_global uses
+        def __init__(self, masked, blocks_per_token_row):
+            self.c = torch.tensor([masked], dtype=torch.int32)
+            self.bpr = blocks_per_token_row
+            self.state = fbq.FallbackThresholdState(threshold=1.0)
+            self.cfg = fbq.ControllerConfig()
+
+        def count_tensor(self):
+            return self.c
+
+        def controller_step(self, global_tokens=None):
+            blocks = (global_tokens // 128) * self.bpr
+            self.state = fbq.controller_update(self.state, int(self.c.item()) / blocks, self.cfg)
+
+    # rank r flags 10 * (r + 1) of its 4 x 32 = 128 local blocks -> global 30 / 256
+    lay = FakeLayer(10 * (rank + 1), 32)
+    controller_step_global(lay, 2 * 512)
+    q = global_quantile(torch.arange(4, dtype=torch.float32) + 4 * rank, 0.5)
+    out[rank] = (int(lay.c.item()), lay.state.threshold, lay.state.last_rate, q)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_global_controller_rate():
+    from paper_2503_08040_b200 import fbq
+    ctx = mp.get_context("spawn")
+    manager = ctx.Manager()
+    out = manager.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_ctl_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    st = fbq.controller_update(fbq.FallbackThresholdState(threshold=1.0), 30 / 256)  # one process
+    for r in (0, 1):
+        cnt, th, rate, q = out[r]
+        assert cnt == 30
+        assert th == st.threshold and rate == st.last_rate
+        assert q == float(torch.quantile(torch.arange(8, dtype=torch.float32), 0.5))
+
+
+def test_theta_for_rate_realises_rates():
+    """theta_for_rate: strict `score > theta` (policy.cpp:77) flags exactly
+    ceil(rate * n) blocks when scores are distinct, and the nearest tie
+    boundary otherwise (what a threshold can realise)."""
+    from paper_2503_08040_b200.fbq import theta_for_rate
+    rng = np.random.default_rng(0)
+    s = rng.random((64, 32)) * 10 + 1
+    for rate in (0.0, 0.05, 0.1, 0.2, 1.0):
+        th, r = theta_for_rate(s, rate)
+        assert th > 0
+        assert (s > th).sum() == int(np.ceil(rate * s.size)) and r == (s > th).mean()
+    tied = np.array([5.0] * 10 + [3.0] * 10 + [1.0] * 80)
+    th, r = theta_for_rate(tied, 0.14)  # 14 splits the 3.0 group: nearest boundary is 10
+    assert (tied > th).sum() == 10 and r == 0.10
+    th, r = theta_for_rate(tied, 0.17)
+    assert (tied > th).sum() == 20 and r == 0.20

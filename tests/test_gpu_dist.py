@@ -1,10 +1,13 @@
 """GPU: the data-parallel MLP step end to end on one B200 -- two ranks (gloo,
 CUDA tensors, both on cuda:0) each run their 128-row-aligned token shard
 through the fused MLP and reduce dW with dist.allreduce_mlp_grads_overlapped
-(dW_down's all-reduce on a side stream ordered by fbq_mlp_wait_grad, the
-gate/up one after the backward).  The summed dW must equal the full-batch dW
-within fp32 reassociation tolerance and the per-row outputs must be
-bit-identical to the full batch.  NCCL needs one GPU per rank, so
+(dW_down, dW_gate and dW_up each on a side stream ordered by
+fbq_mlp_wait_grad) and the controller with dist.controller_step_global (the
+masked-block counts summed over ranks, the global block count), over three
+steps.  The summed dW must equal the full-batch dW within fp32
+reassociation tolerance; the per-row outputs must be bit-identical to the
+full batch, and so must the thresholds and the observed fallback rates after
+every controller step (trainsim.cpp:93,129-133).  NCCL needs one GPU per rank, so
 the collective here is gloo; the stream/event ordering under test is the same."""
 import os
 import socket
@@ -17,6 +20,7 @@ from tests.helpers import outlier_matrix, rel_fro
 pytestmark = pytest.mark.gpu
 
 D, F, T = 256, 384, 512
+STEPS = 3
 
 
 def _free_port():
@@ -45,7 +49,8 @@ def _worker(rank, world, port, q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2503_08040_b200 import linear
-    from paper_2503_08040_b200.dist import allreduce_mlp_grads_overlapped, shard_rows
+    from paper_2503_08040_b200.dist import (allreduce_mlp_grads_overlapped, controller_step_global,
+                                            shard_rows)
     wg, wu, wd, x, gy = _inputs()
     r0, r1 = shard_rows(T, world, rank)
     kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True, threshold_init=4.0)
@@ -53,12 +58,13 @@ def _worker(rank, world, port, q):
     gu, gd = m.grad_tensors()
     comm = torch.cuda.Stream()
     outs = []
-    for step in range(2):
+    for step in range(STEPS):
         m.zero_grad()
         y = m.forward(torch.from_numpy(x[r0:r1]).cuda(), step, row_offset=r0)
         gx = m.backward(torch.from_numpy(gy[r0:r1]).cuda(), step, row_offset=r0)
         allreduce_mlp_grads_overlapped(m, gu, gd, comm)
-        outs.append((y.cpu().numpy(), gx.cpu().numpy()))
+        controller_step_global(m, T)
+        outs.append((y.cpu().numpy(), gx.cpu().numpy(), m.controller_state()))
     torch.cuda.synchronize()
     q.put((rank, r0, r1, outs, gu.cpu().numpy(), gd.cpu().numpy()))
     dist.barrier()
@@ -84,16 +90,20 @@ def test_dp_world2_overlapped_allreduce_matches_full_batch():
     full = linear.GluMlp(wg, wu, wd, T, **kw)
     gu, gd = full.grad_tensors()
     want = []
-    for step in range(2):
+    for step in range(STEPS):
         full.zero_grad()
         y = full.forward(torch.from_numpy(x).cuda(), step).cpu().numpy()
         gx = full.backward(torch.from_numpy(gy).cuda(), step).cpu().numpy()
-        want.append((y, gx))
+        full.controller_step()
+        want.append((y, gx, full.controller_state()))
     torch.cuda.synchronize()
+    # the controller must actually move theta in this test (else it proves nothing)
+    assert want[0][2][1] != want[-1][2][1]
     for rank, r0, r1, outs, g_gu, g_d in res:
-        for (y, gx), (yw, gxw) in zip(outs, want):
-            assert np.array_equal(y.view(np.int32), yw[r0:r1].view(np.int32))
-            assert np.array_equal(gx.view(np.int32), gxw[r0:r1].view(np.int32))
+        for step, ((y, gx, ctl), (yw, gxw, ctlw)) in enumerate(zip(outs, want)):
+            assert np.array_equal(y.view(np.int32), yw[r0:r1].view(np.int32)), step
+            assert np.array_equal(gx.view(np.int32), gxw[r0:r1].view(np.int32)), step
+            assert ctl == ctlw, (step, ctl, ctlw)  # global rates and thresholds
         # both ranks hold the all-reduced sum (last step's dW)
         assert rel_fro(g_gu, gu.cpu().numpy()) < 1e-6
         assert rel_fro(g_d, gd.cpu().numpy()) < 1e-6

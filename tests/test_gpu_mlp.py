@@ -195,9 +195,9 @@ def test_mlp_fma_epilogue_fp32_close_to_reference(mods):
 
 
 def test_mlp_grad_ready_events():
-    """fbq_mlp_wait_grad: a side stream ordered after dW_down's event sees the
-    final dW_down while the rest of the backward may still run (the hook the
-    data-parallel all-reduce overlaps on); likewise dW_gate|up at the end."""
+    """fbq_mlp_wait_grad: a side stream ordered after a gradient's event sees
+    that gradient final while the rest of the backward may still run (the hook
+    the data-parallel all-reduces overlap on): dW_down, dW_gate, dW_up."""
     import torch
     from paper_2503_08040_b200 import linear
     d, f, t = 1024, 2048, 2048
@@ -216,10 +216,14 @@ def test_mlp_grad_ready_events():
             early_d = gd.clone()
         m.wait_grad(0, side)
         with torch.cuda.stream(side):
-            early_gu = gu.clone()
+            early_g = gu[:f].clone()
+        m.wait_grad(1, side)
+        with torch.cuda.stream(side):
+            early_u = gu[f:].clone()
         torch.cuda.synchronize()
         assert torch.equal(early_d, gd)
-        assert torch.equal(early_gu, gu)
+        assert torch.equal(early_g, gu[:f])
+        assert torch.equal(early_u, gu[f:])
         assert float(gd.abs().sum()) > 0
 
 
