@@ -295,8 +295,16 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
             __syncwarp();
             if (lane == 0) {
               const int c0 = bn * 128 + c * cols_per_box;
-              if (p.tma_store == 2) tma_reduce_add_2d(map_o, obuf, c0, (int)row0);
-              else tma_store_2d(map_o, obuf, c0, (int)row0);
+              // the output streams past the L2-resident operand: evict_first
+              // (diag 1 << 24: default policy)
+              if (p.diag & (1 << 24)) {
+                if (p.tma_store == 2) tma_reduce_add_2d(map_o, obuf, c0, (int)row0);
+                else tma_store_2d(map_o, obuf, c0, (int)row0);
+              } else {
+                const uint64_t pol_o = l2_policy_evict_first();
+                if (p.tma_store == 2) tma_reduce_add_2d_hint(map_o, obuf, c0, (int)row0, pol_o);
+                else tma_store_2d_hint(map_o, obuf, c0, (int)row0, pol_o);
+              }
               bulk_commit();
             }
           }
@@ -464,7 +472,10 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint64_t pol_keep = l2_policy_evict_last();
       const bool split_pol = !(p.diag & (1 << 23));
       const uint64_t pol_a = (split_pol && p.n_fastest) ? l2_policy_evict_first() : pol_keep;
-      const uint64_t pol_b = (split_pol && p.group_m == p.MB && p.group_m > 8) ? l2_policy_evict_first() : pol_keep;
+      // B streams (evict_first) whenever A is the resident operand: all
+      // block-rows (A pinned) or row-groups larger than the default
+      const uint64_t pol_b = (split_pol && !p.n_fastest && p.group_m > kGroupM) ? l2_policy_evict_first()
+                                                                                : pol_keep;
       int stage = 0;
       uint32_t phase = 0, pc = 0;
       for (;;) {
@@ -809,18 +820,38 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
     p.tile_ctr = g_ring[dev].load(std::memory_order_acquire) + (size_t)slot * 32;  // one 128 B line per slot
   }
   {
-    // only when the other operand does not fit: with both small, or both
-    // large, the kGroupM groups were as fast or faster (C1 -4 %, C5 -1 %;
-    // gate/up forward +4.5 %, dW_gate/up +5 %: scripts/gemm_raster_ab.py)
-    constexpr double kResident = 48.0 * (1 << 20), kStreamed = 96.0 * (1 << 20);
+    // Raster (DRAM traffic; scripts/gemm_traffic_probe.py,
+    // scripts/gemm_raster_policy.py).  Measured per launch, bf16 out, 10 % fallback:
+    // * the smaller operand fits the L2's effective evict_last capacity (<= 56
+    //   MB) and the other does not: pin it (bm over all block-rows keeps A
+    //   resident, bn fastest keeps B) and stream the other once -- gate/up
+    //   forward 0.22 GB read (0.98 GB with groups of 8), down forward 0.36 GB (0.60);
+    // * A moderately large (<= 112 MB) and B larger: row-groups of A sized to ~40
+    //   MB, B streamed evict_first once per group -- C5 0.98 GB (2.0 GB with groups
+    //   of 8; pinning all 64 MB of A read 3.4 GB: evict_last does not hold it);
+    // * both operands small: bn fastest (C1 4096^3 +4..15 % over groups of 8);
+    // * else groups of kGroupM block-rows with the default policy (the dX GEMM:
+    //   1.5 GB; larger groups with B evict_first read 2.4 GB -- B panels are
+    //   re-read by CTAs that are not in lock-step).
+    // Speed is within +-4 % across rasters on the large shapes.
+    constexpr double kPin = 56.0 * (1 << 20), kPinMax = 112.0 * (1 << 20), kGroupBytes = 40.0 * (1 << 20);
     const double a_bytes = (double)p.M * (double)p.K, b_bytes = (double)p.N * (double)p.K;
     p.group_m = kGroupM;
     p.n_fastest = 0;
     if (p.diag & (1 << 19)) p.group_m = p.MB;          // diagnostics/tests: force each raster
     else if (p.diag & (1 << 20)) p.n_fastest = 1;
     else if (!(p.diag & (1 << 18))) {  // diagnostics: 1 << 18 = always kGroupM groups
-      if (a_bytes <= kResident && b_bytes > kStreamed) p.group_m = p.MB;
-      else if (b_bytes <= kResident && a_bytes > kStreamed) p.n_fastest = 1;
+      const double small = a_bytes < b_bytes ? a_bytes : b_bytes;
+      const double large = a_bytes < b_bytes ? b_bytes : a_bytes;
+      if (small <= kPin && large > kPin) {
+        if (a_bytes <= b_bytes) p.group_m = p.MB;
+        else p.n_fastest = 1;
+      } else if (large <= kPin) {
+        p.n_fastest = 1;
+      } else if (a_bytes <= kPinMax && b_bytes > a_bytes) {
+        const int g = (int)(kGroupBytes / (128.0 * (double)p.K));
+        p.group_m = g < kGroupM ? kGroupM : (g > p.MB ? p.MB : g);
+      }
     }
   }
   const int grid = p.num_tiles < gemm_num_sms() ? p.num_tiles : gemm_num_sms();
