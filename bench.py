@@ -343,19 +343,27 @@ def quant_sweep(device, hbm_peak):
 
 
 # ----------------------------------------------------------------- C4: Qwen-2.5-7B block linears
-def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
-    """BASELINE configs[3] on one GPU: the Qwen-2.5-7B transformer-block linears
-    (q, k, v, o: 3584 -> 3584/512/512/3584 as QuantLinear, q/k/v on three
-    streams; gate/up/down
-    3584 -> 18944 -> 3584 as the fused SwiGLU driver) fwd+bwd with the
-    compressed (int8 stochastic) activation contexts, 8192 tokens, bf16
-    activations, synthetic inputs with outlier channels; the attention core
-    (softmax) is not part of the path.  zero_grad + fwd + bwd + controller."""
+def qwen_block_linears(device, tokens=8192, steps=5, warmup=2, rank=0, world=1):
+    """BASELINE configs[3]: the Qwen-2.5-7B transformer-block linears (q, k, v,
+    o: 3584 -> 3584/512/512/3584 as QuantLinear, q/k/v on three streams;
+    gate/up/down 3584 -> 18944 -> 3584 as the fused SwiGLU driver) fwd+bwd with
+    the compressed (int8 stochastic) activation contexts, `tokens` tokens PER
+    RANK (weak scaling: rank r owns global rows [r T, (r+1) T), row_offset keeps
+    the SR streams global), bf16 activations, synthetic inputs with outlier
+    channels; the attention core (softmax) is not part of the path.
+    zero_grad + fwd + bwd + dW all-reduce (N > 1: NCCL, on a side stream after
+    each layer's backward; the MLP's three dW overlapped with its backward) +
+    controller on the global fallback rate (masked counts summed over ranks).
+    Timed with CUDA events, max over ranks; tokens/s = world x T / t."""
     import torch
+    import torch.distributed as dist
     from paper_2503_08040_b200 import linear
+    from paper_2503_08040_b200.dist import (allreduce_mlp_grads_overlapped, controller_step_global,
+                                            max_over_ranks)
     H, F, KV = 3584, 18944, 512
     rng = torch.Generator(device="cpu")
     rng.manual_seed(11)
+    row0 = rank * tokens
 
     def w(o, i):
         return (torch.randn(o, i, generator=rng) * 0.02).numpy()
@@ -364,10 +372,10 @@ def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
     mlp = linear.GluMlp(w(F, H), w(F, H), w(H, F), tokens, act_dtype=torch.bfloat16,
                         mid_dtype=torch.bfloat16, exact=False, layer_id_base=20, threshold_init=30.0)
     mlp.set_thresholds(30.0, 3.0)
-    x = make_activations(tokens, H, 31, device, torch.bfloat16)
-    attn = make_activations(tokens, H, 32, device, torch.bfloat16)
-    gys = {H: make_grads(tokens, H, 33, device, torch.bfloat16),
-           KV: make_grads(tokens, KV, 34, device, torch.bfloat16)}
+    x = make_activations(tokens, H, 31 + 100 * rank, device, torch.bfloat16, row_offset=row0)
+    attn = make_activations(tokens, H, 32 + 100 * rank, device, torch.bfloat16, row_offset=row0)
+    gys = {H: make_grads(tokens, H, 33 + 100 * rank, device, torch.bfloat16),
+           KV: make_grads(tokens, KV, 34 + 100 * rank, device, torch.bfloat16)}
     outs = {H: torch.empty(tokens, H, device=device, dtype=torch.bfloat16),
             KV: torch.empty(tokens, KV, device=device, dtype=torch.bfloat16)}
     gx = torch.empty(tokens, H, device=device, dtype=torch.bfloat16)
@@ -377,6 +385,16 @@ def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
     qkv_streams = [torch.cuda.Stream() for _ in range(3)]
     qkv_out = [torch.empty(tokens, o, device=device, dtype=torch.bfloat16) for o in (H, KV, KV)]
     qkv_gx = [torch.empty(tokens, H, device=device, dtype=torch.bfloat16) for _ in range(3)]
+    dp = world > 1
+    comm = torch.cuda.Stream() if dp else None
+    grads = [l.grad() for l in qkvo]  # stable device views (materialised once)
+    gu_grad, d_grad = mlp.grad_tensors()
+    works = []
+
+    def reduce_async(t, after):
+        comm.wait_stream(after)
+        with torch.cuda.stream(comm):
+            works.append(dist.all_reduce(t, op=dist.ReduceOp.SUM, async_op=True))
 
     def step(i):
         main = torch.cuda.current_stream()
@@ -384,23 +402,34 @@ def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
             st.wait_stream(main)
             with torch.cuda.stream(st):
                 l.zero_grad()
-                l.forward(x, i, out=qkv_out[n])
-                l.backward(gys[l.out_features], i, out=qkv_gx[n])
-                l.controller_step()
+                l.forward(x, i, row0, out=qkv_out[n])
+                l.backward(gys[l.out_features], i, row0, out=qkv_gx[n])
+                controller_step_global(l, world * tokens)
+            if dp:
+                reduce_async(grads[n], st)
         for st in qkv_streams:
             main.wait_stream(st)
         l = qkvo[3]
         l.zero_grad()
-        l.forward(attn, i, out=outs[H])
-        l.backward(gys[H], i, out=gx)
-        l.controller_step()
+        l.forward(attn, i, row0, out=outs[H])
+        l.backward(gys[H], i, row0, out=gx)
+        controller_step_global(l, world * tokens)
+        if dp:
+            reduce_async(grads[3], main)
         mlp.zero_grad()
-        mlp.forward(x, i, 0, out=outs[H])
-        mlp.backward(gys[H], i, 0, out=gx)
-        mlp.controller_step()
+        mlp.forward(x, i, row0, out=outs[H])
+        mlp.backward(gys[H], i, row0, out=gx)
+        if dp:
+            allreduce_mlp_grads_overlapped(mlp, gu_grad, d_grad, comm)
+        controller_step_global(mlp, world * tokens)
+        for wk in works:
+            wk.wait()
+        works.clear()
     for i in range(warmup):
         step(i)
     torch.cuda.synchronize()
+    if dp:
+        dist.barrier()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
@@ -408,12 +437,54 @@ def qwen_block_linears(device, tokens=8192, steps=5, warmup=2):
         step(warmup + i)
     e1.record(s)
     torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / steps * 1e-3
-    ops = 2 * tokens * (2 * H * H + 2 * H * KV + 3 * H * F) * 3
+    if dp:
+        dist.barrier()
+    t = max_over_ranks(e0.elapsed_time(e1) / steps * 1e-3, device)
+    ops = 2 * tokens * (2 * H * H + 2 * H * KV + 3 * H * F) * 3 * world
     rates = {f"{n}": round(l.controller_state()[0], 4) for n, l in zip("qkvo", qkvo)}
-    return {"workload": f"Qwen-2.5-7B block linears q/k/v/o + SwiGLU MLP, fwd+bwd, {tokens} tokens, 1 GPU",
-            "tokens_per_s": round(tokens / t, 1), "ms_per_step": round(t * 1e3, 3),
+    return {"workload": f"Qwen-2.5-7B block linears q/k/v/o + SwiGLU MLP, fwd+bwd, {tokens} tokens per GPU, "
+                        f"{world} GPU(s), token-sharded, dW all-reduce + global-rate controller",
+            "tokens_per_s": round(world * tokens / t, 1), "ms_per_step": round(t * 1e3, 3),
+            "n_gpus": world, "scaling": "weak",
             "gemm_TOPS_effective": round(ops / t / 1e12, 1), "fallback_rates_qkvo": rates}
+
+
+def c5_fallback_gemm(device, rank=0, world=1, M=8192, rate=0.10, iters=10, warm=3):
+    """BASELINE configs[4] across ranks: the fallback GEMM on the Llama-3.1-70B
+    MLP shape (K 8192 -> N 28672), token-sharded forward (each rank M rows of
+    its own tokens, weights replicated, no communication: weak scaling, global
+    M = world x M), topk fallback at `rate`, FMA epilogue, bf16 out.  CUDA
+    events, max over ranks; TOPS = world x 2MNK / t."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_08040_b200 import fbq
+    from paper_2503_08040_b200.dist import max_over_ranks
+    N, K = 28672, 8192
+    x = make_activations(M, K, 12 + rank, device, torch.bfloat16, row_offset=rank * M)
+    wq = fbq.transpose(fbq.quantize_rtn(torch.randn(N, K, device=device, generator=torch.Generator(
+        device=device).manual_seed(5)) * 0.02))
+    fa = fbq.fallback_quantize(x, fbq.mask_topk(fbq.score_blocks(x), rate))
+    y = torch.empty(M, N, device=device, dtype=torch.bfloat16)
+    for _ in range(warm):
+        fbq.fallback_gemm(fa, wq, out=y, exact=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fbq.fallback_gemm(fa, wq, out=y, exact=False)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = max_over_ranks(e0.elapsed_time(e1) / iters * 1e-3, device)
+    del x, wq, fa, y
+    torch.cuda.empty_cache()
+    return {"workload": f"C5 fallback GEMM {M}x{N}x{K} per GPU ({rate:.0%} topk fallback, FMA epilogue, bf16 "
+                        f"out), {world} GPU(s), token-sharded forward, no communication",
+            "global_M": world * M, "n_gpus": world, "scaling": "weak",
+            "TOPS_effective": round(world * 2 * M * N * K / t / 1e12, 1), "ms": round(t * 1e3, 3)}
 
 
 # ----------------------------------------------------------------- GEMM sweep
@@ -593,10 +664,17 @@ def run_ours(args, rank, world, local):
     from paper_2503_08040_b200.dist import (allreduce_mlp_grads_overlapped, controller_step_global,
                                             global_quantile, max_over_ranks)
 
+    # FBQ_BENCH_DEVICE / FBQ_DIST_BACKEND: test hooks only (two ranks on one
+    # GPU over gloo -- NCCL needs one GPU per rank); the driver's runs use NCCL
+    local = int(os.environ.get("FBQ_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("FBQ_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     T = args.tokens
     row_offset = rank * T  # weak scaling: rank r owns global token rows [r*T, (r+1)*T)
 
@@ -709,6 +787,19 @@ def run_ours(args, rank, world, local):
         except Exception:
             traffic = None
 
+    # C4 / C5 token-sharded across all ranks (N > 1; the sweeps below are
+    # single-GPU and run on rank 0 only)
+    c4_dp = c5_dp = None
+    if world > 1 and not args.no_sweep:
+        try:
+            c4_dp = qwen_block_linears(device, rank=rank, world=world)
+        except Exception as ex:  # pragma: no cover
+            c4_dp = {"error": str(ex)[:200]}
+        try:
+            c5_dp = c5_fallback_gemm(device, rank=rank, world=world)
+        except Exception as ex:  # pragma: no cover
+            c5_dp = {"error": str(ex)[:200]}
+
     result = None
     if rank == 0:
         # ---- e2e through the host-buffer C ABI (fbq_mlp_step_host), N=1 semantics per rank
@@ -761,7 +852,7 @@ def run_ours(args, rank, world, local):
             except Exception as ex:  # pragma: no cover
                 exact = {"error": str(ex)[:200]}
         sweep = qsweep = c4 = None
-        if not args.no_sweep:
+        if not args.no_sweep and world == 1:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
                 qsweep = quant_sweep(device, peaks.get("hbm_gbs", 6522.1))
             except Exception as ex:  # pragma: no cover
@@ -770,6 +861,10 @@ def run_ours(args, rank, world, local):
                 sweep = gemm_sweep(device)
             except Exception as ex:  # pragma: no cover
                 sweep = {"error": str(ex)[:200]}
+            try:
+                c5_dp = c5_fallback_gemm(device)
+            except Exception as ex:  # pragma: no cover
+                c5_dp = {"error": str(ex)[:200]}
             try:
                 c4 = qwen_block_linears(device)
                 # the strong-scaling base of SURVEY 8d (T = 32768 on one GPU)
@@ -822,7 +917,8 @@ def run_ours(args, rank, world, local):
             "exact_mode": exact,
             "gemm_sweep": sweep,
             "quant_sweep": qsweep,
-            "qwen_block_c4": c4,
+            "qwen_block_c4": c4 if world == 1 else c4_dp,
+            "c5_fallback_gemm_dp": c5_dp,
         }
         print(json.dumps(result), flush=True)
     if world > 1:
