@@ -173,6 +173,20 @@ int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols,
                           int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
                           int64_t row_offset, float* g_out, int exact_math, fbq_stream_t stream);
 
+/* mask_threshold (policy.cpp:73-80): bit i of mask_bits = scores[i] > threshold
+ * (strict, double); *masked_count (may be NULL) = flagged blocks (mask_rate
+ * numerator, policy.cpp:82-87).  Writes every word; nothing to pre-zero. */
+int fbq_cuda_mask_threshold(const double* scores, int64_t n, double threshold, uint32_t* mask_bits,
+                            int32_t* masked_count, fbq_stream_t stream);
+
+/* controller_update (policy.cpp:97-109) with the observed rate in device memory */
+int fbq_cuda_controller_update_rate(double* theta_dev, const double* observed_rate_dev, double r_min,
+                                    double r_max, double alpha, double* last_rate_dev,
+                                    fbq_stream_t stream);
+
+/* QuantLinearLayer::apply_sgd (trainsim.cpp:137-143): w[i] -= float(lr * double(grad[i])) */
+int fbq_cuda_sgd_update(float* w, const float* grad, int64_t n, double lr, fbq_stream_t stream);
+
 /* controller_update (policy.cpp:97-109) on device: rate = *masked_count /
  * n_blocks; *theta_dev /= alpha if rate < r_min, *= alpha if rate > r_max;
  * *last_rate_dev = rate (may be NULL). */

@@ -150,8 +150,14 @@ int fbq_linear_controller_step_blocks(void* linear, int64_t blocks, fbq_stream_t
  * zero before returning the pointer. */
 int fbq_linear_zero_grad(void* linear, fbq_stream_t stream);
 float* fbq_linear_grad_ptr(void* linear);
-/* last observed fallback rate and the current threshold (synchronous read) */
+/* last observed fallback rate (of the last forward, trainsim.cpp:93) and the
+ * current threshold (synchronous read) */
 int fbq_linear_get_controller(void* linear, double* last_rate, double* threshold);
+/* QuantLinearLayer::apply_sgd (trainsim.cpp:137-143) on the device master weight */
+int fbq_linear_apply_sgd(void* linear, double lr, fbq_stream_t stream);
+/* synchronous host copies of the fp32 master weight / dW (out x in) */
+int fbq_linear_get_weight(void* linear, float* w_host);
+int fbq_linear_get_grad(void* linear, float* g_host);
 
 /* ---- wire formats (host/io.cpp) ----
  * .fmat: the reference's dense fp32 matrix file (matrix.cpp:75-142), byte-

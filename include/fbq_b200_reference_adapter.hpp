@@ -16,6 +16,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -27,7 +28,9 @@
 #include "fbq/policy.hpp"
 #include "fbq/quant.hpp"
 #include "fbq/rng.hpp"
+#include "fbq/trainsim.hpp"
 #include "fbq_b200.h"
+#include "fbq_b200_host.h"
 
 namespace fbq::b200 {
 
@@ -184,6 +187,7 @@ inline DenseMatrix run_gemm(const QuantizedTensor& qa, const QuantizedTensor& qb
       qb.bits.bits != 8 || !(qa.geometry == GroupGeometry(128, 128)) ||
       !(qb.geometry == GroupGeometry(128, 128)))
     throw std::invalid_argument("block shape/geometry unsupported on B200 (128^3, 8 bits)");
+  check(fbq_cuda_init(), "fbq_cuda_init");  // once per device (idempotent): dynamic tile scheduler
   const int64_t M = qa.rows, K = qa.cols, N = qb.cols;
   const int64_t lda = ld16(K), ldb = ld16(N);
   Dev a(M * lda + 16), b(K * ldb + 16), sa(qa.scales.size() * 4 + 4), sb(qb.scales.size() * 4 + 4),
@@ -251,5 +255,245 @@ inline std::vector<double> score_blocks_absmax(const DenseMatrix& m, const Group
   const std::vector<float> f = detail::download_f32(amax, nb);
   return std::vector<double>(f.begin(), f.end());
 }
+
+// ------------------------------------------------------------------ quant.hpp:68-77
+namespace detail {
+inline DenseMatrix run_dequant(const QuantizedTensor& q, const FallbackTensor* fb) {
+  if (!(q.geometry == GroupGeometry(128, 128)) || q.bits.bits != 8)
+    throw std::invalid_argument("geometry/bit-width unsupported on B200 (128x128 blocks, 8 bits)");
+  const int64_t r = q.rows, c = q.cols, ldq = ld16(c);
+  const int64_t gc = cdiv(c, 128), nb = cdiv(r, 128) * gc;
+  Dev codes(r * ldq + 16), scales(nb * 4 + 4), out(r * c * 4 + 4);
+  upload_codes(q.codes, r, c, ldq, codes);
+  check(fbq_memcpy_h2d(scales.p, q.scales.data(), q.scales.size() * 4), "upload");
+  std::unique_ptr<Dev> bits, res, rs;
+  if (fb) {
+    if (fb->mask.size() != static_cast<size_t>(nb))
+      throw std::invalid_argument("fallback mask does not match the block grid");
+    std::vector<uint32_t> hb(static_cast<size_t>(cdiv(nb, 32)), 0);
+    std::vector<int16_t> dense(static_cast<size_t>(r * c), 0);
+    std::vector<float> hs(static_cast<size_t>(nb), 0.0f);
+    for (int64_t i = 0; i < nb; ++i) {
+      if (!fb->mask[i]) continue;
+      hb[i >> 5] |= 1u << (i & 31);
+      const auto& blk = fb->residuals[fb->residual_index[i]];
+      const int64_t bi = i / gc, bj = i % gc;
+      const int64_t er = std::min<int64_t>(128, r - bi * 128), ec = std::min<int64_t>(128, c - bj * 128);
+      for (int64_t y = 0; y < er; ++y)
+        for (int64_t x = 0; x < ec; ++x) dense[(bi * 128 + y) * c + bj * 128 + x] = blk.codes[y * ec + x];
+      hs[i] = blk.scale;
+    }
+    bits = std::make_unique<Dev>(hb.size() * 4);
+    res = std::make_unique<Dev>(r * ldq + 16);
+    rs = std::make_unique<Dev>(hs.size() * 4);
+    check(fbq_memcpy_h2d(bits->p, hb.data(), hb.size() * 4), "upload");
+    upload_codes(dense, r, c, ldq, *res);
+    check(fbq_memcpy_h2d(rs->p, hs.data(), hs.size() * 4), "upload");
+  }
+  check(fbq_cuda_dequantize(codes.as<int8_t>(), ldq, scales.as<float>(), fb ? bits->as<uint32_t>() : nullptr,
+                            fb ? res->as<int8_t>() : nullptr, fb ? rs->as<float>() : nullptr, r, c,
+                            out.as<float>(), c, nullptr),
+        "dequantize");
+  return DenseMatrix(r, c, download_f32(out, static_cast<size_t>(r * c)));
+}
+}  // namespace detail
+
+// quant.cpp:86-104
+inline DenseMatrix dequantize(const QuantizedTensor& q) { return detail::run_dequant(q, nullptr); }
+
+// quant.cpp:178-202
+inline DenseMatrix dequantize_fallback(const FallbackTensor& f) { return detail::run_dequant(f.primary, &f); }
+
+// quant.cpp:106-126.  The B200 path never materialises a transpose: the GEMM
+// reads the same int8 plane K- or MN-major through a descriptor bit (quantize
+// W once; dgrad/wgrad read it transposed).  For value-API callers this is the
+// reference's data movement on the host: codes and the scale grid transposed.
+inline QuantizedTensor transpose(const QuantizedTensor& q) {
+  if (!(q.geometry == GroupGeometry(128, 128)) || q.bits.bits != 8)
+    throw std::invalid_argument("geometry/bit-width unsupported on B200 (128x128 blocks, 8 bits)");
+  const int64_t r = q.rows, c = q.cols, gr = detail::cdiv(r, 128), gc = detail::cdiv(c, 128);
+  std::vector<int16_t> codes(static_cast<size_t>(r * c));
+  for (int64_t i = 0; i < r; ++i)
+    for (int64_t j = 0; j < c; ++j) codes[j * r + i] = q.codes[i * c + j];
+  std::vector<float> scales(static_cast<size_t>(gr * gc));
+  for (int64_t i = 0; i < gr; ++i)
+    for (int64_t j = 0; j < gc; ++j) scales[j * gr + i] = q.scales[i * gc + j];
+  return detail::make_qt(c, r, std::move(codes), std::move(scales));
+}
+
+// gemm.cpp:200-203: any tile dividing the block is bit-identical to the block
+// GEMM (integer tile products are associative; the tensor core always forms
+// the full 128-deep block product with K = 32 sub-steps)
+inline DenseMatrix tiled_block_gemm(const QuantizedTensor& qa, const QuantizedTensor& qb,
+                                    const GemmBlockShape& shape, const TileShape& tile) {
+  if (shape.m_g % tile.m_t || shape.n_g % tile.n_t || shape.k_g % tile.k_t)
+    throw std::invalid_argument("tile sides must divide the block sides");  // gemm.cpp:104-107
+  return detail::run_gemm(qa, qb, shape, nullptr);
+}
+
+// ------------------------------------------------------------------ policy.hpp:30-47
+namespace detail {
+inline std::vector<uint8_t> bits_to_mask(const std::vector<uint32_t>& bits, size_t n) {
+  std::vector<uint8_t> m(n);
+  for (size_t i = 0; i < n; ++i) m[i] = static_cast<uint8_t>((bits[i >> 5] >> (i & 31)) & 1u);
+  return m;
+}
+}  // namespace detail
+
+// policy.cpp:73-80 (strict >) on the device
+inline std::vector<uint8_t> mask_threshold(const std::vector<double>& scores, double threshold) {
+  if (!(threshold > 0.0)) throw std::invalid_argument("threshold must be > 0");  // policy.cpp:74
+  const int64_t n = static_cast<int64_t>(scores.size());
+  if (n == 0) return {};
+  detail::Dev s(n * 8), bits(detail::cdiv(n, 32) * 4);
+  detail::check(fbq_memcpy_h2d(s.p, scores.data(), n * 8), "upload");
+  detail::check(fbq_cuda_mask_threshold(s.as<double>(), n, threshold, bits.as<uint32_t>(), nullptr, nullptr),
+                "mask_threshold");
+  std::vector<uint32_t> hb(static_cast<size_t>(detail::cdiv(n, 32)));
+  detail::check(fbq_memcpy_d2h(hb.data(), bits.p, hb.size() * 4), "download");
+  return detail::bits_to_mask(hb, static_cast<size_t>(n));
+}
+
+// policy.cpp:56-71 on the device (one-CTA radix select, ties to the lower
+// index).  The device keys are fp32 scores: AbsMax scores are fp32 block
+// maxima widened to double (policy.cpp:18-27), so this is exact for them; other
+// criteria (L1 / L1Rel doubles) throw "unsupported on B200".
+inline std::vector<uint8_t> mask_topk(const std::vector<double>& scores, double rate) {
+  if (!(rate >= 0.0 && rate <= 1.0)) throw std::invalid_argument("rate must be in [0, 1]");  // policy.cpp:57
+  const int64_t n = static_cast<int64_t>(scores.size());
+  if (n == 0) return {};
+  std::vector<float> f(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    f[i] = static_cast<float>(scores[i]);
+    if (static_cast<double>(f[i]) != scores[i] || !(scores[i] >= 0.0))
+      throw std::invalid_argument("mask_topk: non-fp32 or negative scores unsupported on B200 (AbsMax only)");
+  }
+  detail::Dev s(n * 4), bits(detail::cdiv(n, 32) * 4);
+  detail::check(fbq_memcpy_h2d(s.p, f.data(), n * 4), "upload");
+  detail::check(fbq_cuda_mask_topk(s.as<float>(), n, rate, bits.as<uint32_t>(), nullptr, nullptr), "mask_topk");
+  std::vector<uint32_t> hb(static_cast<size_t>(detail::cdiv(n, 32)));
+  detail::check(fbq_memcpy_d2h(hb.data(), bits.p, hb.size() * 4), "download");
+  return detail::bits_to_mask(hb, static_cast<size_t>(n));
+}
+
+// policy.cpp:82-87 (flagged / blocks: a host count over the caller's host mask;
+// on the device the same count comes out of K1 / the mask kernels)
+inline double mask_rate(const std::vector<uint8_t>& mask) {
+  if (mask.empty()) return 0.0;
+  size_t k = 0;
+  for (uint8_t m : mask) k += m ? 1 : 0;
+  return static_cast<double>(k) / static_cast<double>(mask.size());
+}
+
+// policy.cpp:97-109 (Algorithm 2) through the device controller
+inline FallbackThresholdState controller_update(FallbackThresholdState state, double observed_rate,
+                                                const ControllerConfig& cfg) {
+  if (!(observed_rate >= 0.0 && observed_rate <= 1.0))
+    throw std::invalid_argument("observed rate must be in [0, 1]");  // policy.cpp:98-100
+  detail::Dev d(3 * sizeof(double));
+  const double h[3] = {state.threshold, observed_rate, 0.0};
+  detail::check(fbq_memcpy_h2d(d.p, h, sizeof(h)), "upload");
+  detail::check(fbq_cuda_controller_update_rate(d.as<double>(), d.as<double>() + 1, cfg.r_min, cfg.r_max,
+                                                cfg.alpha, d.as<double>() + 2, nullptr),
+                "controller_update");
+  double o[3];
+  detail::check(fbq_memcpy_d2h(o, d.p, sizeof(o)), "download");
+  FallbackThresholdState out;
+  out.threshold = o[0];
+  out.last_rate = o[2];
+  return out;
+}
+
+// ------------------------------------------------------------------ trainsim.hpp:38-73
+// QuantLinearLayer on the device driver (fbq_linear_*): the same constructor
+// arguments and methods; forward/backward take and return host DenseMatrix
+// values like the reference (the e2e value API: host -> device -> host).  The
+// B200 path covers QuantConfig{block = 128, 8-bit x / w / grad / context,
+// not passthrough}; anything else throws std::invalid_argument("...unsupported
+// on B200...") -- in particular the reference's DEFAULT block = 32.
+// max_tokens sizes the device workspaces (forward rows beyond it throw).
+class QuantLinearLayer {
+ public:
+  QuantLinearLayer(std::string name, int layer_id, DenseMatrix weight, QuantConfig cfg,
+                   index_t max_tokens = 4096)
+      : name_(std::move(name)), out_(weight.rows()), in_(weight.cols()) {
+    if (cfg.passthrough || cfg.block != 128 || cfg.bits_x != 8 || cfg.bits_w != 8 || cfg.bits_grad != 8 ||
+        cfg.context_bits != 8)
+      throw std::invalid_argument(
+          "QuantConfig unsupported on B200 (needs block = 128, 8-bit x/w/grad/context, not passthrough)");
+    fbq_linear_config c;
+    fbq_linear_default_config(&c);
+    c.in_features = in_;
+    c.out_features = out_;
+    c.max_tokens = max_tokens;
+    c.act_dtype = FBQ_F32;
+    c.epilogue = FBQ_EPI_EXACT;  // bit-exact with the reference
+    c.layer_id = layer_id;
+    c.seed = cfg.seed;
+    c.threshold_init = cfg.threshold_init;
+    c.r_min = cfg.controller.r_min;
+    c.r_max = cfg.controller.r_max;
+    c.alpha = cfg.controller.alpha;
+    c.fallback_mode = cfg.fallback_mode == FallbackMode::Threshold ? 0
+                      : cfg.fallback_mode == FallbackMode::FixedRate ? 1 : 2;
+    c.fixed_rate = cfg.fixed_rate;
+    h_ = fbq_linear_create(&c, weight.data());
+    if (!h_) throw std::invalid_argument(std::string("fbq_linear_create: ") + fbq_host_last_error());
+    max_tokens_ = max_tokens;
+  }
+  ~QuantLinearLayer() {
+    if (h_) fbq_linear_destroy(h_);
+  }
+  QuantLinearLayer(const QuantLinearLayer&) = delete;
+  QuantLinearLayer& operator=(const QuantLinearLayer&) = delete;
+
+  DenseMatrix forward(const DenseMatrix& x, int step) {
+    if (x.cols() != in_) throw std::invalid_argument("forward: input width != in_features");
+    return run(x, out_, step, true);
+  }
+  // returns grad_x, accumulates grad_w (trainsim.cpp:106-127)
+  DenseMatrix backward(const DenseMatrix& grad_y, int step) {
+    if (grad_y.cols() != out_) throw std::invalid_argument("backward: grad width != out_features");
+    if (!has_ctx_) throw std::logic_error("backward without a forward context");  // trainsim.cpp:108
+    return run(grad_y, in_, step, false);
+  }
+  const std::string& name() const { return name_; }
+  DenseMatrix weight() const { return host_copy(fbq_linear_get_weight); }
+  DenseMatrix grad_weight() const { return host_copy(fbq_linear_get_grad); }
+  double last_fallback_rate() const { return controller_state().first; }
+  double threshold() const { return controller_state().second; }
+  bool holds_full_precision_context() const { return false; }  // the int8 SR context only
+  void controller_step() { detail::check(fbq_linear_controller_step(h_, nullptr), "controller_step"); }
+  void zero_grad() { detail::check(fbq_linear_zero_grad(h_, nullptr), "zero_grad"); }
+  void apply_sgd(double lr) { detail::check(fbq_linear_apply_sgd(h_, lr, nullptr), "apply_sgd"); }
+
+ private:
+  DenseMatrix run(const DenseMatrix& in, int64_t out_cols, int step, bool fwd) {
+    const int64_t t = in.rows();
+    if (t > max_tokens_) throw std::invalid_argument("tokens exceed max_tokens of the B200 layer");
+    detail::Dev di(t * in.cols() * 4 + 4), dout(t * out_cols * 4 + 4);
+    detail::upload(in, di);
+    const int st = fwd ? fbq_linear_forward_device(h_, di.p, t, 0, step, dout.p, nullptr)
+                       : fbq_linear_backward_device(h_, di.p, t, 0, step, dout.p, nullptr);
+    detail::check(st, fwd ? "forward" : "backward");
+    if (fwd) has_ctx_ = true;
+    return DenseMatrix(t, out_cols, detail::download_f32(dout, static_cast<size_t>(t * out_cols)));
+  }
+  DenseMatrix host_copy(int (*fn)(void*, float*)) const {
+    std::vector<float> v(static_cast<size_t>(out_ * in_));
+    detail::check(fn(h_, v.data()), "copy");
+    return DenseMatrix(out_, in_, std::move(v));
+  }
+  std::pair<double, double> controller_state() const {
+    double r = 0.0, th = 0.0;
+    detail::check(fbq_linear_get_controller(h_, &r, &th), "get_controller");
+    return {r, th};
+  }
+  std::string name_;
+  int64_t out_, in_;
+  index_t max_tokens_ = 0;
+  void* h_ = nullptr;
+  bool has_ctx_ = false;
+};
 
 }  // namespace fbq::b200

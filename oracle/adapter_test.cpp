@@ -10,6 +10,7 @@
 #include "fbq/policy.hpp"
 #include "fbq/quant.hpp"
 #include "fbq/rng.hpp"
+#include "fbq/trainsim.hpp"
 #include "fbq_b200_reference_adapter.hpp"
 
 using namespace fbq;
@@ -74,6 +75,90 @@ int main() {
           "block_quant_gemm");
     check(same_dense(fallback_gemm(fr, qb, shape), b200::fallback_gemm(fr, qb, shape)),
           "fallback_gemm");
+  }
+  // ---- dequantize / dequantize_fallback / transpose / tiled_block_gemm (quant.hpp:68-77, gemm.hpp:52-53)
+  {
+    const DenseMatrix x = randm(300, 270, 77, 1.0f, 5);
+    const QuantizedTensor q = quantize_rtn(x, g, b8);
+    check(same_dense(dequantize(q), b200::dequantize(q)), "dequantize");
+    const auto mask = mask_topk(score_blocks(x, g, b8, FallbackCriterion::AbsMax), 0.5);
+    const FallbackTensor f = fallback_quantize(x, g, b8, mask);
+    check(same_dense(dequantize_fallback(f), b200::dequantize_fallback(f)), "dequantize_fallback");
+    check(same_qt(transpose(q), b200::transpose(q)), "transpose");
+    const QuantizedTensor qw = quantize_rtn(randm(270, 200, 78, 0.05f, -1), g, b8);
+    for (const TileShape& t : {TileShape(128, 128, 128), TileShape(64, 32, 16), TileShape(1, 128, 8)})
+      check(same_dense(tiled_block_gemm(q, qw, shape, t), b200::tiled_block_gemm(q, qw, shape, t)),
+            "tiled_block_gemm");
+    bool threw = false;
+    try {
+      b200::tiled_block_gemm(q, qw, shape, TileShape(48, 128, 128));
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    check(threw, "tiled_block_gemm bad tile");
+  }
+  // ---- policy: mask_threshold / mask_topk / mask_rate / controller_update (policy.hpp:30-47)
+  {
+    const DenseMatrix x = randm(640, 1152, 91, 1.0f, 300);
+    const auto scores = score_blocks(x, g, b8, FallbackCriterion::AbsMax);
+    for (double th : {0.5, 2.0, 3.5, 1e9})
+      check(mask_threshold(scores, th) == b200::mask_threshold(scores, th), "mask_threshold");
+    for (double r : {0.0, 0.01, 0.2, 0.5, 1.0})
+      check(mask_topk(scores, r) == b200::mask_topk(scores, r), "mask_topk");
+    std::vector<double> tied(91);
+    for (size_t i = 0; i < tied.size(); ++i) tied[i] = static_cast<double>((i * 7) % 4) * 0.5;
+    for (double r : {0.1, 0.33, 0.9}) check(mask_topk(tied, r) == b200::mask_topk(tied, r), "mask_topk ties");
+    const auto m = mask_topk(scores, 0.2);
+    check(mask_rate(m) == b200::mask_rate(m), "mask_rate");
+    const ControllerConfig cc(0.1, 0.3, 1.3);
+    for (double obs : {0.05, 0.2, 0.35}) {
+      FallbackThresholdState st;
+      st.threshold = 2.5;
+      const auto a = controller_update(st, obs, cc), bb = b200::controller_update(st, obs, cc);
+      check(a.threshold == bb.threshold && a.last_rate == bb.last_rate, "controller_update");
+    }
+  }
+  // ---- QuantLinearLayer (trainsim.hpp:38-73) over steps with the controller and SGD
+  {
+    QuantConfig cfg;
+    cfg.block = 128;
+    cfg.threshold_init = 3.0;
+    const DenseMatrix w = randm(384, 256, 55, 0.05f, -1);
+    QuantLinearLayer ref("fc", 3, w, cfg);
+    b200::QuantLinearLayer gpu("fc", 3, w, cfg, 512);
+    bool ok = true;
+    for (int step = 0; step < 3 && ok; ++step) {
+      const DenseMatrix x = randm(300, 256, 60 + step, 1.0f, 7);
+      const DenseMatrix gy = randm(300, 384, 70 + step, 1e-3f, -1);
+      ref.zero_grad();
+      gpu.zero_grad();
+      ok = ok && same_dense(ref.forward(x, step), gpu.forward(x, step));
+      ok = ok && ref.last_fallback_rate() == gpu.last_fallback_rate();
+      ok = ok && same_dense(ref.backward(gy, step), gpu.backward(gy, step));
+      ok = ok && same_dense(ref.grad_weight(), gpu.grad_weight());
+      ref.controller_step();
+      gpu.controller_step();
+      ok = ok && ref.threshold() == gpu.threshold();
+      ref.apply_sgd(0.5);
+      gpu.apply_sgd(0.5);
+      ok = ok && same_dense(ref.weight(), gpu.weight());
+    }
+    check(ok, "QuantLinearLayer fwd/bwd/grad/controller/sgd over 3 steps");
+    bool threw = false;
+    try {
+      b200::QuantLinearLayer bad("fc", 0, w, QuantConfig{});  // reference default block = 32
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    check(threw, "QuantLinearLayer block = 32 unsupported");
+    threw = false;
+    try {
+      b200::QuantLinearLayer fresh("fc", 0, w, cfg, 512);
+      fresh.backward(randm(10, 384, 1, 1.0f, -1), 0);
+    } catch (const std::logic_error&) {
+      threw = true;
+    }
+    check(threw, "backward without context");
   }
   // error behaviour mirrors the reference
   bool threw = false;

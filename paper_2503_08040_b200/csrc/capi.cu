@@ -8,6 +8,14 @@
 #include "gemm_kernel.cuh"
 #include "quant_kernels.cuh"
 
+namespace fbq {
+cudaError_t launch_threshold(const double* scores, int64_t n, double theta, uint32_t* mask_bits,
+                             int32_t* count, cudaStream_t s);
+cudaError_t launch_controller_rate(double* theta, const double* rate, double r_min, double r_max,
+                                   double alpha, double* last_rate, cudaStream_t s);
+cudaError_t launch_sgd(float* w, const float* g, int64_t n, double lr, cudaStream_t s);
+}  // namespace fbq
+
 namespace {
 
 thread_local int g_last_cuda = 0;
@@ -265,6 +273,29 @@ int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* ma
   if (k > n) k = n;
   return cuda_status(fbq::launch_topk(scores, n, k, mask_bits, masked_count,
                                       reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_mask_threshold(const double* scores, int64_t n, double threshold, uint32_t* mask_bits,
+                            int32_t* masked_count, fbq_stream_t stream) {
+  if (n < 0 || n >= (1ll << 31)) return FBQ_ERR_SHAPE;
+  if (n == 0) return FBQ_OK;
+  if (!scores || !mask_bits) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_threshold(scores, n, threshold, mask_bits, masked_count,
+                                           reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_controller_update_rate(double* theta_dev, const double* observed_rate_dev, double r_min,
+                                    double r_max, double alpha, double* last_rate_dev,
+                                    fbq_stream_t stream) {
+  if (!theta_dev || !observed_rate_dev) return FBQ_ERR_ARG;
+  if (!(0.0 <= r_min && r_min < r_max && r_max <= 1.0) || !(alpha > 1.0)) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_controller_rate(theta_dev, observed_rate_dev, r_min, r_max, alpha,
+                                                 last_rate_dev, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_sgd_update(float* w, const float* grad, int64_t n, double lr, fbq_stream_t stream) {
+  if (n < 0 || (n > 0 && (!w || !grad))) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_sgd(w, grad, n, lr, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int fbq_cuda_quantize_rtn(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,

@@ -643,10 +643,12 @@ struct QuantLinear {
 
   void controller(cudaStream_t s, int64_t blocks = 0) {
     if (c.fallback_mode != 0) return;  // trainsim.cpp:129-133: Threshold mode only
+    ctl_blocks = blocks > 0 ? blocks : 0;
     FBQ_TRY(fbq_cuda_controller_update(theta.as<double>(), count.as<int32_t>(),
                                        blocks > 0 ? blocks : last_blocks, c.r_min, c.r_max,
                                        c.alpha, rate.as<double>(), s));
   }
+  int64_t ctl_blocks = 0;  // global block count of the last data-parallel controller step
 };
 
 thread_local std::string g_host_err;
@@ -906,6 +908,32 @@ int fbq_linear_controller_step_blocks(void* l, int64_t blocks, fbq_stream_t stre
 int32_t* fbq_linear_count_ptr(void* l) {
   return l ? static_cast<QuantLinear*>(l)->count.as<int32_t>() : nullptr;
 }
+int fbq_linear_apply_sgd(void* l, double lr, fbq_stream_t stream) {
+  if (!l) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* q = static_cast<QuantLinear*>(l);
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (q->grad_zero_pending) return;  // grad is (pending) zero: w unchanged
+    FBQ_TRY(fbq_cuda_sgd_update(q->w.as<float>(), q->g.as<float>(), q->Out * q->In, lr, s));
+  });
+}
+int fbq_linear_get_weight(void* l, float* w_host) {
+  if (!l || !w_host) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* q = static_cast<QuantLinear*>(l);
+    CU_TRY(cudaDeviceSynchronize());
+    CU_TRY(cudaMemcpy(w_host, q->w.p, q->Out * q->In * 4, cudaMemcpyDeviceToHost));
+  });
+}
+int fbq_linear_get_grad(void* l, float* g_host) {
+  if (!l || !g_host) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* q = static_cast<QuantLinear*>(l);
+    CU_TRY(cudaDeviceSynchronize());
+    if (q->grad_zero_pending) std::fill(g_host, g_host + q->Out * q->In, 0.0f);
+    else CU_TRY(cudaMemcpy(g_host, q->g.p, q->Out * q->In * 4, cudaMemcpyDeviceToHost));
+  });
+}
 int fbq_linear_zero_grad(void* l, fbq_stream_t stream) {
   if (!l) return FBQ_ERR_ARG;
   (void)stream;
@@ -927,8 +955,18 @@ int fbq_linear_get_controller(void* l, double* last_rate, double* threshold) {
   if (!l || !last_rate || !threshold) return FBQ_ERR_ARG;
   return guarded([&] {
     auto* q = static_cast<QuantLinear*>(l);
-    if (q->c.fallback_mode == 0) CU_TRY(cudaMemcpy(last_rate, q->rate.p, sizeof(double), cudaMemcpyDeviceToHost));
-    else *last_rate = q->last_fixed_rate;
+    CU_TRY(cudaDeviceSynchronize());
+    if (q->c.fallback_mode == 0) {
+      // the observed rate of the LAST FORWARD (trainsim.cpp:93: last_rate_ is set
+      // in forward, before any controller step): masked / blocks -- global
+      // counts and blocks after a data-parallel controller step
+      int32_t cnt = 0;
+      CU_TRY(cudaMemcpy(&cnt, q->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      const int64_t b = q->ctl_blocks > 0 ? q->ctl_blocks : q->last_blocks;
+      *last_rate = b > 0 ? (double)cnt / (double)b : 0.0;
+    } else {
+      *last_rate = q->last_fixed_rate;
+    }
     CU_TRY(cudaMemcpy(threshold, q->theta.p, sizeof(double), cudaMemcpyDeviceToHost));
   });
 }

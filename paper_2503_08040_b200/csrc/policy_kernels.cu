@@ -68,4 +68,66 @@ cudaError_t launch_topk(const float* scores, int64_t n, int64_t k, uint32_t* mas
   return cudaGetLastError();
 }
 
+// mask_threshold (policy.cpp:73-80): bit i = scores[i] > theta (strict, in
+// double), packed 32 per word by warp ballots; one CTA also sums the flagged
+// blocks (the mask_rate numerator, policy.cpp:82-87) -- deterministic, nothing
+// to pre-zero.
+__global__ void __launch_bounds__(kTopkThreads)
+fbq_threshold_kernel(const double* scores, int64_t n, double theta, uint32_t* mask_bits, int32_t* count) {
+  __shared__ int32_t s_count[kTopkThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t words = (n + 31) / 32;
+  int32_t c = 0;
+  for (int64_t w = warp; w < words; w += kTopkThreads / 32) {
+    const int64_t i = w * 32 + lane;
+    const uint32_t bits = __ballot_sync(0xffffffffu, i < n && scores[i] > theta);
+    if (lane == 0) {
+      mask_bits[w] = bits;
+      c += __popc(bits);
+    }
+  }
+  if (lane == 0) s_count[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0 && count) {
+    int32_t t = 0;
+    for (int i = 0; i < kTopkThreads / 32; ++i) t += s_count[i];
+    *count = t;
+  }
+}
+
+cudaError_t launch_threshold(const double* scores, int64_t n, double theta, uint32_t* mask_bits,
+                             int32_t* count, cudaStream_t s) {
+  fbq_threshold_kernel<<<1, kTopkThreads, 0, s>>>(scores, n, theta, mask_bits, count);
+  return cudaGetLastError();
+}
+
+// controller_update (policy.cpp:97-109) on an observed rate held in device memory
+__global__ void fbq_controller_rate_kernel(double* theta, const double* rate, double r_min, double r_max,
+                                           double alpha, double* last_rate) {
+  const double r = *rate;
+  if (r < r_min) *theta /= alpha;
+  else if (r > r_max) *theta *= alpha;
+  if (last_rate) *last_rate = r;
+}
+
+cudaError_t launch_controller_rate(double* theta, const double* rate, double r_min, double r_max,
+                                   double alpha, double* last_rate, cudaStream_t s) {
+  fbq_controller_rate_kernel<<<1, 1, 0, s>>>(theta, rate, r_min, r_max, alpha, last_rate);
+  return cudaGetLastError();
+}
+
+// QuantLinearLayer::apply_sgd (trainsim.cpp:137-143): w -= float(lr * double(g))
+__global__ void fbq_sgd_kernel(float* w, const float* g, int64_t n, double lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = __fsub_rn(w[i], (float)(lr * (double)g[i]));
+}
+
+cudaError_t launch_sgd(float* w, const float* g, int64_t n, double lr, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  fbq_sgd_kernel<<<(unsigned)blocks, 256, 0, s>>>(w, g, n, lr);
+  return cudaGetLastError();
+}
+
 }  // namespace fbq
