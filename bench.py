@@ -654,6 +654,42 @@ def exact_mode_rate(device, T=TOKENS, steps=5, warmup=2):
             "ms_per_step": ms}
 
 
+def context_memory(device, T=TOKENS, steps=10, warmup=3):
+    """Activation contexts saved for the backward vs BF16 (PAPER.md:55, 527, 535:
+    62 %), for both storages of the 10-bit GluCombine contexts, and the step
+    rate with the packed storage (the bench's headline uses int16 containers,
+    the reference's QuantizedTensor storage)."""
+    import torch
+    from paper_2503_08040_b200 import linear
+    wg, wu, wd = make_weights()
+    out = {}
+    x = make_activations(T, D_MODEL, 1000, device, torch.bfloat16)
+    gy = make_grads(T, D_MODEL, 2000, device, torch.bfloat16)
+    for packed in (False, True):
+        m = linear.GluMlp(wg, wu, wd, T, ctx_packed=packed)
+        ours, bf = m.context_bytes(T)
+        key = "packed10" if packed else "int16"
+        out[f"{key}_MB"] = round(ours / 1e6, 1)
+        out["bf16_MB"] = round(bf / 1e6, 1)
+        out[f"{key}_frac_of_bf16"] = round(ours / bf, 4)
+        if packed:
+            m.set_thresholds(30.0, 3.0)
+            i = [0]
+
+            def step():
+                m.zero_grad()
+                m.forward(x, i[0])
+                m.backward(gy, i[0])
+                m.controller_step()
+                i[0] += 1
+            out["packed10_tokens_per_s"] = T / (_event_time(step, steps, warmup) * 1e-3)
+        del m
+    torch.cuda.empty_cache()
+    out["workload"] = (f"C3 MLP, {T} tokens: X contexts (2 x int8 SR), a / b 10-bit 1x128 contexts, h "
+                       "context (int8 SR), scale grids vs X, a, b, h in bf16")
+    return out
+
+
 # ----------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     import numpy as np
@@ -840,7 +876,7 @@ def run_ours(args, rank, world, local):
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
-        comparator = exact = None
+        comparator = exact = ctxmem = None
         if not args.no_sweep:
             try:
                 comparator = bf16_mlp_comparator(device, T)
@@ -851,6 +887,10 @@ def run_ours(args, rank, world, local):
                 exact = exact_mode_rate(device, T)
             except Exception as ex:  # pragma: no cover
                 exact = {"error": str(ex)[:200]}
+            try:
+                ctxmem = context_memory(device, T)
+            except Exception as ex:  # pragma: no cover
+                ctxmem = {"error": str(ex)[:200]}
         sweep = qsweep = c4 = None
         if not args.no_sweep and world == 1:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
@@ -915,6 +955,7 @@ def run_ours(args, rank, world, local):
             "clocks": clk.summary(),
             "bf16_mlp_comparator": comparator,
             "exact_mode": exact,
+            "context_memory": ctxmem,
             "gemm_sweep": sweep,
             "quant_sweep": qsweep,
             "qwen_block_c4": c4 if world == 1 else c4_dp,

@@ -52,6 +52,11 @@ enum fbq_mask_mode {
   FBQ_MASK_GIVEN = 2      /* u read from mask_bits (e.g. mask_topk, policy.cpp:56-71) */
 };
 enum fbq_major { FBQ_K_MAJOR = 0, FBQ_MN_MAJOR = 1 };
+/* storage of the 10-bit 1 x 128 non-linear contexts (GluCombine a / b) */
+enum fbq_ctx_format {
+  FBQ_CTX_INT16 = 0,    /* int16 codes, rows x ld_ctx (the reference's QuantizedTensor storage) */
+  FBQ_CTX_PACKED10 = 1  /* packed 10-bit planes, fbq_ctx10_bytes(rows, ld_ctx) bytes */
+};
 enum fbq_epilogue {
   FBQ_EPI_EXACT = 0, /* bit-identical to gemm.cpp's fl(acc + fl(s*P)) chain */
   FBQ_EPI_FMA = 1    /* acc = fma(P, s, acc): ~5e-8 rel. Frobenius from EXACT */
@@ -143,16 +148,24 @@ int fbq_cuda_quantize_linear_input(const void* x, int dtype, int64_t rows, int64
                                    uint64_t ctx_seed, int8_t* ctx_codes2, uint64_t ctx_seed2,
                                    int64_t row_offset, fbq_stream_t stream);
 
+/* bytes of one packed 10-bit context plane of rows x ld_ctx codes */
+int64_t fbq_ctx10_bytes(int64_t rows, int64_t ld_ctx);
+
 /* GluCombine::forward (trainsim.cpp:224-246) fused with the down projection's
  * input quantizer: ab = [a | b] (rows x 2*cols, the gate/up GEMM output, fp32
- * or bf16); writes the ctx_bits-bit 1x128 RTN contexts of a and b (int16 codes,
- * trainsim.cpp:240-243) and quantizes h = silu(a)*b exactly like
+ * or bf16); writes the ctx_bits-bit 1x128 RTN contexts of a and b
+ * (trainsim.cpp:240-243) in ctx_format: FBQ_CTX_INT16 (int16 codes, rows x
+ * ld_ctx) or FBQ_CTX_PACKED10 (ctx_bits <= 10; per context the low byte of
+ * every code, int8 [rows][ld_ctx], followed by the top two bits of each code's
+ * 10-bit two's complement, four codes per byte, [rows][ld_ctx/4], code c at
+ * bits 2*(c%4): 1.25 bytes per element, 5/8 of bf16, fbq_ctx10_bytes(rows,
+ * ld_ctx) bytes; ld_ctx % 16 == 0) -- and quantizes h = silu(a)*b exactly like
  * fbq_cuda_quantize_linear_input (threshold mode) with one context plane.
  * h itself is not written unless h_out != NULL (fp32, parity/debug).  With
  * exact_math != 0 silu is evaluated like silu_scalar (trainsim.cpp:38-41):
  * double exp, one rounding; otherwise a fast fp32 form (a few ulp away). */
 int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, int64_t ld_ab,
-                         int16_t* ctx_a, int16_t* ctx_b, int64_t ld_ctx, float* ctx_a_scales,
+                         void* ctx_a, void* ctx_b, int64_t ld_ctx, int ctx_format, float* ctx_a_scales,
                          float* ctx_b_scales, int ctx_bits, int exact_math, double theta,
                          const double* theta_dev, uint32_t* mask_bits, int8_t* codes,
                          int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
@@ -168,7 +181,7 @@ int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, 
  * [2][rows][cols]) receives ga, gb for parity checks.  exact_math as in
  * fbq_cuda_glu_forward (silu / silu_grad_scalar, trainsim.cpp:38-46). */
 int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols, int64_t ld_gh,
-                          const int16_t* ctx_a, const int16_t* ctx_b, int64_t ld_ctx,
+                          const void* ctx_a, const void* ctx_b, int64_t ld_ctx, int ctx_format,
                           const float* ctx_a_scales, const float* ctx_b_scales, int8_t* gq,
                           int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
                           int64_t row_offset, float* g_out, int exact_math, fbq_stream_t stream);

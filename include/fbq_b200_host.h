@@ -37,6 +37,9 @@ typedef struct fbq_mlp_config {
   uint64_t seed;          /* 0x5eed (QuantConfig::seed) */
   double threshold_init;  /* 1.0 (QuantConfig::threshold_init) */
   double r_min, r_max, alpha; /* 0.1, 0.3, 1.3 (ControllerConfig) */
+  int ctx_format;         /* GluCombine a / b contexts: FBQ_CTX_INT16 (default, like the
+                             reference's QuantizedTensor codes) or FBQ_CTX_PACKED10 (10 bits
+                             per code: the paper's context memory) */
 } fbq_mlp_config;
 
 void fbq_mlp_default_config(fbq_mlp_config* cfg);
@@ -91,6 +94,11 @@ int fbq_mlp_host_sync(void* mlp);
 
 /* Set the device-resident thresholds (gate/up share one, down has its own). */
 int fbq_mlp_set_thresholds(void* mlp, double theta_gate_up, double theta_down);
+/* Bytes the forward saves for the backward (activation contexts: the two int8
+ * stochastic X contexts, the a / b non-linear contexts, the int8 h context and
+ * all their scale grids) at `tokens` tokens -- and, for comparison, what a BF16
+ * implementation saves (X, a, b, h in bf16). */
+int fbq_mlp_context_bytes(void* mlp, int64_t tokens, int64_t* ours, int64_t* bf16);
 /* Optional CUDA-event timing of every GEMM launch (on the launching stream);
  * fbq_mlp_gemm_time returns the summed GEMM time since profiling was enabled
  * or last read (synchronise first) and resets. */

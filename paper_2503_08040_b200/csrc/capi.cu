@@ -54,6 +54,8 @@ int fbq_block_side(void) { return 128; }
 
 int fbq_cuda_init(void) { return cuda_status(fbq::gemm_init()); }
 
+int64_t fbq_ctx10_bytes(int64_t rows, int64_t ld_ctx) { return rows * ld_ctx + rows * (ld_ctx / 4); }
+
 int fbq_malloc(void** ptr, size_t bytes) {
   if (!ptr) return FBQ_ERR_ARG;
   *ptr = nullptr;
@@ -150,7 +152,7 @@ int fbq_cuda_quantize_linear_input(const void* x, int dtype, int64_t rows, int64
 }
 
 int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, int64_t ld_ab,
-                         int16_t* ctx_a, int16_t* ctx_b, int64_t ld_ctx, float* ctx_a_scales,
+                         void* ctx_a, void* ctx_b, int64_t ld_ctx, int ctx_format, float* ctx_a_scales,
                          float* ctx_b_scales, int ctx_bits, int exact_math, double theta,
                          const double* theta_dev, uint32_t* mask_bits,
                          int8_t* codes, int64_t ldq, float* scales, int8_t* res_codes,
@@ -164,9 +166,11 @@ int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, 
   if (!ab || ld_ab < 2 * cols || (h_out && ld_h < cols)) return FBQ_ERR_ARG;
   if ((ctx_a || ctx_b) && ld_ctx < cols) return FBQ_ERR_ARG;
   if (ctx_bits < 2 || ctx_bits > 16) return FBQ_ERR_ARG;
+  if (ctx_format != FBQ_CTX_INT16 && ctx_format != FBQ_CTX_PACKED10) return FBQ_ERR_ARG;
+  if ((ctx_a || ctx_b) && ctx_format == FBQ_CTX_PACKED10 && ctx_bits > 10) return FBQ_ERR_UNSUPPORTED;
   // vectorised 16-byte loads of a and b, 16-byte context stores
   if (cols % 8 || (ld_ab * esz) % 16 || !aligned16(ab) || (cols * esz) % 16 ||
-      ((ctx_a || ctx_b) && (ld_ctx % 8 || (ctx_a && !aligned16(ctx_a)) || (ctx_b && !aligned16(ctx_b)))))
+      ((ctx_a || ctx_b) && (ld_ctx % 16 || (ctx_a && !aligned16(ctx_a)) || (ctx_b && !aligned16(ctx_b)))))
     return FBQ_ERR_UNSUPPORTED;
   if (cdiv(rows, 128) > 65535) return FBQ_ERR_UNSUPPORTED;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -177,13 +181,14 @@ int fbq_cuda_glu_forward(const void* ab, int dtype, int64_t rows, int64_t cols, 
                                  row_offset, s, theta_dev))
     return st;
   if (ldq % 16) return FBQ_ERR_UNSUPPORTED;
-  fbq::GluParams g{ab, rows, cols, ld_ab, ctx_a, ctx_b, ld_ctx, ctx_a_scales, ctx_b_scales,
-                   (float)((1 << (ctx_bits - 1)) - 1), h_out, ld_h, exact_math ? 1 : 0};
+  fbq::GluParams g{ab, rows, cols, ld_ab, static_cast<uint8_t*>(ctx_a), static_cast<uint8_t*>(ctx_b), ld_ctx,
+                   ctx_a_scales, ctx_b_scales, (float)((1 << (ctx_bits - 1)) - 1), h_out, ld_h,
+                   exact_math ? 1 : 0, ctx_format == FBQ_CTX_PACKED10 ? 1 : 0};
   return cuda_status(fbq::launch_glu_forward(g, p, dtype == FBQ_BF16, s));
 }
 
 int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols, int64_t ld_gh,
-                          const int16_t* ctx_a, const int16_t* ctx_b, int64_t ld_ctx,
+                          const void* ctx_a, const void* ctx_b, int64_t ld_ctx, int ctx_format,
                           const float* ctx_a_scales, const float* ctx_b_scales, int8_t* gq,
                           int64_t ldq, float* gq_scales, uint64_t seed_a, uint64_t seed_b,
                           int64_t row_offset, float* g_out, int exact_math, fbq_stream_t stream) {
@@ -194,12 +199,15 @@ int fbq_cuda_glu_backward(const void* gh, int dtype, int64_t rows, int64_t cols,
   if (!gh || !ctx_a || !ctx_b || !ctx_a_scales || !ctx_b_scales || !gq || !gq_scales)
     return FBQ_ERR_ARG;
   if (ld_gh < cols || ld_ctx < cols || ldq < 2 * cols || row_offset < 0) return FBQ_ERR_ARG;
-  if (cols % 8 || (ld_gh * esz) % 16 || !aligned16(gh) || ldq % 16 || cols % 16)
+  if (ctx_format != FBQ_CTX_INT16 && ctx_format != FBQ_CTX_PACKED10) return FBQ_ERR_ARG;
+  if (cols % 8 || (ld_gh * esz) % 16 || !aligned16(gh) || ldq % 16 || cols % 16 || ld_ctx % 16 ||
+      !aligned16(ctx_a) || !aligned16(ctx_b))
     return FBQ_ERR_UNSUPPORTED;
   if (cdiv(rows, 128) > 65535) return FBQ_ERR_UNSUPPORTED;
-  fbq::GluBwdParams g{gh,    rows,   cols,   ld_gh,      ctx_a,     ctx_b,    ld_ctx,
-                      ctx_a_scales, ctx_b_scales, gq, ldq, gq_scales, seed_a, seed_b,
-                      row_offset, g_out, exact_math ? 1 : 0};
+  fbq::GluBwdParams g{gh, rows, cols, ld_gh, static_cast<const uint8_t*>(ctx_a),
+                      static_cast<const uint8_t*>(ctx_b), ld_ctx, ctx_a_scales, ctx_b_scales, gq, ldq,
+                      gq_scales, seed_a, seed_b, row_offset, g_out, exact_math ? 1 : 0,
+                      ctx_format == FBQ_CTX_PACKED10 ? 1 : 0};
   return cuda_status(fbq::launch_glu_backward(g, dtype == FBQ_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 

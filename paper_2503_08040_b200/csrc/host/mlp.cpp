@@ -147,8 +147,15 @@ struct Mlp {
     x_res_scales = DevBuf(gT * gD * f4);
     x_mask = DevBuf(cdiv(gT * gD, 32) * 4);
     ab = DevBuf(T * 2 * F * esize(c.mid_dtype));
-    ctx_a = DevBuf(T * ldF * 2);
-    ctx_b = DevBuf(T * ldF * 2);
+    // a / b contexts: int16 codes or packed 10-bit planes (1.25 B per element,
+    // fbq_ctx10_bytes; the plane layout follows the call's row count, so the
+    // buffers are sized for the capacity)
+    if (c.ctx_format != FBQ_CTX_INT16 && c.ctx_format != FBQ_CTX_PACKED10)
+      throw CudaError(FBQ_ERR_ARG, "bad ctx_format");
+    if (c.ctx_format == FBQ_CTX_PACKED10 && c.nonlinear_bits > 10)
+      throw CudaError(FBQ_ERR_UNSUPPORTED, "nonlinear_bits > 10 with packed 10-bit contexts");
+    ctx_a = DevBuf(ctx_bytes(T) + 16);
+    ctx_b = DevBuf(ctx_bytes(T) + 16);
     ctx_a_s = DevBuf(T * gF * f4);
     ctx_b_s = DevBuf(T * gF * f4);
     h_codes = DevBuf(T * ldF);
@@ -278,7 +285,7 @@ struct Mlp {
                           tok, 2 * F, D, ab.p, c.mid_dtype, 2 * F, 0, c.epilogue, s); }, s);
     // GLU + contexts + quantization of h for the down projection
     FBQ_TRY(fbq_cuda_glu_forward(
-        ab.p, c.mid_dtype, tok, F, 2 * F, ctx_a.as<int16_t>(), ctx_b.as<int16_t>(), ldF,
+        ab.p, c.mid_dtype, tok, F, 2 * F, ctx_a.p, ctx_b.p, ldF, c.ctx_format,
         ctx_a_s.as<float>(), ctx_b_s.as<float>(), c.nonlinear_bits, exact_math(), c.threshold_init, th + 1,
         h_mask.as<uint32_t>(), h_codes.as<int8_t>(), ldF, h_scales.as<float>(),
         h_res.as<int8_t>(), h_res_scales.as<float>(), cnt + 1, ctx_h.as<int8_t>(),
@@ -334,8 +341,8 @@ struct Mlp {
     // on a side stream here, overlapped with the rest of the backward
     CU_TRY(cudaEventRecord(ev_grad[2], b));
     // GLU backward fused with SR(ga), SR(gb)
-    FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.as<int16_t>(),
-                                  ctx_b.as<int16_t>(), ldF, ctx_a_s.as<float>(),
+    FBQ_TRY(fbq_cuda_glu_backward(gh.p, c.mid_dtype, tok, F, F, ctx_a.p, ctx_b.p, ldF, c.ctx_format,
+                                  ctx_a_s.as<float>(),
                                   ctx_b_s.as<float>(), gq.as<int8_t>(), ldF2,
                                   gq_scales.as<float>(), layer_seed(c.seed, layer(0), 1, step),
                                   layer_seed(c.seed, layer(1), 1, step), row_off, nullptr,
@@ -397,7 +404,11 @@ struct Mlp {
                                        rates.as<double>() + 1, s));
   }
   int64_t last_blocks[2] = {1, 1};
-  int64_t ctl_blocks[2] = {0, 0};  // blocks the last controller step divided by (0: none yet)
+  int64_t ctl_blocks[2] = {0, 0};
+  // one a / b context plane at `tok` tokens
+  int64_t ctx_bytes(int64_t tok) const {
+    return c.ctx_format == FBQ_CTX_PACKED10 ? fbq_ctx10_bytes(tok, ldF) : tok * ldF * 2;
+  }  // blocks the last controller step divided by (0: none yet)
 
   void step_host(const float* x, const float* gy, int64_t tok, int step, float* y, float* gx) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
@@ -679,6 +690,7 @@ void fbq_mlp_default_config(fbq_mlp_config* c) {
   c->mid_dtype = FBQ_BF16;
   c->epilogue = FBQ_EPI_FMA;
   c->nonlinear_bits = 10;
+  c->ctx_format = FBQ_CTX_INT16;
   c->layer_id_base = 0;
   c->seed = 0x5eedull;
   c->threshold_init = 1.0;
@@ -771,6 +783,18 @@ int fbq_mlp_set_thresholds(void* m, double theta_gate_up, double theta_down) {
     const double th[2] = {theta_gate_up, theta_down};
     CU_TRY(cudaMemcpy(static_cast<Mlp*>(m)->theta.p, th, sizeof(th), cudaMemcpyHostToDevice));
   });
+}
+
+int fbq_mlp_context_bytes(void* m, int64_t tokens, int64_t* ours, int64_t* bf16) {
+  if (!m || tokens < 0 || !ours || !bf16) return FBQ_ERR_ARG;
+  auto* mlp = static_cast<Mlp*>(m);
+  const int64_t t = tokens, D = mlp->D, F = mlp->F, gt = cdiv(t, 128);
+  const int64_t x_ctx = 2 * t * mlp->ldD + 2 * gt * mlp->gD * 4;          // gate + up SR contexts of X
+  const int64_t ab_ctx = 2 * mlp->ctx_bytes(t) + 2 * t * mlp->gF * 4;      // a, b (1 x 128 scales)
+  const int64_t h_ctx = t * mlp->ldF + gt * mlp->gF * 4;                   // SR context of h
+  *ours = x_ctx + ab_ctx + h_ctx;
+  *bf16 = 2 * (t * D + 2 * t * F + t * F);                                  // X, a, b, h in bf16
+  return FBQ_OK;
 }
 
 int fbq_mlp_set_profiling(void* m, int on) {

@@ -117,6 +117,46 @@ __device__ __forceinline__ void store_codes16(int16_t* p, const uint32_t* w) {
   else *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// ---- packed 10-bit context planes (GluCombine's a / b contexts, trainsim.cpp:240-243)
+// A context of rows x cols codes (|code| <= 511) with row stride ld (elements,
+// ld % 16 == 0) is stored as 10 bits per code: the LOW byte of every code
+// (int8 [rows][ld]) followed by the top two bits of the 10-bit two's
+// complement, four codes per byte ([rows][ld / 4], code c at bits 2 (c % 4)).
+// 1.25 bytes per element = 5/8 of bf16.
+template <int V>
+__device__ __forceinline__ void store_ctx10(uint8_t* lo, uint8_t* hi, const uint32_t* w) {
+  if constexpr (V == 8) *reinterpret_cast<uint2*>(lo) = make_uint2(pack4_lo8(w), pack4_lo8(w + 4));
+  else *reinterpret_cast<uint32_t*>(lo) = pack4_lo8(w);
+  uint32_t h = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) h |= ((w[i] >> 8) & 3u) << (2 * i);
+  if constexpr (V == 8) *reinterpret_cast<uint16_t*>(hi) = (uint16_t)h;
+  else *hi = (uint8_t)h;
+}
+// V codes as int32 scaled by 2^22 (exact: |code| < 2^9): the low byte shifted to
+// bits 22-29 and the two top bits to bits 30-31 -- two shifts and one LOP3 per
+// code; the caller folds 2^-22 into the scale.
+template <int V>
+__device__ __forceinline__ void load_ctx10_x4m(const uint8_t* lo, const uint8_t* hi, int32_t (&c)[V]) {
+  uint32_t L[V / 4], H;
+  if constexpr (V == 8) {
+    const uint2 l = *reinterpret_cast<const uint2*>(lo);
+    L[0] = l.x;
+    L[1] = l.y;
+    H = *reinterpret_cast<const uint16_t*>(hi);
+  } else {
+    L[0] = *reinterpret_cast<const uint32_t*>(lo);
+    H = *hi;
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int k = i & 3;
+    const uint32_t lb = k <= 2 ? (L[i >> 2] << (22 - 8 * k)) : (L[i >> 2] >> (8 * k - 22));
+    const uint32_t hb = 30 >= 2 * i ? (H << (30 - 2 * i)) : (H >> (2 * i - 30));
+    c[i] = (int32_t)((lb & 0x3FC00000u) | (hb & 0xC0000000u));
+  }
+}
+
 // ------------------------------------------------------------------ staging
 // Copy a 128 x 128 block of T (row stride ld) into smem (row stride 128),
 // zero-filling outside [rows) x [cols).  All vector loads are issued before the
@@ -752,7 +792,7 @@ __device__ __forceinline__ float group_rtn(const float (&x)[V], uint32_t (&w)[V]
 // in the row; only the VPR threads of that row -- one warp or half-warp --
 // touch it, so a __syncwarp orders their reads before their writes).  h is
 // thus evaluated once and never reaches HBM.
-template <typename T, bool kStaged, int kMinBlocks = 1>
+template <typename T, bool kStaged, int kMinBlocks = 1, bool kPacked = false>
 __global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_glu_forward_kernel(GluParams g, QuantParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -828,10 +868,20 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
     load_ab(rb, lc, va, vb);
     uint32_t code[V];
     float s = group_rtn<V, VPR>(va, code, g.ctx_level);
-    if (ok && g.ctx_a) store_codes16<V>(g.ctx_a + r * g.ld_ctx + cc, code);
+    if (ok && g.ctx_a) {
+      if constexpr (kPacked)
+        store_ctx10<V>(g.ctx_a + r * g.ld_ctx + cc, g.ctx_a + g.rows * g.ld_ctx + r * (g.ld_ctx >> 2) + (cc >> 2), code);
+      else
+        store_codes16<V>(reinterpret_cast<int16_t*>(g.ctx_a) + r * g.ld_ctx + cc, code);
+    }
     if (ok && g.ctx_a_scales && lc == 0) g.ctx_a_scales[r * gcols + bj] = s;
     s = group_rtn<V, VPR>(vb, code, g.ctx_level);
-    if (ok && g.ctx_b) store_codes16<V>(g.ctx_b + r * g.ld_ctx + cc, code);
+    if (ok && g.ctx_b) {
+      if constexpr (kPacked)
+        store_ctx10<V>(g.ctx_b + r * g.ld_ctx + cc, g.ctx_b + g.rows * g.ld_ctx + r * (g.ld_ctx >> 2) + (cc >> 2), code);
+      else
+        store_codes16<V>(reinterpret_cast<int16_t*>(g.ctx_b) + r * g.ld_ctx + cc, code);
+    }
     if (ok && g.ctx_b_scales && lc == 0) g.ctx_b_scales[r * gcols + bj] = s;
     float vh[V];
     hval(va, vb, vh);
@@ -874,13 +924,11 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
 // two CTAs per SM); otherwise every pass reads them straight from global
 // memory (the second pass hits L2) with three CTAs per SM -- more warps for
 // an issue-bound kernel.
-template <typename T, bool kStaged, int kMinBlocks = 1>
+template <typename T, bool kStaged, int kMinBlocks = 1, bool kPacked = false>
 __global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_glu_backward_kernel(GluBwdParams g) {
   extern __shared__ __align__(16) uint8_t dsm[];
   T* tg = reinterpret_cast<T*>(dsm);
-  int16_t* tca = reinterpret_cast<int16_t*>(tg + kTileElems);
-  int16_t* tcb = tca + kTileElems;
   __shared__ float sa_row[kBlock], sb_row[kBlock];
   __shared__ float red[kQuantThreads / 32], red2[kQuantThreads / 32];
   constexpr int V = Tiling<T>::V;
@@ -890,9 +938,10 @@ fbq_glu_backward_kernel(GluBwdParams g) {
   const int64_t gcols = (g.cols + kBlock - 1) / kBlock;
   if constexpr (kStaged) {
     stage_tile<T, true>(tg, reinterpret_cast<const T*>(g.gh), g.ld_gh, g.rows, g.cols, r0, c0);
-    stage_tile<int16_t, true>(tca, g.ctx_a, g.ld_ctx, g.rows, g.cols, r0, c0);
-    stage_tile<int16_t, true>(tcb, g.ctx_b, g.ld_ctx, g.rows, g.cols, r0, c0);
   }
+  // the row scales with the packed contexts' 2^22 folded in; a scale small
+  // enough for that product to leave the normal range (never for real data)
+  // takes the exact path: the code is then read unscaled
   if (threadIdx.x < kBlock) {
     const int64_t r = r0 + threadIdx.x;
     sa_row[threadIdx.x] = r < g.rows ? g.ctx_a_scales[r * gcols + bj] : 0.0f;
@@ -900,21 +949,35 @@ fbq_glu_backward_kernel(GluBwdParams g) {
   }
   __syncthreads();
   // dequantized contexts: fl(code * scale) (quant.cpp:86-104); a zero scale
-  // has all-zero codes, so no special case is needed
-  auto deq = [&](const int16_t* t, const int16_t* gt, float s, int rb, int cb, float (&v)[V]) {
-    int16_t c[V];
-    if constexpr (kStaged) {
-      if constexpr (V == 8) *reinterpret_cast<uint4*>(c) = *reinterpret_cast<const uint4*>(t + rb * kBlock + cb);
-      else *reinterpret_cast<uint2*>(c) = *reinterpret_cast<const uint2*>(t + rb * kBlock + cb);
-    } else {
-      const int64_t r = r0 + rb, cc = c0 + cb;
-      const bool ok = r < g.rows && cc < g.cols;
-      const int16_t* src = gt + r * g.ld_ctx + cc;
+  // has all-zero codes, so no special case is needed.  fl((code 2^22) (s 2^-22))
+  // == fl(code s) while s 2^-22 stays a normal float (s >= 2^-104).
+  auto deq = [&](const uint8_t* gt, float s, int rb, int cb, float (&v)[V]) {
+    const int64_t r = r0 + rb, cc = c0 + cb;
+    const bool ok = r < g.rows && cc < g.cols;
+    if constexpr (!kPacked) {  // int16 codes (the reference's QuantizedTensor storage)
+      int16_t c[V];
+      const int16_t* src = reinterpret_cast<const int16_t*>(gt) + r * g.ld_ctx + cc;
       if constexpr (V == 8) *reinterpret_cast<uint4*>(c) = ok ? *reinterpret_cast<const uint4*>(src) : make_uint4(0, 0, 0, 0);
       else *reinterpret_cast<uint2*>(c) = ok ? *reinterpret_cast<const uint2*>(src) : make_uint2(0, 0);
-    }
 #pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = __fmul_rn((float)c[i], s);
+      for (int i = 0; i < V; ++i) v[i] = __fmul_rn((float)c[i], s);
+      return;
+    }
+    int32_t c[V];
+    if (ok) {
+      load_ctx10_x4m<V>(gt + r * g.ld_ctx + cc, gt + g.rows * g.ld_ctx + r * (g.ld_ctx >> 2) + (cc >> 2), c);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) c[i] = 0;
+    }
+    if (s >= 0x1p-104f) {
+      const float s22 = s * 0x1p-22f;
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = __fmul_rn((float)c[i], s22);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = __fmul_rn((float)(c[i] >> 22), s);
+    }
   };
   auto eval = [&](int rb, int cb, float (&ga)[V], float (&gb)[V]) {
     float a[V], b[V];
@@ -929,8 +992,8 @@ fbq_glu_backward_kernel(GluBwdParams g) {
         for (int i = 0; i < V; ++i) ga[i] = 0.0f;
       }
     }
-    deq(tca, g.ctx_a, sa_row[rb], rb, cb, a);
-    deq(tcb, g.ctx_b, sb_row[rb], rb, cb, b);
+    deq(g.ctx_a, sa_row[rb], rb, cb, a);
+    deq(g.ctx_b, sb_row[rb], rb, cb, b);
     if (g.exact_math) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
@@ -1566,8 +1629,8 @@ cudaError_t launch_quantize(const QuantParams& p, bool bf16, cudaStream_t s) {
   return vec ? launch_k1<float, true>(p, grid, s) : launch_k1<float, false>(p, grid, s);
 }
 
-cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16,
-                               cudaStream_t s) {
+template <bool kPacked>
+static cudaError_t launch_glu_forward_t(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s) {
   const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
                   (unsigned)((g.rows + kBlock - 1) / kBlock));
   // staged (default): h computed once into shared memory, three CTAs per SM
@@ -1575,43 +1638,52 @@ cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf
   // a|b from L2 and re-evaluates h per pass at four CTAs per SM (505 us)
   if (bf16) {
     if (g_quant_diag & 256)
-      return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16, false, 4>, grid, dim3(kQuantThreads), 0, s,
+      return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16, false, 4, kPacked>, grid, dim3(kQuantThreads), 0, s,
                        p.pdl, g, p);
     const size_t smem = 2 * sizeof(__nv_bfloat16) * kTileElems;  // a|b rows, then h (fp32) in place
-    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16, true, 3>, smem)) return e;
-    return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16, true, 3>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
+    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<__nv_bfloat16, true, 3, kPacked>, smem)) return e;
+    return launch_ex(fbq_glu_forward_kernel<__nv_bfloat16, true, 3, kPacked>, grid, dim3(kQuantThreads), smem, s,
+                     p.pdl, g, p);
+  }
+  const size_t smem = 2 * sizeof(float) * kTileElems;
+  if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<float, true, 1, kPacked>, smem)) return e;
+  return launch_ex(fbq_glu_forward_kernel<float, true, 1, kPacked>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
+}
+
+cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s) {
+  return g.ctx_packed ? launch_glu_forward_t<true>(g, p, bf16, s) : launch_glu_forward_t<false>(g, p, bf16, s);
+}
+
+template <bool kPacked>
+static cudaError_t launch_glu_backward_t(const GluBwdParams& g, bool bf16, cudaStream_t s) {
+  const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
+                  (unsigned)((g.rows + kBlock - 1) / kBlock));
+  const bool staged = (g_quant_diag & 32) != 0;  // diagnostics: dH staged in shared memory
+  if (bf16) {
+    if (!staged) {
+      // four CTAs (32 warps) per SM: 64 registers; measured 484 us vs 590 us
+      // at 82 registers / three CTAs (int16 contexts); packed 10-bit contexts:
+      // 582 us at four CTAs (a few spilled bytes) vs 621 us at three
+      fbq_glu_backward_kernel<__nv_bfloat16, false, 4, kPacked><<<grid, kQuantThreads, 0, s>>>(g);
+      return cudaGetLastError();
+    }
+    const size_t smem = sizeof(__nv_bfloat16) * kTileElems;
+    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<__nv_bfloat16, true, 1, kPacked>, smem)) return e;
+    fbq_glu_backward_kernel<__nv_bfloat16, true, 1, kPacked><<<grid, kQuantThreads, smem, s>>>(g);
   } else {
-    const size_t smem = 2 * sizeof(float) * kTileElems;
-    if (cudaError_t e = opt_in_smem(fbq_glu_forward_kernel<float, true>, smem)) return e;
-    return launch_ex(fbq_glu_forward_kernel<float, true>, grid, dim3(kQuantThreads), smem, s, p.pdl, g, p);
+    if (!staged) {
+      fbq_glu_backward_kernel<float, false, 3, kPacked><<<grid, kQuantThreads, 0, s>>>(g);
+      return cudaGetLastError();
+    }
+    const size_t smem = sizeof(float) * kTileElems;
+    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<float, true, 1, kPacked>, smem)) return e;
+    fbq_glu_backward_kernel<float, true, 1, kPacked><<<grid, kQuantThreads, smem, s>>>(g);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s) {
-  const dim3 grid((unsigned)((g.cols + kBlock - 1) / kBlock),
-                  (unsigned)((g.rows + kBlock - 1) / kBlock));
-  const bool staged = (g_quant_diag & 32) != 0;  // diagnostics: the smem-staged variant
-  if (bf16) {
-    if (!staged) {
-      // four CTAs (32 warps) per SM: 64 registers; measured 484 us vs 590 us
-      // at 82 registers / three CTAs (a few spilled bytes notwithstanding)
-      fbq_glu_backward_kernel<__nv_bfloat16, false, 4><<<grid, kQuantThreads, 0, s>>>(g);
-      return cudaGetLastError();
-    }
-    const size_t smem = (sizeof(__nv_bfloat16) + 2 * sizeof(int16_t)) * kTileElems;
-    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<__nv_bfloat16, true>, smem)) return e;
-    fbq_glu_backward_kernel<__nv_bfloat16, true><<<grid, kQuantThreads, smem, s>>>(g);
-  } else {
-    if (!staged) {
-      fbq_glu_backward_kernel<float, false, 3><<<grid, kQuantThreads, 0, s>>>(g);
-      return cudaGetLastError();
-    }
-    const size_t smem = (sizeof(float) + 2 * sizeof(int16_t)) * kTileElems;
-    if (cudaError_t e = opt_in_smem(fbq_glu_backward_kernel<float, true>, smem)) return e;
-    fbq_glu_backward_kernel<float, true><<<grid, kQuantThreads, smem, s>>>(g);
-  }
-  return cudaGetLastError();
+  return g.ctx_packed ? launch_glu_backward_t<true>(g, bf16, s) : launch_glu_backward_t<false>(g, bf16, s);
 }
 
 cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,

@@ -34,8 +34,8 @@ struct QuantParams {
 struct GluParams {
   const void* ab;          // rows x ld_ab: a in cols [0, cols), b in [cols, 2 cols)
   int64_t rows, cols, ld_ab;
-  int16_t* ctx_a;          // 1 x 128 RTN contexts (rows x ld_ctx), may be null
-  int16_t* ctx_b;
+  uint8_t* ctx_a;          // 1 x 128 RTN contexts (int16 codes, or packed 10-bit planes), may be null
+  uint8_t* ctx_b;
   int64_t ld_ctx;
   float* ctx_a_scales;     // rows x ceil(cols/128)
   float* ctx_b_scales;
@@ -43,14 +43,15 @@ struct GluParams {
   float* h_out;            // optional fp32 h (rows x ld_h), parity/debug
   int64_t ld_h;
   int exact_math;          // 1: silu like the reference (double); 0: fast fp32
+  int ctx_packed;          // 1: packed 10-bit context planes (store_ctx10); 0: int16 codes
 };
 
 // GluCombine backward fused with the gate/up dY stochastic quantizers.
 struct GluBwdParams {
   const void* gh;          // dH, rows x ld_gh
   int64_t rows, cols, ld_gh;
-  const int16_t* ctx_a;
-  const int16_t* ctx_b;
+  const uint8_t* ctx_a;    // int16 codes or packed 10-bit planes (rows x ld_ctx)
+  const uint8_t* ctx_b;
   int64_t ld_ctx;
   const float* ctx_a_scales;
   const float* ctx_b_scales;
@@ -61,6 +62,7 @@ struct GluBwdParams {
   int64_t row_offset;
   float* g_out;            // optional fp32 [2][rows][cols] (ga, gb), parity/debug
   int exact_math;          // 1: silu / silu' like the reference (double); 0: fast fp32
+  int ctx_packed;          // as GluParams::ctx_packed
 };
 
 struct DequantParams {

@@ -23,7 +23,7 @@ class MlpConfig(C.Structure):
         ("act_dtype", C.c_int), ("mid_dtype", C.c_int), ("epilogue", C.c_int),
         ("nonlinear_bits", C.c_int), ("layer_id_base", C.c_int), ("seed", C.c_uint64),
         ("threshold_init", C.c_double), ("r_min", C.c_double), ("r_max", C.c_double),
-        ("alpha", C.c_double),
+        ("alpha", C.c_double), ("ctx_format", C.c_int),
     ]
 
 
@@ -51,6 +51,7 @@ _sigs = {
     "fbq_mlp_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "fbq_host_last_error": (C.c_char_p, []),
     "fbq_mlp_set_thresholds": (C.c_int, [C.c_void_p, C.c_double, C.c_double]),
+    "fbq_mlp_context_bytes": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "fbq_mlp_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "fbq_mlp_gemm_time": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "fbq_mlp_launch_count": (C.c_int64, [C.c_void_p]),
@@ -131,7 +132,8 @@ class GluMlp:
 
     def __init__(self, w_gate, w_up, w_down, max_tokens, *, act_dtype=torch.bfloat16,
                  mid_dtype=torch.bfloat16, exact=False, threshold_init=1.0, seed=0x5EED,
-                 layer_id_base=0, nonlinear_bits=10, r_min=0.1, r_max=0.3, alpha=1.3):
+                 layer_id_base=0, nonlinear_bits=10, r_min=0.1, r_max=0.3, alpha=1.3,
+                 ctx_packed=False):
         wg = np.ascontiguousarray(np.asarray(w_gate, np.float32))
         wu = np.ascontiguousarray(np.asarray(w_up, np.float32))
         wd = np.ascontiguousarray(np.asarray(w_down, np.float32))
@@ -145,6 +147,9 @@ class GluMlp:
         cfg.epilogue = K.FBQ_EPI_EXACT if exact else K.FBQ_EPI_FMA
         cfg.threshold_init, cfg.seed, cfg.layer_id_base = threshold_init, seed, layer_id_base
         cfg.nonlinear_bits, cfg.r_min, cfg.r_max, cfg.alpha = nonlinear_bits, r_min, r_max, alpha
+        # GluCombine a / b contexts: int16 codes (the reference's storage) or
+        # packed 10-bit planes (the paper's context memory)
+        cfg.ctx_format = 1 if ctx_packed else 0
         self.cfg = cfg
         self.act_dtype = act_dtype
         self.max_tokens = max_tokens
@@ -247,6 +252,13 @@ class GluMlp:
 
     def set_thresholds(self, theta_gate_up: float, theta_down: float):
         _check(lib.fbq_mlp_set_thresholds(self._h, theta_gate_up, theta_down), "set_thresholds")
+
+    def context_bytes(self, tokens: int):
+        """(bytes saved for the backward by this driver, bytes a BF16 MLP saves)
+        at `tokens` tokens -- PAPER.md:527,535 (contexts at 62 % of BF16)."""
+        ours, bf = C.c_int64(), C.c_int64()
+        _check(lib.fbq_mlp_context_bytes(self._h, tokens, C.byref(ours), C.byref(bf)), "context_bytes")
+        return ours.value, bf.value
 
     def set_profiling(self, on: bool):
         _check(lib.fbq_mlp_set_profiling(self._h, int(on)), "set_profiling")
