@@ -69,6 +69,31 @@ __device__ __forceinline__ void consume32_denorm(const uint32_t* v, float2* acc,
   }
 }
 
+// offset-binary operands (u8 x u8): P' = P + bias >= 0 is a denormal; one FFMA removes the
+// uniform bias exactly (t = P' 2^-149 * s 2^149 - s 2^21, single rounding), one FADD accumulates
+__device__ __forceinline__ void consume32_offset(const uint32_t* v, float2* acc, float s) {
+  const float2 s2 = make_float2(s * 0x1p126f * 0x1p23f, s * 0x1p126f * 0x1p23f);
+  const float2 b2 = make_float2(-s * 2097152.0f, -s * 2097152.0f);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 t = __ffma2_rn(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), s2, b2);
+    acc[i] = __fadd2_rn(acc[i], t);
+  }
+}
+// upper bound: one FFMA2 per pair on the raw words (no conversion, no bias removal)
+__device__ __forceinline__ void consume32_raw(const uint32_t* v, float2* acc, float s) {
+  const float2 s2 = make_float2(s, s);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    acc[i] = __ffma2_rn(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), s2, acc[i]);
+}
+
+template <bool kOff>
+__device__ __forceinline__ void consume_sel(const uint32_t* v, float2* acc, float s) {
+  if constexpr (kOff) consume32_offset(v, acc, s);
+  else consume32(v, acc, s);
+}
+
 __device__ __forceinline__ void st8(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v)
                : "memory");
@@ -172,7 +197,8 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
       }
     }
   } else if (warp == 1 && rank == 0) {
-    const uint32_t idesc = idesc_i8(128 * kCta, 256, 0, 0);
+    const uint32_t idesc = (kEpi == 6 || kEpi == 7 || kEpi == 8) ? (idesc_i8(128 * kCta, 256, 0, 0) & ~((1u << 7) | (1u << 10)))
+                                                    : idesc_i8(128 * kCta, 256, 0, 0);
     int stage = 0;
     uint32_t phase = 0, item = 0;
     t0 = clock64();
@@ -248,8 +274,8 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
       for (int i = 0; i < 32; ++i) a += acc[i].x + acc[i].y;
       if (a == 1234.5f) sink[0] = a;
     }
-  } else if (kEpi == 4 && warp >= 4) {
-    if constexpr (kEpi == 4) {
+  } else if ((kEpi == 4 || kEpi == 8) && warp >= 4) {
+    if constexpr (kEpi == 4 || kEpi == 8) {
       setmaxnreg_inc<224>();
       const int q = warp & 3, h = (warp - 4) >> 2;
       const uint32_t lane_base = tmem + ((q * 32) << 16) + h * 128;
@@ -270,13 +296,13 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
         const int slot = it & 1;
         const uint32_t tb = lane_base + slot * 256;
         ld32p(tb + 32, vb);
-        consume32(va, acc + 0, s);
+        consume_sel<kEpi == 8>(va, acc + 0, s);
         tmem_ld_wait();
         ld32p(tb + 64, va);
-        consume32(vb, acc + 16, s);
+        consume_sel<kEpi == 8>(vb, acc + 16, s);
         tmem_ld_wait();
         ld32p(tb + 96, vb);
-        consume32(va, acc + 32, s);
+        consume_sel<kEpi == 8>(va, acc + 32, s);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -287,7 +313,7 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
           tc_fence_after();
           ld32p(lane_base + ns * 256, va);
         }
-        consume32(vb, acc + 48, s);
+        consume_sel<kEpi == 8>(vb, acc + 48, s);
         tmem_ld_wait();
       }
       float a = 0.f;
@@ -295,7 +321,7 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
       for (int i = 0; i < 64; ++i) a += acc[i].x + acc[i].y;
       if (a == 1234.5f) sink[0] = a;
     }
-  } else if (kEpi != 3 && kEpi != 4 && warp >= 4) {
+  } else if (kEpi != 3 && kEpi != 4 && kEpi != 8 && warp >= 4) {
     setmaxnreg_inc<224>();
     const int q = warp & 3, h = (warp - 4) >> 2;
     const uint32_t lane_base = tmem + ((q * 32) << 16) + h * 128;
@@ -349,17 +375,29 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
           ld32p(tb, va);
           ld32p(tb + 32, vb);
           tmem_ld_wait();
-          consume32(va, acc, s);
+          if constexpr (kEpi == 6) consume32_offset(va, acc, s);
+          else if constexpr (kEpi == 7) consume32_raw(va, acc, s);
+          else consume32(va, acc, s);
           ld32p(tb + 64, va);
-          consume32(vb, acc + 16, s);
+          if constexpr (kEpi == 6) consume32_offset(vb, acc + 16, s);
+          else if constexpr (kEpi == 7) consume32_raw(vb, acc + 16, s);
+          else consume32(vb, acc + 16, s);
           ld32p(tb + 96, vb);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_any(tempty + slot, tempty_r + slot * 8, kCta == 2);
-          consume32(va, acc + 32, s);
-          if constexpr (kEpi == 5) consume32_denorm(vb, acc + 48, s);
-          else consume32(vb, acc + 48, s);
+          if constexpr (kEpi == 6) {
+            consume32_offset(va, acc + 32, s);
+            consume32_offset(vb, acc + 48, s);
+          } else if constexpr (kEpi == 7) {
+            consume32_raw(va, acc + 32, s);
+            consume32_raw(vb, acc + 48, s);
+          } else {
+            consume32(va, acc + 32, s);
+            if constexpr (kEpi == 5) consume32_denorm(vb, acc + 48, s);
+            else consume32(vb, acc + 48, s);
+          }
         }
       }
     }
@@ -455,7 +493,12 @@ int main() {
   cudaMalloc(&b, (size_t)kN * kK);
   fill<<<1024, 256>>>((uint32_t*)a, (size_t)kM * kK / 4, 1);
   fill<<<1024, 256>>>((uint32_t*)b, (size_t)kN * kK / 4, 2);
-  run<1, 3, 1>(a, b);
-  run<1, 3, 5>(a, b);
+  run<1, 4, 0>(a, b);
+  run<1, 4, 1>(a, b);
+  run<1, 4, 4>(a, b);
+  run<1, 4, 6>(a, b);
+  run<1, 4, 8>(a, b);
+  run<1, 3, 6>(a, b);
+  run<1, 4, 7>(a, b);
   return 0;
 }
