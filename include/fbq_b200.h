@@ -267,7 +267,8 @@ int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
  * (kernels.cpp:24-40), out_sr[i] = SR code with RNG bits[i] (quant.cpp:69-77).
  * path 0: scalar functions, 1: the kernels' vector paths (V = 1), 2: 10-bit
  * context RTN (int16 out), 3: the 8-wide packed RTN path (n % 8 == 0, one
- * scale per 8-element vector = a[8g]). */
+ * scale per 8-element vector = a[8g]), 4: the same packed path at level 511
+ * (the 10-bit contexts' group RTN incl. its packed exact fix; int16 out). */
 int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
                          int8_t* out_sr, int64_t n, int path, fbq_stream_t stream);
 

@@ -440,8 +440,8 @@ int fbq_cuda_dequantize(const int8_t* codes, int64_t ldq, const float* scales,
 
 int fbq_cuda_round_probe(const float* x, const float* a, const uint64_t* bits, int8_t* out_rtn,
                          int8_t* out_sr, int64_t n, int path, fbq_stream_t stream) {
-  if (path < 0 || path > 3 || (path >= 2 && out_sr)) return FBQ_ERR_ARG;
-  if (path == 3 && (n % 8 || !out_rtn)) return FBQ_ERR_ARG;
+  if (path < 0 || path > 4 || (path >= 2 && out_sr)) return FBQ_ERR_ARG;
+  if (path >= 3 && (n % 8 || !out_rtn)) return FBQ_ERR_ARG;
   if (n < 0) return FBQ_ERR_SHAPE;
   if (n == 0) return FBQ_OK;
   if (!x || !a || (out_sr && !bits)) return FBQ_ERR_ARG;

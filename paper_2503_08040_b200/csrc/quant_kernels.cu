@@ -217,9 +217,10 @@ template <int V>
 __device__ __forceinline__ void rtn_vec(const float (&v)[V], float a, float inv_a, int mode,
                                         uint32_t (&w)[V]) {
   if (mode == 2) {
-    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) {
-      if constexpr (V % 2 == 0) rtn_fix_vec<V>(v, a, w);
-      else rtn_exact_vec<V>(v, a, inv_a, 127.0f, w);
+    if constexpr (V % 2 == 0) {
+      if (rtn_fast_vec_x<V>(v, a, inv_a, w)) rtn_fix_vec<V>(v, a, w);
+    } else {
+      if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) rtn_exact_vec<V>(v, a, inv_a, 127.0f, w);
     }
   } else {
 #pragma unroll
@@ -449,7 +450,7 @@ __device__ __forceinline__ uint2 rtn_raw(const uint4& raw, float a, float inv_a,
     float v[V];
     unpack<T>(raw, v);
     uint32_t w[V];
-    if (rtn_fast_vec<V>(v, inv_a, rtn_window(127.0f), w)) return rtn_fix_raw<T>(raw, a, inv_a);
+    if (rtn_fast_vec_x<V>(v, a, inv_a, w)) return rtn_fix_raw<T>(raw, a, inv_a);
     uint2 out;
     out.x = pack4_lo8(w);
     out.y = V == 8 ? pack4_lo8(w + 4) : 0u;
@@ -531,14 +532,36 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   // ---- RTN codes (kernels.cpp:24-40) ----
   // (the codes are not kept in registers: the fallback residual below -- 5-20 %
   // of blocks -- recomputes them, which keeps this variant inside 80 registers)
-  int8_t* cp = p.codes ? p.codes + r0 * p.ldq + cc : nullptr;
+  // (rounding mode and row range decided once per block; the destination
+  // walks by one pointer increment per pass)
+  if (p.codes && col_ok) {
+    int8_t* dst = p.codes + r0 * p.ldq + cc;
+    const int64_t step = (int64_t)RPP * p.ldq;
+    if (mode == 2 && nrow == NP) {
 #pragma unroll
-  for (int ps = 0; ps < NP; ++ps) {
-    const uint2 code = rtn_raw<T>(raw[ps], a, inv_a, mode);
-    if (cp && col_ok && ps < nrow) {
-      int8_t* dst = cp + (int64_t)ps * RPP * p.ldq;
-      if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), code);
-      else __stcs(reinterpret_cast<unsigned int*>(dst), code.x);
+      for (int ps = 0; ps < NP; ++ps, dst += step) {
+        constexpr int VV = 16 / sizeof(T);
+        float v[VV];
+        unpack<T>(raw[ps], v);
+        uint32_t w[VV];
+        uint2 code;
+        if (rtn_fast_vec_x<VV>(v, a, inv_a, w)) {
+          code = rtn_fix_raw<T>(raw[ps], a, inv_a);
+        } else {
+          code.x = pack4_lo8(w);
+          code.y = VV == 8 ? pack4_lo8(w + 4) : 0u;
+        }
+        if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), code);
+        else __stcs(reinterpret_cast<unsigned int*>(dst), code.x);
+      }
+    } else {
+#pragma unroll
+      for (int ps = 0; ps < NP; ++ps, dst += step) {
+        if (ps >= nrow) break;
+        const uint2 code = rtn_raw<T>(raw[ps], a, inv_a, mode);
+        if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), code);
+        else __stcs(reinterpret_cast<unsigned int*>(dst), code.x);
+      }
     }
   }
   // ---- stochastic context planes (quant.cpp:55-84): RNG index (row_offset + r) * cols + c ----
@@ -776,9 +799,10 @@ __device__ __forceinline__ float group_rtn(const float (&x)[V], uint32_t (&w)[V]
     // (a per-element second-level test |d| + |q| 2^-22 >= 1/2 in front of the
     // fix was measured 8 % slower on the GLU forward: the bf16 vectors that
     // fire are mostly genuine near-ties; scripts/ab_glu_refine.sh)
-    if (rtn_fast_vec<V>(x, inv, rtn_window(level), w)) {
-      if constexpr (V % 2 == 0) rtn_fix_vec<V>(x, s, w);
-      else rtn_exact_vec<V>(x, s, inv, level, w);
+    if constexpr (V % 2 == 0) {
+      if (rtn_fast_vec_x<V>(x, s, inv, w)) rtn_fix_vec<V>(x, s, w);
+    } else {
+      if (rtn_fast_vec<V>(x, inv, rtn_window(level), w)) rtn_exact_vec<V>(x, s, inv, level, w);
     }
   } else {
 #pragma unroll
@@ -1329,6 +1353,29 @@ __global__ void fbq_dequantize_kernel(DequantParams p) {
 // context RTN (group_rtn's path, level 511, |x| <= 511 a; out_rtn holds n int16).
 __global__ void fbq_round_probe_kernel(const float* x, const float* a, const uint64_t* bits,
                                        int8_t* out_rtn, int8_t* out_sr, int64_t n, int path) {
+  if (path == 4) {
+    // group_rtn's packed level-511 path (the 10-bit GluCombine contexts): the
+    // 8-wide fast path at window(511) + the packed exact fix (rtn_fix_vec),
+    // one vector per thread with the scale of its first element, int16 out
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n / 8;
+         g += (int64_t)gridDim.x * blockDim.x) {
+      const float ai = a[8 * g];
+      const float inv = ai > 0.0f ? __frcp_rn(ai) : 0.0f;
+      float v[8];
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = x[8 * g + j];
+      if (ai >= kTinyScale) {
+        if (rtn_fast_vec_x<8>(v, ai, inv, w)) rtn_fix_vec<8>(v, ai, w);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = ai > 0.0f ? (uint32_t)rtn_code_slow(v[j], ai, 511.0f) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) reinterpret_cast<int16_t*>(out_rtn)[8 * g + j] = (int16_t)(uint16_t)w[j];
+    }
+    return;
+  }
   if (path == 3) {
     // the 8-wide packed RTN fast path with its two-level boundary test, one
     // vector per thread with the scale of the vector's first element

@@ -43,7 +43,7 @@ def probe(x, a, bits=None, path=0, rtn=True):
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
     ad = torch.from_numpy(np.ascontiguousarray(a)).cuda()
     bd = torch.from_numpy(bits.view(np.int64)).cuda() if bits is not None else None
-    o_r = torch.empty(n, dtype=torch.int16 if path == 2 else torch.int8, device="cuda") if rtn else None
+    o_r = torch.empty(n, dtype=torch.int16 if path in (2, 4) else torch.int8, device="cuda") if rtn else None
     o_s = torch.empty(n, dtype=torch.int8, device="cuda") if bits is not None else None
     K.check(K.lib.fbq_cuda_round_probe(xd.data_ptr(), ad.data_ptr(),
                                        bd.data_ptr() if bd is not None else None,
@@ -110,6 +110,28 @@ def test_rtn_packed_vector_path_near_ties():
     x = np.where(np.isfinite(x), x, 0).astype(np.float32)
     got, _ = probe(x, a, path=3)
     assert np.array_equal(got, ref_rtn(x, a))
+
+
+def test_rtn10_packed_vector_path_near_ties():
+    """Path 4: group_rtn's packed level-511 path (10-bit contexts) -- the fast
+    path's window(511) boundary test and the packed exact fix (parity-denormal
+    tie rule) on vectors sharing one scale: near-ties, exact ties, repeated values."""
+    rng = np.random.default_rng(15)
+    n = 1 << 21
+    g = n // 8
+    e = rng.integers(-140, 60, g)
+    a = np.repeat((rng.uniform(1, 2, g) * 2.0 ** e).astype(np.float32), 8)
+    k = rng.integers(-511, 512, n)
+    half = 0.5 * rng.choice([-1, 1, 0], n)
+    base = ((k + half) * a.astype(np.float64)).astype(np.float32)
+    jit = rng.integers(-3, 4, n).astype(np.int32)
+    x = (base.view(np.int32) + jit).view(np.float32)
+    x[::5] = np.repeat(x[::40], 8)[: x[::5].size]
+    amax = 511 * a.astype(np.float64)
+    x = np.where(np.abs(x.astype(np.float64)) <= amax, x, (np.sign(x) * amax).astype(np.float32))
+    x = np.where(np.isfinite(x), x, 0).astype(np.float32)
+    got, _ = probe(x, a, path=4)
+    assert np.array_equal(got, ref_rtn(x, a, 511))
 
 
 def test_rtn10_context_path():
