@@ -760,6 +760,13 @@ cudaError_t gemm_init() {
 
 static bool gemm_ready(int dev) { return dev >= 0 && g_ring[dev].load(std::memory_order_acquire) != nullptr; }
 
+int* counter_slot() {
+  const int dev = current_device();
+  if (!gemm_ready(dev)) return nullptr;
+  const unsigned slot = g_next_slot[dev].fetch_add(1, std::memory_order_relaxed) % kCounterSlots;
+  return g_ring[dev].load(std::memory_order_acquire) + (size_t)slot * 32;
+}
+
 int gemm_num_sms() {
   const int dev = current_device();
   const int n = dev >= 0 ? g_num_sms[dev].load() : 0;

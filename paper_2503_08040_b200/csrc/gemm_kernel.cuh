@@ -46,5 +46,10 @@ struct GemmParams {
 cudaError_t gemm_init();
 cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream_t s);
 int gemm_num_sms();
+// The next self-resetting 128-byte counter slot of the current device's ring
+// (two ints, both zero at rest; the kernel that uses it leaves them zero), or
+// null before gemm_init() ran on the device.  Shared by the GEMM's and the
+// quantizer's dynamic schedulers.
+int* counter_slot();
 
 }  // namespace fbq

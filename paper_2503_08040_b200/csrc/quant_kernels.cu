@@ -33,6 +33,7 @@
 
 #include "fbq_round.cuh"
 #include "quant_kernels.cuh"
+#include "gemm_kernel.cuh"
 #include "sm100.cuh"
 
 namespace fbq {
@@ -470,6 +471,53 @@ __device__ __forceinline__ float code_of(const uint2& c, int i) {
   return (float)(int8_t)(uint8_t)(w >> (8 * (i & 3)));
 }
 
+// x -> fl(x - fl(c a)) in place, c = RTN code of x (the fallback residual,
+// quant.cpp:150-156).  Fast mode: c from the magic words (n = m - M exactly).
+template <int V>
+__device__ __forceinline__ void residual_vec(float (&v)[V], float a, float inv_a, int mode) {
+  if (mode == 2) {
+    uint32_t w[V];
+    if (rtn_fast_vec_x<V>(v, a, inv_a, w)) rtn_fix_vec<V>(v, a, w);
+    const float2 nmag = make_float2(-kMagic, -kMagic), a2 = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const float2 n = __fadd2_rn(make_float2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), nmag);
+      const float2 rec = __fmul2_rn(n, a2);                       // fl(c * a)
+      const float2 r = __fadd2_rn(make_float2(v[i], v[i + 1]), make_float2(-rec.x, -rec.y));
+      v[i] = r.x;
+      v[i + 1] = r.y;
+    }
+  } else if (mode == 1) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)rtn_code_slow(v[i], a, 127.0f), a));
+  }  // mode 0: a == 0, codes 0, residual = x
+}
+
+// Out of line (flagged blocks only; keeps the main path's registers): the
+// residual's absmax of one raw vector, and its residual RTN codes (packed).
+template <typename T>
+__device__ __noinline__ float residual_absmax_raw(uint4 raw, float a, float inv_a, int mode) {
+  constexpr int V = 16 / sizeof(T);
+  float v[V];
+  unpack<T>(raw, v);
+  residual_vec<V>(v, a, inv_a, mode);
+  float m = 0.0f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+  return m;
+}
+template <typename T>
+__device__ __noinline__ uint2 residual_codes_raw(uint4 raw, float a, float inv_a, int mode, float ra,
+                                                 float inv_ra, int rmode) {
+  constexpr int V = 16 / sizeof(T);
+  float v[V];
+  unpack<T>(raw, v);
+  residual_vec<V>(v, a, inv_a, mode);
+  uint32_t w[V];
+  rtn_vec<V>(v, ra, inv_ra, rmode, w);
+  return make_uint2(pack4_lo8(w), V == 8 ? pack4_lo8(w + 4) : 0u);
+}
+
 // One block's work given its raw values in registers (all threads; contains
 // CTA barriers).
 template <typename T, int kSR = 0>
@@ -592,15 +640,11 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   }
   if (!flagged) return;  // block-uniform
   // ---- fallback residual (quant.cpp:146-172): res = fl(x - fl(c * a)) ----
+  // the primary codes are recomputed from the raw values (not held: 80-register
+  // budget) as magic words, whose n = m - M is the code as a float (no I2F)
   float rm = 0.0f;
 #pragma unroll
-  for (int ps = 0; ps < NP; ++ps) {
-    float v[V];
-    unpack<T>(raw[ps], v);
-    const uint2 code = rtn_raw_call<T>(raw[ps], a, inv_a, mode);
-#pragma unroll
-    for (int i = 0; i < V; ++i) rm = fmaxf(rm, fabsf(__fsub_rn(v[i], __fmul_rn(code_of(code, i), a))));
-  }
+  for (int ps = 0; ps < NP; ++ps) rm = fmaxf(rm, residual_absmax_raw<T>(raw[ps], a, inv_a, mode));
   const float ra = block_scale(block_max(rm, red));
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
   const int rmode = round_mode(ra);
@@ -610,16 +654,10 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
 #pragma unroll
   for (int ps = 0; ps < NP; ++ps) {
     if (ps >= nrow) break;
-    float v[V];
-    unpack<T>(raw[ps], v);
-    const uint2 code = rtn_raw_call<T>(raw[ps], a, inv_a, mode);
-#pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn(code_of(code, i), a));
-    uint32_t w[V];
-    rtn_vec<V>(v, ra, inv_ra, rmode, w);
+    const uint2 code = residual_codes_raw<T>(raw[ps], a, inv_a, mode, ra, inv_ra, rmode);
     int8_t* dst = rp + (int64_t)ps * RPP * p.ldq;
-    if constexpr (V == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(pack4_lo8(w), pack4_lo8(w + 4));
-    else *reinterpret_cast<uint32_t*>(dst) = pack4_lo8(w);
+    if constexpr (V == 8) *reinterpret_cast<uint2*>(dst) = code;
+    else *reinterpret_cast<uint32_t*>(dst) = code.x;
   }
 }
 
@@ -654,6 +692,15 @@ fbq_quantize_reg_kernel(QuantParams p) {
 // Persistent + TMA ring + register compute (bf16): tiles land in a kQStages
 // shared-memory ring by TMA while the CTA quantizes the current tile from
 // registers; a slot is handed back to TMA as soon as its values are in registers.
+// Block schedule: the first kQStages blocks of a CTA are static (blockIdx.x +
+// s * gridDim.x); with p.blk_ctr every further one is claimed from the launch's
+// counter by thread 0 one refill AHEAD (the atomic's latency hides behind a
+// block of rounding), so CTAs that drew flagged (about 3x costlier) blocks take
+// fewer -- the fallback blocks of outlier channels otherwise pile up on the
+// CTAs whose static stride hits their block-column.  A slot's block id travels
+// with its TMA (slot_blk, published before the arrive); -1 ends the CTA.  The
+// counter slot self-resets: every CTA's final claim is past the end, and the
+// last of those zeroes it (same protocol as the GEMM's tile counter).
 template <typename T, int kQStages, int kMinBlocks, int kSR>
 __global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantParams p, int nblk,
@@ -661,10 +708,12 @@ fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantPara
   extern __shared__ __align__(128) uint8_t dsm[];
   T* tiles = reinterpret_cast<T*>(dsm);
   __shared__ __align__(8) uint64_t full[kQStages];
+  __shared__ int slot_blk[kQStages];
   __shared__ float red[kQuantThreads / 32];
   using Tl = Tiling<T>;
   constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   constexpr uint32_t kTileBytes = sizeof(T) * kTileElems;
+  const int static_end = (int64_t)kQStages * gridDim.x < nblk ? kQStages * (int)gridDim.x : nblk;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kQStages; ++s) sm100::mbar_init(full + s, 1);
     sm100::fence_barrier_init();
@@ -672,10 +721,35 @@ fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantPara
   }
   __syncthreads();
   const uint64_t pol = sm100::l2_policy_evict_first();  // X is streamed once
+  // thread 0: the static successor of each slot, or the next dynamic claim
+  int claim = 0;
+  auto next_block = [&](int cur) -> int {
+    if (!p.blk_ctr) return cur + kQStages * (int)gridDim.x;
+    const int b = claim;
+    if (b < nblk) {
+      claim = static_end + atomicAdd(p.blk_ctr, 1);
+      if (claim >= nblk && atomicAdd(p.blk_ctr + 1, 1) == (int)gridDim.x - 1) {
+        atomicExch(p.blk_ctr, 0);  // every CTA made its final claim: reset the slot
+        atomicExch(p.blk_ctr + 1, 0);
+      }
+    }
+    return b;
+  };
   if (threadIdx.x == 0) {
+    if (p.blk_ctr) {
+      claim = static_end + atomicAdd(p.blk_ctr, 1);
+      if (claim >= nblk && atomicAdd(p.blk_ctr + 1, 1) == (int)gridDim.x - 1) {
+        atomicExch(p.blk_ctr, 0);
+        atomicExch(p.blk_ctr + 1, 0);
+      }
+    }
     for (int s = 0; s < kQStages; ++s) {
       const int b = (int)blockIdx.x + s * (int)gridDim.x;
-      if (b >= nblk) break;
+      slot_blk[s] = b < nblk ? b : -1;
+      if (b >= nblk) {
+        sm100::mbar_arrive(full + s);
+        continue;
+      }
       sm100::mbar_arrive_expect_tx(full + s, kTileBytes);
       sm100::tma_load_2d(tiles + s * kTileElems, &map_x, full + s, (b % gcols) * kBlock, (b / gcols) * kBlock, pol);
     }
@@ -683,19 +757,24 @@ fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantPara
   const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
   int s = 0;
   uint32_t phase = 0;
-  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+  for (;;) {
     sm100::mbar_wait(full + s, phase);
+    const int b = slot_blk[s];
+    if (b < 0) break;
     uint4 raw[NP];
     const T* tile = tiles + s * kTileElems + lr * kBlock + lc;
 #pragma unroll
     for (int ps = 0; ps < NP; ++ps) raw[ps] = *reinterpret_cast<const uint4*>(tile + ps * RPP * kBlock);
-    __syncthreads();  // every thread holds its values: slot s goes back to TMA
+    __syncthreads();  // every thread holds its values (and b): slot s goes back to TMA
     if (threadIdx.x == 0) {
-      const int nb = b + kQStages * (int)gridDim.x;
+      const int nb = next_block(b);
+      slot_blk[s] = nb < nblk ? nb : -1;
       if (nb < nblk) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sm100::mbar_arrive_expect_tx(full + s, kTileBytes);
         sm100::tma_load_2d(tiles + s * kTileElems, &map_x, full + s, (nb % gcols) * kBlock, (nb / gcols) * kBlock, pol);
+      } else {
+        sm100::mbar_arrive(full + s);  // no tile: wake the CTA to exit
       }
     }
     if (++s == kQStages) { s = 0; phase ^= 1; }
@@ -1598,8 +1677,11 @@ static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
   const int64_t nblk = (int64_t)gcols * ((p.rows + kBlock - 1) / kBlock);
   int64_t grid = (int64_t)num_sms() * ctas_per_sm;
   if (grid > nblk) grid = nblk;
+  // dynamic block schedule when fbq_cuda_init() set up the counter ring (diag 4096: static)
+  QuantParams q = p;
+  q.blk_ctr = (g_quant_diag & 4096) ? nullptr : counter_slot();
   return launch_ex(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, dim3((unsigned)grid), dim3(kQuantThreads),
-                   smem, s, p.pdl, m, p, (int)nblk, gcols);
+                   smem, s, p.pdl, m, q, (int)nblk, gcols);
 }
 
 template <typename T>

@@ -28,6 +28,7 @@ struct QuantParams {
   int8_t* sr_codes2;       // optional second stochastic plane (own seed), may be null
   uint64_t sr_seed2;
   int64_t row_offset;      // global row of this shard's row 0 (RNG index)
+  int* blk_ctr;            // persistent K1: dynamic block counter slot (counter_slot()), or null
 };
 
 // GluCombine forward fused with the next linear's input quantizer.

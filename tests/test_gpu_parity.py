@@ -318,3 +318,35 @@ def test_mask_topk_device_matches_reference(F, orc, rate):
     tied = rng.choice(np.array([0.0, 0.5, 1.0, 2.0], np.float32), size=(37, 91)).astype(np.float64)
     got = host(F.mask_topk(torch.from_numpy(tied).cuda(), rate))
     assert np.array_equal(got, orc.mask_topk(tied, rate))
+
+
+@pytest.mark.parametrize("rate", [0.0, 0.2])
+def test_quantizer_dynamic_block_schedule(F, orc, rate):
+    """The persistent bf16 K1 claims blocks from a self-resetting counter: its
+    codes, scales, mask and residuals equal the static schedule's (diag 4096)
+    and the oracle's, launch after launch (the counter slot is reused)."""
+    import torch
+    lib = F.K.lib
+    lib.fbq_debug_set_quant_diag.argtypes = [F.K.cint]
+    x = bf16_round(outlier_matrix(2100, 3000, seed=17, channels=[5, 1300], tokens=[7], occasional=40))
+    xt = dev(x).to(torch.bfloat16)
+    scores = orc.score_blocks_absmax(x)
+    mask = orc.mask_topk(scores, rate) if rate > 0 else np.zeros_like(scores, dtype=np.uint8)
+    c, s, rc, rs = orc.fallback_quantize(x, mask)
+    outs = []
+    try:
+        for d in (0, 4096, 0, 0):
+            lib.fbq_debug_set_quant_diag(d)
+            fa = F.fallback_quantize(xt, dev(mask))
+            outs.append(fa)
+    finally:
+        lib.fbq_debug_set_quant_diag(0)
+    for fa in outs:
+        assert np.array_equal(host(fa.primary.codes_int16()), c)
+        assert np.array_equal(host(fa.primary.scales).view(np.int32), s.view(np.int32))
+        for bi, bj in zip(*np.nonzero(mask)):
+            r0, c0 = bi * 128, bj * 128
+            got = host(fa.res_codes[r0:r0 + 128, c0:min(c0 + 128, x.shape[1])].to(torch.int16))
+            assert np.array_equal(got, rc[r0:r0 + 128, c0:c0 + 128])
+        assert np.array_equal(host(fa.res_scales)[mask.astype(bool)].view(np.int32),
+                              rs[mask.astype(bool)].view(np.int32))
