@@ -85,11 +85,17 @@ static_assert(kSmemBytes <= 232448, "shared memory budget");
 // With kGroupM groups everywhere the gate/up forward re-read all of B once per
 // group (1.03 GB of DRAM reads for 0.15 GB of operands, ncu).
 constexpr int kGroupM = 8;
+//  * n_fastest = c > 0: bn fastest inside chunks of c n-tiles (c >= NT: the
+//    whole N), chunk after chunk -- one pinned chunk of B, A streamed once per chunk.
 __device__ __forceinline__ void tile_coords(int tile, int MB, int NT, int group_m, int n_fastest,
                                             int& bm, int& bn2) {
   if (n_fastest) {
-    bm = tile / NT;
-    bn2 = tile - bm * NT;
+    const int c = n_fastest < NT ? n_fastest : NT;
+    const int chunk = tile / (MB * c);
+    const int in = tile - chunk * (MB * c);
+    const int width = c < NT - chunk * c ? c : NT - chunk * c;  // the last chunk may be narrower
+    bm = in / width;
+    bn2 = chunk * c + (in - bm * width);
     return;
   }
   const int per_group = group_m * NT;
@@ -845,19 +851,30 @@ cudaError_t launch_gemm(const GemmOperands& o, GemmParams p, int epi, cudaStream
     const double a_bytes = (double)p.M * (double)p.K, b_bytes = (double)p.N * (double)p.K;
     p.group_m = kGroupM;
     p.n_fastest = 0;
+    const int NTt = (p.NB + 1) / 2;
     if (p.diag & (1 << 19)) p.group_m = p.MB;          // diagnostics/tests: force each raster
-    else if (p.diag & (1 << 20)) p.n_fastest = 1;
+    else if (p.diag & (1 << 20)) p.n_fastest = NTt;
+    else if (p.diag & (1 << 17)) p.n_fastest = (NTt + 2) / 3;  // tests: B in chunks of ~NT/3
     else if (!(p.diag & (1 << 18))) {  // diagnostics: 1 << 18 = always kGroupM groups
       const double small = a_bytes < b_bytes ? a_bytes : b_bytes;
       const double large = a_bytes < b_bytes ? b_bytes : a_bytes;
+      const double b_panel = 256.0 * (double)p.K;  // bytes of one 256-wide B n-tile over K
       if (small <= kPin && large > kPin) {
         if (a_bytes <= b_bytes) p.group_m = p.MB;
-        else p.n_fastest = 1;
+        else p.n_fastest = NTt;
       } else if (large <= kPin) {
-        p.n_fastest = 1;
+        p.n_fastest = NTt;
       } else if (a_bytes <= kPinMax && b_bytes > a_bytes) {
         const int g = (int)(kGroupBytes / (128.0 * (double)p.K));
         p.group_m = g < kGroupM ? kGroupM : (g > p.MB ? p.MB : g);
+      } else if (b_bytes <= a_bytes && b_panel <= kPin && !(p.diag & (1 << 27))) {
+        // both operands too large to pin, B the smaller: B in equal chunks that
+        // fit the pin capacity, each chunk's every tile (bn fastest) before the
+        // next, so A streams once per chunk and each B chunk once (dX =
+        // dG W_gu: A 235 MB, B 117 MB -> two 58 MB chunks; diag 1 << 27: groups)
+        const int nmax = (int)(kPin / b_panel);
+        const int nchunks = (NTt + nmax - 1) / nmax;
+        p.n_fastest = (NTt + nchunks - 1) / nchunks;
       }
     }
   }

@@ -278,7 +278,7 @@ def test_gemm_many_tiles_odd_pairs(F, orc):
     assert rel_fro(host(y2), want) <= FMA_TOL
 
 
-@pytest.mark.parametrize("raster", [1 << 18, 1 << 19, 1 << 20])
+@pytest.mark.parametrize("raster", [1 << 17, 1 << 18, 1 << 19, 1 << 20])
 def test_gemm_tile_rasters(F, orc, raster):
     """Every tile rasterisation the launcher may pick (kGroupM groups, bm over
     all block-rows, bn fastest) covers each tile exactly once: bit-exact on a
