@@ -1184,33 +1184,86 @@ fbq_glu_backward_kernel(GluBwdParams g) {
 // ------------------------------------------------------------------ RMSNorm
 // RmsNorm (trainsim.cpp:154-211) with its 10-bit 1 x 128 input context.
 // The reference accumulates every row's sum of squares (and, backward, the
-// gain-weighted dot product) SEQUENTIALLY in double; to reproduce those exact
-// roundings one thread owns one row and walks the columns in order, reading
-// 128-row x 32-column tiles staged through shared memory (coalesced loads,
-// +1 padding against bank conflicts).  Everything per element is parallel.
-constexpr int kRmsRows = 128, kRmsCols = 32;
+// gain-weighted dot product) SEQUENTIALLY in double, and grad_gain over the
+// rows in order in float; to reproduce those exact roundings each sum is one
+// thread's dependent chain.  There are only rows (or cols) such chains, so the
+// kernels are built to keep enough bytes in flight per chain: a lane owns a
+// row and reads it from a cp.async ring of [32 rows x 128 columns] tiles (row
+// statistics), or owns a column of a warp's 32 and reads [kGgRows x 32] tiles
+// of the per-element grad_gain terms from a cp.async ring (grad_gain).
+
+// Row statistics: one warp per 32 rows, lane = row, columns in order.  The
+// rows are streamed through a kRsStages ring of [32 rows x 128 columns] shared
+// memory tiles filled by cp.async in row-contiguous 16-byte pieces (each warp
+// instruction moves two 256-byte row segments, so HBM sees long runs; a lane
+// loading its own row 16 bytes at a time opened a DRAM page per access and ran
+// at 0.3 TB/s); rows are padded by 16 bytes so each lane's LDS.128 of its row
+// hits its own banks.
+constexpr int kRsCols = 128, kRsStages = 6;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool pred) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Fill stage rows [r0, r0 + 32) x columns [c0, c0 + kRsCols) of a row-major
+// T matrix into smem (row stride RS bytes); out-of-range pieces are zeros.
+template <typename T, int RS>
+__device__ __forceinline__ void rs_fill(uint8_t* dst, const T* src, int64_t ld, int64_t rows, int64_t cols,
+                                        int64_t r0, int64_t c0) {
+  constexpr int PPR = kRsCols * (int)sizeof(T) / 16;  // 16-byte pieces per row
+  constexpr int EPP = 16 / (int)sizeof(T);
+  for (int i = threadIdx.x; i < 32 * PPR; i += 32) {
+    const int rr = i / PPR, pc = i % PPR;
+    const int64_t r = r0 + rr, c = c0 + (int64_t)pc * EPP;
+    const bool ok = r < rows && c < cols;  // cols % 8 == 0 keeps pieces whole
+    cp_async16(dst + rr * RS + pc * 16, src + (ok ? r * ld + c : 0), ok);
+  }
+}
 
 template <typename T>
-__global__ void __launch_bounds__(kRmsRows)
+__global__ void __launch_bounds__(32)
 fbq_rms_rowstat_fwd_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
                            float* __restrict__ rms) {
-  __shared__ float tile[kRmsRows][kRmsCols + 1];
-  const int64_t r0 = (int64_t)blockIdx.x * kRmsRows;
-  double ss = 0.0;
-  for (int64_t c0 = 0; c0 < cols; c0 += kRmsCols) {
-    for (int i = threadIdx.x; i < kRmsRows * kRmsCols; i += kRmsRows) {
-      const int rr = i / kRmsCols, cc = i % kRmsCols;
-      const int64_t r = r0 + rr, c = c0 + cc;
-      tile[rr][cc] = (r < rows && c < cols) ? to_f32(x[r * ldx + c]) : 0.0f;
-    }
-    __syncthreads();
-    const int n = cols - c0 < kRmsCols ? (int)(cols - c0) : kRmsCols;
-    for (int cc = 0; cc < n; ++cc) {
-      const double v = (double)tile[threadIdx.x][cc];
-      ss = __fma_rn(v, v, ss);  // v*v is exact in double: == ss + v*v (trainsim.cpp:160-163)
-    }
-    __syncthreads();
+  constexpr int RS = kRsCols * (int)sizeof(T) + 16;
+  constexpr int E = 16 / (int)sizeof(T);
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int64_t nch = (cols + kRsCols - 1) / kRsCols;
+#pragma unroll
+  for (int k = 0; k < kRsStages - 1; ++k) {
+    if (k < nch) rs_fill<T, RS>(rsm + k * 32 * RS, x, ldx, rows, cols, r0, (int64_t)k * kRsCols);
+    cp_async_commit();
   }
+  double ss = 0.0;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int64_t pre = ch + kRsStages - 1;
+    if (pre < nch) rs_fill<T, RS>(rsm + (pre % kRsStages) * 32 * RS, x, ldx, rows, cols, r0, pre * kRsCols);
+    cp_async_commit();
+    cp_async_wait<kRsStages - 1>();
+    __syncwarp();
+    const uint8_t* row = rsm + (ch % kRsStages) * 32 * RS + threadIdx.x * RS;
+#pragma unroll 4
+    for (int pc = 0; pc < kRsCols / E; ++pc) {
+      float v[E];
+      unpack<T>(*reinterpret_cast<const uint4*>(row + pc * 16), v);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double d = (double)v[e];  // zero fill past the end adds exactly nothing
+        ss = __fma_rn(d, d, ss);         // d*d is exact in double: == ss + d*d (trainsim.cpp:160-163)
+      }
+    }
+    __syncwarp();  // the stage is refilled by a later iteration
+  }
+  cp_async_wait<0>();
   const int64_t r = r0 + threadIdx.x;
   if (r < rows)  // sqrt(float(ss / cols) + eps) in float (trainsim.cpp:164-165)
     rms[r] = __fsqrt_rn(__fadd_rn(__double2float_rn(__ddiv_rn(ss, (double)cols)), 1e-6f));
@@ -1264,38 +1317,85 @@ fbq_rms_apply_fwd_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, in
 
 // backward row statistics (trainsim.cpp:186-199), sequential per row in double:
 // x = dequantize(ctx); ss = sum x^2; dot = sum fl(fl(g*dy)*x); rms = sqrt(ss/cols
-// + eps); inv = 1 / rms; corr = dot / (((cols*rms)*rms)*rms)
+// + eps); inv = 1 / rms; corr = dot / (((cols*rms)*rms)*rms).  Lane = row; the
+// codes, dy, the block's scale per row and the chunk's gains stream through a
+// kRsBwdStages cp.async ring like the forward.
+constexpr int kRsBwdStages = 4;
 template <typename T>
-__global__ void __launch_bounds__(kRmsRows)
+struct RsBwdLayout {
+  static constexpr int RSC = kRsCols * 2 + 16;                    // code row stride (bytes)
+  static constexpr int RSD = kRsCols * (int)sizeof(T) + 16;       // dy row stride
+  static constexpr int kCodes = 0, kDy = 32 * RSC, kScale = kDy + 32 * RSD, kGain = kScale + 32 * 4;
+  static constexpr int kStage = kGain + kRsCols * 4;
+};
+template <typename T>
+__global__ void __launch_bounds__(32)
 fbq_rms_rowstat_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
                            const float* __restrict__ ctx_scales, const T* __restrict__ gy,
                            int64_t ldgy, int64_t rows, int64_t cols, const float* __restrict__ gain,
                            double* __restrict__ inv_out, double* __restrict__ corr_out) {
-  __shared__ float tx[kRmsRows][kRmsCols + 1];
-  __shared__ float tg[kRmsRows][kRmsCols + 1];
-  const int64_t r0 = (int64_t)blockIdx.x * kRmsRows;
+  using L = RsBwdLayout<T>;
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const int lane = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int64_t gcols = (cols + kBlock - 1) / kBlock;
-  double ss = 0.0, dot = 0.0;
-  for (int64_t c0 = 0; c0 < cols; c0 += kRmsCols) {
-    for (int i = threadIdx.x; i < kRmsRows * kRmsCols; i += kRmsRows) {
-      const int rr = i / kRmsCols, cc = i % kRmsCols;
-      const int64_t r = r0 + rr, c = c0 + cc;
-      const bool ok = r < rows && c < cols;
-      // dequantize: fl(code * scale) (quant.cpp:86-104)
-      tx[rr][cc] = ok ? __fmul_rn((float)ctx[r * ld_ctx + c], ctx_scales[r * gcols + c / kBlock]) : 0.0f;
-      tg[rr][cc] = ok ? to_f32(gy[r * ldgy + c]) : 0.0f;
+  const int64_t nch = (cols + kRsCols - 1) / kRsCols;  // kRsCols == kBlock: one scale per row per chunk
+  auto fill = [&](int sidx, int64_t ch) {
+    uint8_t* st = rsm + sidx * L::kStage;
+    const int64_t c0 = ch * kRsCols;
+    rs_fill<int16_t, L::RSC>(st + L::kCodes, ctx, ld_ctx, rows, cols, r0, c0);
+    rs_fill<T, L::RSD>(st + L::kDy, gy, ldgy, rows, cols, r0, c0);
+    const int64_t r = r0 + lane;
+    cp_async4(st + L::kScale + lane * 4, ctx_scales + (r < rows ? r * gcols + ch : 0), r < rows);
+    for (int i = lane; i < kRsCols / 4; i += 32) {
+      const bool ok = c0 + i * 4 < cols;
+      cp_async16(st + L::kGain + i * 16, gain + (ok ? c0 + i * 4 : 0), ok);
     }
-    __syncthreads();
-    const int n = cols - c0 < kRmsCols ? (int)(cols - c0) : kRmsCols;
-    for (int cc = 0; cc < n; ++cc) {
-      const double v = (double)tx[threadIdx.x][cc];
-      ss = __fma_rn(v, v, ss);
-      const double h = __dmul_rn((double)gain[c0 + cc], (double)tg[threadIdx.x][cc]);
-      dot = __dadd_rn(dot, __dmul_rn(h, v));
-    }
-    __syncthreads();
+  };
+#pragma unroll
+  for (int k = 0; k < kRsBwdStages - 1; ++k) {
+    if (k < nch) fill(k, k);
+    cp_async_commit();
   }
-  const int64_t r = r0 + threadIdx.x;
+  double ss = 0.0, dot = 0.0;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int64_t pre = ch + kRsBwdStages - 1;
+    if (pre < nch) fill((int)(pre % kRsBwdStages), pre);
+    cp_async_commit();
+    cp_async_wait<kRsBwdStages - 1>();
+    __syncwarp();
+    const uint8_t* st = rsm + (ch % kRsBwdStages) * L::kStage;
+    const uint8_t* crow = st + L::kCodes + lane * L::RSC;
+    const uint8_t* drow = st + L::kDy + lane * L::RSD;
+    const float sc = *reinterpret_cast<const float*>(st + L::kScale + lane * 4);
+    const float* gv = reinterpret_cast<const float*>(st + L::kGain);
+#pragma unroll 2
+    for (int pc = 0; pc < kRsCols / 8; ++pc) {  // 8 columns per step
+      const uint4 cw4 = *reinterpret_cast<const uint4*>(crow + pc * 16);
+      const uint32_t cw[4] = {cw4.x, cw4.y, cw4.z, cw4.w};
+      float dy[8];
+      if constexpr (sizeof(T) == 2) {
+        unpack<T>(*reinterpret_cast<const uint4*>(drow + pc * 16), dy);
+      } else {
+        float lo[4], hi[4];
+        unpack<float>(*reinterpret_cast<const uint4*>(drow + pc * 32), lo);
+        unpack<float>(*reinterpret_cast<const uint4*>(drow + pc * 32 + 16), hi);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { dy[e] = lo[e]; dy[4 + e] = hi[e]; }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int code = (int)(int16_t)(cw[e >> 1] >> (16 * (e & 1)));
+        const double v = (double)__fmul_rn((float)code, sc);  // dequantize: fl(code * scale)
+        ss = __fma_rn(v, v, ss);                               // zero-filled columns add nothing
+        const double h = __dmul_rn((double)gv[pc * 8 + e], (double)dy[e]);
+        dot = __dadd_rn(dot, __dmul_rn(h, v));
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  const int64_t r = r0 + lane;
   if (r < rows) {
     const double rms = __dsqrt_rn(__dadd_rn(__ddiv_rn(ss, (double)cols), (double)1e-6f));
     inv_out[r] = __ddiv_rn(1.0, rms);
@@ -1328,37 +1428,84 @@ __global__ void fbq_rms_apply_bwd_kernel(const int16_t* __restrict__ ctx, int64_
 }
 
 // grad_gain[c] += term[r][c] for r = 0, 1, ... in order (float adds, the
-// reference's accumulation order); loads run far ahead of the add chain.
-__global__ void fbq_rms_grad_gain_kernel(const float* __restrict__ term, int64_t rows, int64_t cols,
-                                         float* __restrict__ grad_gain) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float acc = grad_gain[c];
-  int64_t r = 0;
-  for (; r + 8 <= rows; r += 8) {
-    float t[8];
+// reference's accumulation order).  Only `cols` chains exist, so a warp owns 32
+// columns and streams [kGgRows x 32] chunks of `term` through a kGgStages
+// cp.async ring: each lane's add chain (4 cycles per row) never waits on HBM.
+constexpr int kGgRows = 64, kGgStages = 5;  // 40 KB of static shared memory
+__global__ void __launch_bounds__(32)
+fbq_rms_grad_gain_kernel(const float* __restrict__ term, int64_t rows, int64_t cols,
+                         float* __restrict__ grad_gain) {
+  __shared__ __align__(16) float st[kGgStages][kGgRows][32];
+  const int lane = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * 32, c = c0 + lane;
+  const bool cok = c < cols;
+  const int64_t nch = (rows + kGgRows - 1) / kGgRows;
+  auto fill = [&](int sidx, int64_t ch) {
+    // kGgRows rows x 128 B = 8 pieces per row; cols % 8 == 0 keeps pieces whole
+    for (int i = lane; i < kGgRows * 8; i += 32) {
+      const int rr = i >> 3, pc = i & 7;
+      const int64_t r = ch * kGgRows + rr, col = c0 + pc * 4;
+      const bool ok = r < rows && col < cols;
+      cp_async16(&st[sidx][rr][pc * 4], term + (ok ? r * cols + col : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
 #pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = term[(r + j) * cols + c];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc = __fadd_rn(acc, t[j]);
+  for (int k = 0; k < kGgStages - 1; ++k) {
+    if (k < nch) fill(k, k);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  for (; r < rows; ++r) acc = __fadd_rn(acc, term[r * cols + c]);
-  grad_gain[c] = acc;
+  float acc = cok ? grad_gain[c] : 0.0f;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int64_t pre = ch + kGgStages - 1;
+    if (pre < nch) fill((int)(pre % kGgStages), pre);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGgStages - 1) : "memory");
+    __syncwarp();
+    const float(*t)[32] = st[ch % kGgStages];
+    const int nr = rows - ch * kGgRows < kGgRows ? (int)(rows - ch * kGgRows) : kGgRows;
+    if (nr == kGgRows) {
+#pragma unroll 16
+      for (int rr = 0; rr < kGgRows; ++rr) acc = __fadd_rn(acc, t[rr][lane]);
+    } else {
+      for (int rr = 0; rr < nr; ++rr) acc = __fadd_rn(acc, t[rr][lane]);
+    }
+    __syncwarp();  // this stage is refilled by the next iteration's prefetch
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (cok) grad_gain[c] = acc;
+}
+
+// per-device one-time opt-in to `bytes` of dynamic shared memory for kernel K
+template <auto K>
+static cudaError_t smem_once(size_t bytes) {
+  static std::once_flag flag[64];
+  static cudaError_t err[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::call_once(flag[dev], [&] {
+    err[dev] = bytes > 48 * 1024 ? cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
+                                 : cudaSuccess;
+  });
+  return err[dev];
 }
 
 cudaError_t launch_rmsnorm_forward(const void* x, bool bf16, int64_t rows, int64_t cols, int64_t ldx,
                                    const float* gain, void* y, int64_t ldy, int16_t* ctx,
                                    int64_t ld_ctx, float* ctx_scales, float* rms, cudaStream_t s) {
-  const unsigned rb = (unsigned)((rows + kRmsRows - 1) / kRmsRows);
+  const unsigned rb = (unsigned)((rows + 31) / 32);  // one warp per 32 rows
   const dim3 grid((unsigned)((cols + kBlock - 1) / kBlock), (unsigned)((rows + kBlock - 1) / kBlock));
+  const size_t sm16 = (size_t)kRsStages * 32 * (kRsCols * 2 + 16), sm32 = (size_t)kRsStages * 32 * (kRsCols * 4 + 16);
+  if (cudaError_t e = smem_once<fbq_rms_rowstat_fwd_kernel<__nv_bfloat16>>(sm16)) return e;
+  if (cudaError_t e = smem_once<fbq_rms_rowstat_fwd_kernel<float>>(sm32)) return e;
   if (bf16) {
-    fbq_rms_rowstat_fwd_kernel<__nv_bfloat16><<<rb, kRmsRows, 0, s>>>(
+    fbq_rms_rowstat_fwd_kernel<__nv_bfloat16><<<rb, 32, sm16, s>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), rows, cols, ldx, rms);
     fbq_rms_apply_fwd_kernel<__nv_bfloat16><<<grid, kQuantThreads, 0, s>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), rows, cols, ldx, gain, rms,
         reinterpret_cast<__nv_bfloat16*>(y), ldy, ctx, ld_ctx, ctx_scales, 511.0f);
   } else {
-    fbq_rms_rowstat_fwd_kernel<float><<<rb, kRmsRows, 0, s>>>(reinterpret_cast<const float*>(x), rows,
+    fbq_rms_rowstat_fwd_kernel<float><<<rb, 32, sm32, s>>>(reinterpret_cast<const float*>(x), rows,
                                                               cols, ldx, rms);
     fbq_rms_apply_fwd_kernel<float><<<grid, kQuantThreads, 0, s>>>(
         reinterpret_cast<const float*>(x), rows, cols, ldx, gain, rms, reinterpret_cast<float*>(y),
@@ -1371,7 +1518,11 @@ cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const fl
                                     const void* gy, bool bf16, int64_t rows, int64_t cols,
                                     int64_t ldgy, const float* gain, void* gx, int64_t ldgx,
                                     float* grad_gain, double* row_ws, float* term, cudaStream_t s) {
-  const unsigned rb = (unsigned)((rows + kRmsRows - 1) / kRmsRows);
+  const unsigned rb = (unsigned)((rows + 31) / 32);  // one warp per 32 rows
+  const size_t sm16 = (size_t)kRsBwdStages * RsBwdLayout<__nv_bfloat16>::kStage;
+  const size_t sm32 = (size_t)kRsBwdStages * RsBwdLayout<float>::kStage;
+  if (cudaError_t e = smem_once<fbq_rms_rowstat_bwd_kernel<__nv_bfloat16>>(sm16)) return e;
+  if (cudaError_t e = smem_once<fbq_rms_rowstat_bwd_kernel<float>>(sm32)) return e;
   double* inv = row_ws;
   double* corr = row_ws + rows;
   const int64_t n = rows * cols;
@@ -1379,20 +1530,20 @@ cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const fl
   if (blocks < 1) blocks = 1;
   if (bf16) {
     auto g = reinterpret_cast<const __nv_bfloat16*>(gy);
-    fbq_rms_rowstat_bwd_kernel<__nv_bfloat16><<<rb, kRmsRows, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy,
+    fbq_rms_rowstat_bwd_kernel<__nv_bfloat16><<<rb, 32, sm16, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy,
                                                                       rows, cols, gain, inv, corr);
     fbq_rms_apply_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
         ctx, ld_ctx, ctx_scales, g, ldgy, rows, cols, gain, inv, corr,
         reinterpret_cast<__nv_bfloat16*>(gx), ldgx, term);
   } else {
     auto g = reinterpret_cast<const float*>(gy);
-    fbq_rms_rowstat_bwd_kernel<float><<<rb, kRmsRows, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows,
+    fbq_rms_rowstat_bwd_kernel<float><<<rb, 32, sm32, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows,
                                                               cols, gain, inv, corr);
     fbq_rms_apply_bwd_kernel<float><<<blocks, 256, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows, cols,
                                                            gain, inv, corr, reinterpret_cast<float*>(gx),
                                                            ldgx, term);
   }
-  fbq_rms_grad_gain_kernel<<<(unsigned)((cols + 127) / 128), 128, 0, s>>>(term, rows, cols, grad_gain);
+  fbq_rms_grad_gain_kernel<<<(unsigned)((cols + 31) / 32), 32, 0, s>>>(term, rows, cols, grad_gain);
   return cudaGetLastError();
 }
 
