@@ -558,6 +558,28 @@ def gemm_sweep(device):
 
 
 # ----------------------------------------------------------------- C3 comparators
+def rmsnorm_perf(device, T=TOKENS, D=D_MODEL, reps=20):
+    """RmsNorm (trainsim.cpp:154-211) fwd and bwd at the Llama-3.1-8B
+    block input (T x d_model, bf16): the sequential per-row double sums
+    (bit-exact with the reference) + the element-parallel parts.  Bytes moved:
+    fwd x twice (row statistics, apply) + y + the int16 context; bwd codes + dy
+    twice, dx, and the fp32 grad_gain terms written and re-read."""
+    import torch
+    from paper_2503_08040_b200 import fbq
+    x = make_activations(T, D, 3, device, torch.bfloat16)
+    gy = (torch.randn(T, D, device=device) * 1e-3).to(torch.bfloat16)
+    n = fbq.RmsNorm(D)
+    tf = _event_time(lambda: n.forward(x), reps, 3) * 1e-3  # seconds
+    tb = _event_time(lambda: n.backward(gy), reps, 3) * 1e-3
+    e = T * D
+    fb, bb = e * (2 + 2 + 2 + 2), e * (2 + 2 + 2 + 2 + 2 + 4 + 4)
+    return {"workload": f"RmsNorm fwd / bwd, {T} x {D} bf16, 10-bit 1x128 context, bit-exact sequential "
+                        "double row sums (reference order)",
+            "fwd_us": round(tf * 1e6, 1), "bwd_us": round(tb * 1e6, 1),
+            "fwd_GBps": round(fb / tf / 1e9, 0), "bwd_GBps": round(bb / tb / 1e9, 0),
+            "round1_fwd_us": 1496.0, "round1_bwd_us": 1508.0}
+
+
 def _event_time(fn, steps, warmup):
     import torch
     for _ in range(warmup):
@@ -891,7 +913,7 @@ def run_ours(args, rank, world, local):
                 ctxmem = context_memory(device, T)
             except Exception as ex:  # pragma: no cover
                 ctxmem = {"error": str(ex)[:200]}
-        sweep = qsweep = c4 = None
+        sweep = qsweep = c4 = rms = None
         if not args.no_sweep and world == 1:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
                 qsweep = quant_sweep(device, peaks.get("hbm_gbs", 6522.1))
@@ -901,6 +923,10 @@ def run_ours(args, rank, world, local):
                 sweep = gemm_sweep(device)
             except Exception as ex:  # pragma: no cover
                 sweep = {"error": str(ex)[:200]}
+            try:
+                rms = rmsnorm_perf(device)
+            except Exception as ex:  # pragma: no cover
+                rms = {"error": str(ex)[:200]}
             try:
                 c5_dp = c5_fallback_gemm(device)
             except Exception as ex:  # pragma: no cover
@@ -960,6 +986,7 @@ def run_ours(args, rank, world, local):
             "quant_sweep": qsweep,
             "qwen_block_c4": c4 if world == 1 else c4_dp,
             "c5_fallback_gemm_dp": c5_dp,
+            "rmsnorm": rms,
         }
         print(json.dumps(result), flush=True)
     if world > 1:
