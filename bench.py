@@ -37,9 +37,11 @@ REF_SAMPLE_TOKENS = 1024  # bounded CPU sample (tokens per reference step; the r
 # fixed per-step weight quantization is amortised over >= 1024 tokens)
 
 
-# GluCombine a / b contexts stored at 10 bits (1.25 B/code) --
-# lossless for |code| <= 511, bit-exact with the reference's int16 storage
-CTX_PACKED = True
+# GluCombine a / b contexts: int16 containers (the reference's QuantizedTensor
+# storage) for the headline -- interleaved A/B on one box (scripts/ctx_ab.py)
+# measured the packed 10-bit storage (1.25 B/code, bit-exact too)
+# ~2 % slower; context_memory() reports its bytes and rate
+CTX_PACKED = False
 
 
 def parse():
