@@ -609,11 +609,41 @@ def rmsnorm_perf(device, T=TOKENS, D=D_MODEL, reps=20):
     tb = _event_time(lambda: n.backward(gy), reps, 3) * 1e-3
     e = T * D
     fb, bb = e * (2 + 2 + 2 + 2), e * (2 + 2 + 2 + 2 + 2 + 4 + 4)
+    # RmsNorm -> the next linear's input quantizer (threshold, two SR context
+    # planes, as the gate/up X): unfused (y through HBM) vs fused
+    from paper_2503_08040_b200 import _capi as K
+    theta = float(fbq.score_blocks(n.forward(x)).flatten().float().quantile(0.85).item())
+    nb = (T // 128) * (D // 128)
+    codes = torch.empty(T, D, dtype=torch.int8, device=device)
+    res, sr1, sr2 = torch.empty_like(codes), torch.empty_like(codes), torch.empty_like(codes)
+    sc, rsc = torch.empty(nb, device=device), torch.empty(nb, device=device)
+    bits = torch.empty((nb + 31) // 32, dtype=torch.int32, device=device)
+    cnt = torch.empty(1, dtype=torch.int32, device=device)
+    ctx = torch.empty(T, D, dtype=torch.int16, device=device)
+    ctx_s, rms = torch.empty(T, D // 128, device=device), torch.empty(T, device=device)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def unfused():
+        y = n.forward(x)
+        K.call("fbq_cuda_quantize_linear_input", y.data_ptr(), K.FBQ_BF16, T, D, D, K.FBQ_MASK_THRESHOLD, theta,
+               None, bits.data_ptr(), codes.data_ptr(), D, sc.data_ptr(), res.data_ptr(), rsc.data_ptr(),
+               cnt.data_ptr(), sr1.data_ptr(), 11, sr2.data_ptr(), 12, 0, st)
+
+    def fused():
+        K.call("fbq_cuda_rmsnorm_quantize_input", x.data_ptr(), K.FBQ_BF16, T, D, D, n.gain.data_ptr(),
+               ctx.data_ptr(), D, ctx_s.data_ptr(), rms.data_ptr(), K.FBQ_MASK_THRESHOLD, theta, None,
+               bits.data_ptr(), codes.data_ptr(), D, sc.data_ptr(), res.data_ptr(), rsc.data_ptr(),
+               cnt.data_ptr(), sr1.data_ptr(), 11, sr2.data_ptr(), 12, 0, st)
+    tu = _event_time(unfused, reps, 3) * 1e-3
+    tz = _event_time(fused, reps, 3) * 1e-3
     return {"workload": f"RmsNorm fwd / bwd, {T} x {D} bf16, 10-bit 1x128 context, bit-exact sequential "
                         "double row sums (reference order)",
             "fwd_us": round(tf * 1e6, 1), "bwd_us": round(tb * 1e6, 1),
             "fwd_GBps": round(fb / tf / 1e9, 0), "bwd_GBps": round(bb / tb / 1e9, 0),
-            "round1_fwd_us": 1496.0, "round1_bwd_us": 1508.0}
+            "round1_fwd_us": 1496.0, "round1_bwd_us": 1508.0,
+            "fwd_plus_input_quantizer_us": {"unfused": round(tu * 1e6, 1), "fused": round(tz * 1e6, 1),
+                                            "note": "threshold fallback + two int8 SR context planes of y; "
+                                                    "fused: y never materialised (-64 MB)"}}
 
 
 def _event_time(fn, steps, warmup):

@@ -104,6 +104,23 @@ int fbq_cuda_block_absmax(const void* x, int dtype, int64_t rows, int64_t cols, 
 int fbq_cuda_rmsnorm_forward(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
                              const float* gain, void* y, int64_t ldy, int16_t* ctx_codes,
                              int64_t ld_ctx, float* ctx_scales, float* rms_ws, fbq_stream_t stream);
+/* RmsNorm::forward fused with the next QuantLinearLayer's input quantizer
+ * (the transformer block's RMSNorm -> q/k/v or gate/up, trainsim.cpp:294-301,
+ * SURVEY 8f-2): writes the RmsNorm context (ctx_codes / ctx_scales, as
+ * fbq_cuda_rmsnorm_forward) and, for y = fl(fl(x / rms) * gain) rounded to the
+ * activation dtype, exactly the outputs of fbq_cuda_quantize_linear_input(y, ...)
+ * -- RTN codes, scales, fallback mask / count, residual plane, up to two
+ * stochastic context planes -- without materialising y.  Same argument rules
+ * as those two entry points (cols % 8 == 0, 16-byte aligned rows, ldq % 16 == 0). */
+int fbq_cuda_rmsnorm_quantize_input(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                                    const float* gain, int16_t* ctx_codes, int64_t ld_ctx,
+                                    float* ctx_scales, float* rms_ws, int mask_mode, double theta,
+                                    const double* theta_dev, uint32_t* mask_bits, int8_t* codes,
+                                    int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
+                                    int32_t* masked_count, int8_t* sr_codes, uint64_t sr_seed,
+                                    int8_t* sr_codes2, uint64_t sr_seed2, int64_t row_offset,
+                                    fbq_stream_t stream);
+
 int fbq_cuda_rmsnorm_backward(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales,
                               const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
                               const float* gain, void* gx, int64_t ldgx, float* grad_gain,

@@ -46,6 +46,10 @@ _SIGS = {
     "fbq_cuda_quantize_stochastic": (cint, [vp, cint, i64, i64, i64, u64, i64, vp, i64, vp, vp]),
     "fbq_cuda_gemm": (cint, [vp, i64, vp, cint, vp, i64, vp, cint, vp, vp, vp, i64, i64, i64, vp,
                              cint, i64, cint, cint, vp]),
+    "fbq_cuda_quantize_linear_input": (cint, [vp, cint, i64, i64, i64, cint, dbl, vp, vp, vp, i64, vp, vp, vp,
+                                              vp, vp, u64, vp, u64, i64, vp]),
+    "fbq_cuda_rmsnorm_quantize_input": (cint, [vp, cint, i64, i64, i64, vp, vp, i64, vp, vp, cint, dbl, vp,
+                                               vp, vp, i64, vp, vp, vp, vp, vp, u64, vp, u64, i64, vp]),
     "fbq_cuda_gemm_block_products": (cint, [vp, i64, cint, vp, i64, cint, vp, vp, i64, i64, i64,
                                             vp, vp]),
     "fbq_cuda_dequantize": (cint, [vp, i64, vp, vp, vp, vp, i64, i64, vp, i64, vp]),

@@ -256,6 +256,33 @@ int fbq_cuda_rmsnorm_forward(const void* x, int dtype, int64_t rows, int64_t col
                                                  reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int fbq_cuda_rmsnorm_quantize_input(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
+                                    const float* gain, int16_t* ctx_codes, int64_t ld_ctx,
+                                    float* ctx_scales, float* rms_ws, int mask_mode, double theta,
+                                    const double* theta_dev, uint32_t* mask_bits, int8_t* codes,
+                                    int64_t ldq, float* scales, int8_t* res_codes, float* res_scales,
+                                    int32_t* masked_count, int8_t* sr_codes, uint64_t sr_seed,
+                                    int8_t* sr_codes2, uint64_t sr_seed2, int64_t row_offset,
+                                    fbq_stream_t stream) {
+  if (int st = check_x(x, dtype, rows, cols, ldx)) return st;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!gain || !ctx_codes || !ctx_scales || !rms_ws || !codes || !scales) return FBQ_ERR_ARG;
+  if (ld_ctx < cols) return FBQ_ERR_ARG;
+  const size_t esz = dtype == FBQ_F32 ? 4 : 2;
+  if (!rms_layout_ok(cols, ldx, x, esz) || !rms_layout_ok(cols, ld_ctx, ctx_codes, 2) ||
+      ldq % 16 || !aligned16(codes) || (res_codes && !aligned16(res_codes)) ||
+      (sr_codes && !aligned16(sr_codes)) || (sr_codes2 && !aligned16(sr_codes2)))
+    return FBQ_ERR_UNSUPPORTED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  fbq::QuantParams p;
+  if (int st = fill_quant_params(p, x, rows, cols, ldx, mask_mode, theta, mask_bits, codes, ldq,
+                                 scales, res_codes, res_scales, masked_count, nullptr, sr_codes,
+                                 sr_seed, sr_codes2, sr_seed2, row_offset, s, theta_dev))
+    return st;
+  return cuda_status(fbq::launch_rmsnorm_quantize(p, dtype == FBQ_BF16, gain, ctx_codes, ld_ctx, ctx_scales,
+                                                  rms_ws, s));
+}
+
 int fbq_cuda_rmsnorm_backward(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales,
                               const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
                               const float* gain, void* gx, int64_t ldgx, float* grad_gain,

@@ -1315,6 +1315,65 @@ fbq_rms_apply_fwd_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, in
   }
 }
 
+// RmsNorm fused with the next QuantLinearLayer's input quantizer:
+// per 128 x 128 block of x, the 10-bit 1 x 128 context of x (the RmsNorm's own
+// saved input, trainsim.cpp:171-176), then y = T(fl(fl(x / rms) * gain))
+// (trainsim.cpp:166-168; rounded to the activation dtype exactly like the
+// unfused RmsNorm output) repacked into the register-resident K1 -- codes,
+// scale, fallback flag / residual and the stochastic context planes of the
+// linear input (quant.cpp:36-84, 128-176) -- so y never reaches HBM.  rms[] comes
+// from fbq_rms_rowstat_fwd_kernel.  One block per CTA.
+template <typename T, int kSR, int kMinBlocks>
+__global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
+fbq_rms_quant_kernel(QuantParams p, const float* __restrict__ gain, const float* __restrict__ rms,
+                     int16_t* __restrict__ ctx, int64_t ld_ctx, float* __restrict__ ctx_scales) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  T* tile = reinterpret_cast<T*>(dsm);  // y of the block (zeros outside the tensor), as the K1 tile
+  __shared__ float red[kQuantThreads / 32];
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  const int64_t gcols = (p.cols + kBlock - 1) / kBlock;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t cc = bj * kBlock + lc;
+  const bool col_ok = cc < p.cols;  // cols % V == 0
+  float g[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) g[i] = col_ok ? gain[cc + i] : 0.0f;
+  const T* xp = reinterpret_cast<const T*>(p.x);
+#pragma unroll 2
+  for (int ps = 0; ps < NP; ++ps) {
+    const int rb = lr + ps * RPP;
+    const int64_t r = bi * kBlock + rb;
+    const bool ok = r < p.rows;  // row-uniform across the VPR threads of the group
+    float v[V];
+    if (ok && col_ok) {
+      load_vec<T, V>(xp + r * p.ldx + cc, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = 0.0f;
+    }
+    uint32_t code[V];
+    const float s = group_rtn<V, VPR>(v, code, 511.0f);
+    if (ok && col_ok) {
+      store_codes16<V>(ctx + r * ld_ctx + cc, code);
+      if (lc == 0) ctx_scales[r * gcols + bj] = s;
+    }
+    T out[V];
+    const float rr = ok ? rms[r] : 1.0f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float o = (ok && col_ok) ? __fmul_rn(__fdiv_rn(v[i], rr), g[i]) : 0.0f;
+      if constexpr (sizeof(T) == 2) out[i] = __float2bfloat16_rn(o);
+      else out[i] = o;
+    }
+    *reinterpret_cast<uint4*>(tile + rb * kBlock + lc) = *reinterpret_cast<const uint4*>(out);
+  }
+  __syncthreads();
+  quantize_block<V, kSR>(p, bi * gcols + bj, bi * kBlock, bj * kBlock, red,
+                         [&](int rb, int cb, float (&v)[V]) { load_vec<T, V>(tile + rb * kBlock + cb, v); });
+}
+
 // backward row statistics (trainsim.cpp:186-199), sequential per row in double:
 // x = dequantize(ctx); ss = sum x^2; dot = sum fl(fl(g*dy)*x); rms = sqrt(ss/cols
 // + eps); inv = 1 / rms; corr = dot / (((cols*rms)*rms)*rms).  Lane = row; the
@@ -1990,6 +2049,46 @@ cudaError_t launch_round_probe(const float* x, const float* a, const uint64_t* b
   if (blocks < 1) blocks = 1;
   fbq_round_probe_kernel<<<blocks, 256, 0, s>>>(x, a, bits, out_rtn, out_sr, n, path);
   return cudaGetLastError();
+}
+
+cudaError_t launch_rmsnorm_quantize(const QuantParams& p, bool bf16, const float* gain, int16_t* ctx,
+                                    int64_t ld_ctx, float* ctx_scales, float* rms, cudaStream_t s) {
+  const unsigned rb = (unsigned)((p.rows + 31) / 32);
+  const size_t sm16 = (size_t)kRsStages * 32 * (kRsCols * 2 + 16), sm32 = (size_t)kRsStages * 32 * (kRsCols * 4 + 16);
+  if (cudaError_t e = smem_once<fbq_rms_rowstat_fwd_kernel<__nv_bfloat16>>(sm16)) return e;
+  if (cudaError_t e = smem_once<fbq_rms_rowstat_fwd_kernel<float>>(sm32)) return e;
+  if (bf16) fbq_rms_rowstat_fwd_kernel<__nv_bfloat16><<<rb, 32, sm16, s>>>(
+      reinterpret_cast<const __nv_bfloat16*>(p.x), p.rows, p.cols, p.ldx, rms);
+  else fbq_rms_rowstat_fwd_kernel<float><<<rb, 32, sm32, s>>>(reinterpret_cast<const float*>(p.x), p.rows,
+                                                             p.cols, p.ldx, rms);
+  if (cudaError_t e = cudaGetLastError()) return e;
+  // (launched without programmatic dependence: the kernel reads rms[] at once)
+  QuantParams q = p;  // compact the stochastic planes into kSR = 0, 1, 2
+  if (!q.sr_codes && q.sr_codes2) {
+    q.sr_codes = q.sr_codes2;
+    q.sr_seed = q.sr_seed2;
+    q.sr_codes2 = nullptr;
+  }
+  const int nsr = q.sr_codes2 ? 2 : (q.sr_codes ? 1 : 0);
+  const dim3 grid((unsigned)((p.cols + kBlock - 1) / kBlock), (unsigned)((p.rows + kBlock - 1) / kBlock));
+  const dim3 b(kQuantThreads);
+  // y staged as the K1 tile: bf16 32 KiB at four CTAs per SM, fp32 64 KiB (as launch_k1_sr)
+  const size_t t16 = 2 * kTileElems, t32 = 4 * kTileElems;
+#define FBQ_RQ(TT, NSR, MB, SM)                                                                        \
+  do {                                                                                                  \
+    if (cudaError_t e = smem_once<fbq_rms_quant_kernel<TT, NSR, MB>>(SM)) return e;                     \
+    return launch_ex(fbq_rms_quant_kernel<TT, NSR, MB>, grid, b, SM, s, false, q, gain, rms, ctx,       \
+                     ld_ctx, ctx_scales);                                                               \
+  } while (0)
+  if (bf16) {
+    if (nsr == 2) FBQ_RQ(__nv_bfloat16, 2, 4, t16);
+    if (nsr == 1) FBQ_RQ(__nv_bfloat16, 1, 4, t16);
+    FBQ_RQ(__nv_bfloat16, 0, 4, t16);
+  }
+  if (nsr == 2) FBQ_RQ(float, 2, 1, t32);
+  if (nsr == 1) FBQ_RQ(float, 1, 1, t32);
+  FBQ_RQ(float, 0, 1, t32);
+#undef FBQ_RQ
 }
 
 }  // namespace fbq

@@ -82,6 +82,8 @@ extern int g_quant_diag;
 cudaError_t launch_rmsnorm_forward(const void* x, bool bf16, int64_t rows, int64_t cols, int64_t ldx,
                                    const float* gain, void* y, int64_t ldy, int16_t* ctx,
                                    int64_t ld_ctx, float* ctx_scales, float* rms, cudaStream_t s);
+cudaError_t launch_rmsnorm_quantize(const QuantParams& p, bool bf16, const float* gain, int16_t* ctx,
+                                    int64_t ld_ctx, float* ctx_scales, float* rms, cudaStream_t s);
 cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales,
                                     const void* gy, bool bf16, int64_t rows, int64_t cols,
                                     int64_t ldgy, const float* gain, void* gx, int64_t ldgx,

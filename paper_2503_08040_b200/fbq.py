@@ -492,6 +492,49 @@ class RmsNorm:
         self._ctx = (codes, scales, r, c)
         return y
 
+    def forward_quantized(self, x: torch.Tensor, *, mask: torch.Tensor | None = None,
+                          theta: float | None = None, sr_seed: int | None = None,
+                          sr_seed2: int | None = None, row_offset: int = 0):
+        """forward() fused with the next linear's input quantizer: the same
+        context as forward(), and for y = forward(x) exactly the outputs of
+        fallback_quantize(y, mask | theta, sr_seed) (+ a second stochastic plane
+        with sr_seed2), without materialising y.  Returns the FallbackTensor and
+        the stochastic QuantizedTensors (as fallback_quantize)."""
+        x = _check_input(x)
+        r, c = x.shape
+        if c != self.dim:
+            raise ValueError("width does not match the gain vector")
+        gr, gc = cdiv(r, BLOCK), cdiv(c, BLOCK)
+        dev = x.device
+        if mask is not None:
+            mode, bits_t, th = K.FBQ_MASK_GIVEN, mask_to_bits(mask.to(dev)), 1.0
+        elif theta is not None:
+            if not theta > 0.0:
+                raise ValueError("threshold must be > 0")
+            mode, th = K.FBQ_MASK_THRESHOLD, float(theta)
+            bits_t = torch.empty(cdiv(max(gr * gc, 1), 32), dtype=torch.int32, device=dev)
+        else:
+            raise ValueError("forward_quantized needs a mask or a threshold")
+        ldc = _ld16(c)
+        ctx = torch.empty((r, ldc), dtype=torch.int16, device=dev)
+        ctx_s = torch.empty((r, gc), dtype=torch.float32, device=dev)
+        rms = torch.empty(r, dtype=torch.float32, device=dev)
+        codes, scales = _alloc_codes(r, c, dev), _alloc_grid(r, c, dev)
+        res_codes, res_scales = _alloc_codes(r, c, dev), _alloc_grid(r, c, dev)
+        count = torch.empty(1, dtype=torch.int32, device=dev)
+        sr = _alloc_codes(r, c, dev) if sr_seed is not None else None
+        sr2 = _alloc_codes(r, c, dev) if sr_seed2 is not None else None
+        K.call("fbq_cuda_rmsnorm_quantize_input", x.data_ptr(), _dtype_code(x), r, c, x.stride(0),
+               self.gain.data_ptr(), ctx.data_ptr(), ldc, ctx_s.data_ptr(), rms.data_ptr(), mode, th, None,
+               bits_t.data_ptr(), codes.data_ptr(), codes.stride(0), scales.data_ptr(), res_codes.data_ptr(),
+               res_scales.data_ptr(), count.data_ptr(), sr.data_ptr() if sr is not None else None,
+               (sr_seed or 0) & (2 ** 64 - 1), sr2.data_ptr() if sr2 is not None else None,
+               (sr_seed2 or 0) & (2 ** 64 - 1), row_offset, _stream())
+        self._ctx = (ctx, ctx_s, r, c)
+        f = FallbackTensor(QuantizedTensor(r, c, codes, scales), bits_t, res_codes, res_scales, count)
+        extra = tuple(QuantizedTensor(r, c, t, scales) for t in (sr, sr2) if t is not None)
+        return (f,) + extra if extra else f
+
     def context(self):
         """(int16 codes rows x ld, fp32 scales rows x ceil(cols/128)) of the last input."""
         return self._ctx[:2]

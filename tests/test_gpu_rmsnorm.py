@@ -66,3 +66,51 @@ def test_rmsnorm_bf16_llama_width(rows, dim):
     assert np.array_equal(gx, bf16_round(ref.backward(gy)))
     _, gg_r = ref.state()
     assert np.array_equal(dev.grad_gain.cpu().numpy().view(np.int32), gg_r.view(np.int32))
+
+
+@pytest.mark.parametrize("rows,dim,dtype,nsr", [(256, 384, "f32", 2), (300, 1152, "bf16", 1),
+                                                (1000, 4096, "bf16", 2), (129, 512, "f32", 0)])
+@pytest.mark.parametrize("masking", ["threshold", "given"])
+def test_rmsnorm_fused_input_quantizer(rows, dim, dtype, nsr, masking):
+    """RmsNorm.forward_quantized == forward() then the linear-input quantizer on
+    y (codes, scales, mask, residuals, stochastic planes) -- bit for bit -- and
+    the same RmsNorm context; y is never materialised on the fused path."""
+    import torch
+    from paper_2503_08040_b200 import fbq
+    from tests.helpers import bf16_round
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = outlier_matrix(rows, dim, seed=90, body=1.0, channels=[5], tokens=[7], mag_c=40.0, mag_t=25.0)
+    if dtype == "bf16":
+        x = bf16_round(x)
+    xt = torch.from_numpy(x).cuda().to(tdt)
+    a, b = fbq.RmsNorm(dim), fbq.RmsNorm(dim)
+    g = torch.linspace(0.5, 1.5, dim, device="cuda")
+    a.gain.copy_(g)
+    b.gain.copy_(g)
+    y = a.forward(xt)
+    scores = fbq.score_blocks(y)
+    kw = {"theta": float(scores.flatten().median().item())} if masking == "threshold" else \
+        {"mask": fbq.mask_topk(scores, 0.2)}
+    s1, s2 = fbq.layer_seed(7, 3, 0, 1), fbq.layer_seed(7, 3, 1, 1)
+    want = fbq.fallback_quantize(y, sr_seed=s1 if nsr >= 1 else None, **kw)
+    got = b.forward_quantized(xt, sr_seed=s1 if nsr >= 1 else None, sr_seed2=s2 if nsr == 2 else None, **kw)
+    wf, gf = (want[0], got[0]) if nsr >= 1 else (want, got)
+    eq = lambda u, v: torch.equal(u.view(torch.int32) if u.dtype == torch.float32 else u,
+                                  v.view(torch.int32) if v.dtype == torch.float32 else v)
+    assert eq(gf.primary.codes[:, :dim], wf.primary.codes[:, :dim])
+    assert eq(gf.primary.scales, wf.primary.scales)
+    assert torch.equal(gf.mask, wf.mask)
+    assert int(gf.masked_count.item()) == int(wf.masked_count.item())
+    m = wf.mask.bool()
+    for bi, bj in zip(*torch.nonzero(m, as_tuple=True)):
+        r0, c0 = int(bi) * 128, int(bj) * 128
+        assert torch.equal(gf.res_codes[r0:r0 + 128, c0:min(c0 + 128, dim)],
+                           wf.res_codes[r0:r0 + 128, c0:min(c0 + 128, dim)])
+    assert eq(gf.res_scales[m], wf.res_scales[m])
+    if nsr >= 1:
+        assert torch.equal(got[1].codes[:, :dim], want[1].codes[:, :dim])
+    if nsr == 2:
+        q2 = fbq.quantize_stochastic(y, s2)
+        assert torch.equal(got[2].codes[:, :dim], q2.codes[:, :dim])
+    for u, v in zip(a.context(), b.context()):
+        assert torch.equal(u, v)
