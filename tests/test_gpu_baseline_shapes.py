@@ -248,3 +248,28 @@ def test_c3_bench_fast_path_vs_reference_same_inputs(F, R, c3_weights):
     assert e_gx <= FAST_SR_FRACTION * sr_gx, (e_gx, sr_gx)
     for e, sr in zip(e_g, sr_g):
         assert e <= FAST_SR_FRACTION * sr, (e, sr)
+
+
+def test_dx_gemm_chunked_raster_bit_identical():
+    """The C3 dX GEMM shape (dG 8192 x 28672 K-major x W_gu 28672 x 4096 MN-major)
+    takes the chunked-B raster (neither operand pinnable): bit-identical to the
+    kGroupM-group raster (diag 1 << 27) in the exact epilogue, and within the
+    FMA tolerance -- the raster only reorders whole tiles."""
+    import torch
+    from paper_2503_08040_b200 import fbq
+    lib = fbq.K.lib
+    lib.fbq_debug_set_gemm_diag.argtypes = [fbq.K.cint]
+    M, N, K = 8192, 4096, 28672
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qa = fbq.quantize_stochastic(torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16) * 1e-3, 5)
+    qb = fbq.quantize_rtn(torch.randn(K, N, device="cuda", generator=g) * 0.02)
+    outs = []
+    try:
+        for d in (0, 1 << 27):
+            lib.fbq_debug_set_gemm_diag(d)
+            outs.append(fbq.block_quant_gemm(qa, qb))
+    finally:
+        lib.fbq_debug_set_gemm_diag(0)
+    assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
+    fma = fbq.block_quant_gemm(qa, qb, exact=False)
+    assert float((fma - outs[0]).norm() / outs[0].norm()) <= 1e-5
