@@ -494,7 +494,42 @@ __device__ __forceinline__ void residual_vec(float (&v)[V], float a, float inv_a
 }
 
 // Out of line (flagged blocks only; keeps the main path's registers): the
-// residual's absmax of one raw vector, and its residual RTN codes (packed).
+// primary codes of one raw vector together with its residual's absmax (the code
+// pass of a flagged block), the residual's absmax alone, and the residual RTN
+// codes (packed).
+struct CodeMax {
+  uint2 code;
+  float rm;
+};
+template <typename T>
+__device__ __noinline__ CodeMax rtn_resmax_raw(uint4 raw, float a, float inv_a, int mode) {
+  constexpr int V = 16 / sizeof(T);
+  float v[V];
+  unpack<T>(raw, v);
+  uint32_t w[V];
+  CodeMax out;
+  out.rm = 0.0f;
+  if (mode == 2) {
+    if (rtn_fast_vec_x<V>(v, a, inv_a, w)) rtn_fix_vec<V>(v, a, w);
+    const float2 nmag = make_float2(-kMagic, -kMagic), a2 = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const float2 n = __fadd2_rn(make_float2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), nmag);
+      const float2 rec = __fmul2_rn(n, a2);  // fl(c * a)
+      const float2 r = __fadd2_rn(make_float2(v[i], v[i + 1]), make_float2(-rec.x, -rec.y));
+      out.rm = fmaxf(out.rm, fmaxf(fabsf(r.x), fabsf(r.y)));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = mode == 1 ? rtn_code_slow(v[i], a, 127.0f) : 0;
+      w[i] = (uint32_t)c;
+      out.rm = fmaxf(out.rm, fabsf(__fsub_rn(v[i], __fmul_rn((float)c, a))));
+    }
+  }
+  out.code = make_uint2(pack4_lo8(w), V == 8 ? pack4_lo8(w + 4) : 0u);
+  return out;
+}
 template <typename T>
 __device__ __noinline__ float residual_absmax_raw(uint4 raw, float a, float inv_a, int mode) {
   constexpr int V = 16 / sizeof(T);
@@ -582,10 +617,22 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   // of blocks -- recomputes them, which keeps this variant inside 80 registers)
   // (rounding mode and row range decided once per block; the destination
   // walks by one pointer increment per pass)
+  float rm = 0.0f;       // flagged blocks: the residual's absmax, fused into the code pass
+  bool have_rm = false;
   if (p.codes && col_ok) {
     int8_t* dst = p.codes + r0 * p.ldq + cc;
     const int64_t step = (int64_t)RPP * p.ldq;
-    if (mode == 2 && nrow == NP) {
+    if (flagged && !(p.diag & 1)) {  // diag: the separate residual-absmax pass
+#pragma unroll
+      for (int ps = 0; ps < NP; ++ps, dst += step) {
+        if (ps >= nrow) break;  // rows past the end hold zeros: residual 0
+        const CodeMax cm = rtn_resmax_raw<T>(raw[ps], a, inv_a, mode);
+        rm = fmaxf(rm, cm.rm);
+        if constexpr (V == 8) __stcs(reinterpret_cast<uint2*>(dst), cm.code);
+        else __stcs(reinterpret_cast<unsigned int*>(dst), cm.code.x);
+      }
+      have_rm = true;
+    } else if (mode == 2 && nrow == NP) {
 #pragma unroll
       for (int ps = 0; ps < NP; ++ps, dst += step) {
         constexpr int VV = 16 / sizeof(T);
@@ -642,9 +689,10 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
   // ---- fallback residual (quant.cpp:146-172): res = fl(x - fl(c * a)) ----
   // the primary codes are recomputed from the raw values (not held: 80-register
   // budget) as magic words, whose n = m - M is the code as a float (no I2F)
-  float rm = 0.0f;
+  if (!have_rm) {
 #pragma unroll
-  for (int ps = 0; ps < NP; ++ps) rm = fmaxf(rm, residual_absmax_raw<T>(raw[ps], a, inv_a, mode));
+    for (int ps = 0; ps < NP; ++ps) rm = fmaxf(rm, residual_absmax_raw<T>(raw[ps], a, inv_a, mode));
+  }
   const float ra = block_scale(block_max(rm, red));
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
   const int rmode = round_mode(ra);
@@ -1890,6 +1938,7 @@ static cudaError_t launch_k1_tma_reg(const QuantParams& p, cudaStream_t s) {
   // dynamic block schedule when fbq_cuda_init() set up the counter ring (diag 4096: static)
   QuantParams q = p;
   q.blk_ctr = (g_quant_diag & 4096) ? nullptr : counter_slot();
+  q.diag = (g_quant_diag & 16384) ? 1 : 0;
   return launch_ex(fbq_quantize_tma_reg_kernel<T, kQStages, kMinBlocks, kSR>, dim3((unsigned)grid), dim3(kQuantThreads),
                    smem, s, p.pdl, m, q, (int)nblk, gcols);
 }

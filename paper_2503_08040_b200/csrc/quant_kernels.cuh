@@ -29,6 +29,7 @@ struct QuantParams {
   uint64_t sr_seed2;
   int64_t row_offset;      // global row of this shard's row 0 (RNG index)
   int* blk_ctr;            // persistent K1: dynamic block counter slot (counter_slot()), or null
+  int diag;                // A/B diagnostics inside the kernels (0 = production)
 };
 
 // GluCombine forward fused with the next linear's input quantizer.
