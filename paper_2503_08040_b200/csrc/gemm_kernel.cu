@@ -58,8 +58,6 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + kEpiWarps * 32;  // WG0: TMA, MMA, scales, idle; WG1-2: epilogue
 constexpr int kPage = 32;                       // k-blocks per staged scale page
 constexpr int kOutChunk = 4096;                 // per-warp output staging buffer (TMA store box)
-constexpr uint32_t kMagicBits = 0x4B400000u;    // magic-bias decode (see consume)
-constexpr float kMagicF = 12582912.0f;          // 1.5 * 2^23
 
 struct ScalePage {
   float prim[2][kPage];  // fl(sA * sB) for the two 128-column halves
@@ -111,28 +109,20 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t blk) {
   return (bits[blk >> 5] >> (blk & 31)) & 1u;
 }
 
-// int32 -> fp32 is I2F (one FMA-pipe slot, exact for |P| < 2^24), then one
-// FFMA2 per element pair (FMA mode).  `one` is a runtime 1.0f: ptxas
-// contracts FMUL2 + FADD2 into FFMA2 even for the _rn intrinsics, but cannot
-// fold a multiply by an unknown value, so the exact chain fl(acc + fl(s*P)) is
-// expressed as FMUL2 then FFMA2(t, one, acc).
-//
-// kBiased: words accumulated onto the magic bias 0x4B400000 (as_float(v) =
-// 1.5 * 2^23 + P exactly for |P| <= 128 * 127^2 < 2^22) decode with one FADD2
-// (FMA pipe) instead of I2F (half-rate ALU pipe).  Evaluated in round 1: a
-// bias needs either a separate N=128 MMA for the biased half (N=128 runs the
-// tensor pipe at ~55-70%) or TMEM zero-fills of the other half, and neither
-// paid for itself (profiles/r01_gemm_isolation.txt); kept for reference.
-template <int kEpi, bool kBiased>
+// int32 -> fp32 is I2F (ALU pipe, exact for |P| < 2^24), then one FFMA2 per
+// element pair (FMA mode).  `one` is a runtime 1.0f: ptxas contracts FMUL2 +
+// FADD2 into FFMA2 even for the _rn intrinsics, but cannot fold a multiply by an
+// unknown value, so the exact chain fl(acc + fl(s*P)) is expressed as FMUL2 then
+// FFMA2(t, one, acc).  (Decoding biased words on the FMA pipe instead of I2F was
+// evaluated twice -- round 1 with TMEM bias fills, round 2 with offset-binary
+// operands -- and did not pay.)
+template <int kEpi>
 __device__ __forceinline__ void consume(const uint32_t (&v)[32], float2* acc, float s, float one) {
   const float2 s2 = make_float2(s, s);
   const float2 one2 = make_float2(one, one);
-  const float2 m2 = make_float2(-kMagicF, -kMagicF);
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const float2 pf =
-        kBiased ? __fadd2_rn(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), m2)
-                : make_float2(__int2float_rn((int)v[2 * i]), __int2float_rn((int)v[2 * i + 1]));
+    const float2 pf = make_float2(__int2float_rn((int)v[2 * i]), __int2float_rn((int)v[2 * i + 1]));
     if constexpr (kEpi == kEpiExact) {
       acc[i] = __ffma2_rn(__fmul2_rn(s2, pf), one2, acc[i]);  // fl(acc + fl(s * P))
     } else {
@@ -144,7 +134,7 @@ __device__ __forceinline__ void consume(const uint32_t (&v)[32], float2* acc, fl
 // Epilogue warps: warp (4 + q + 4h) owns TMEM lane quadrant q and the
 // 128-column half h of every 128 x 256 tile.
 // kProf: per-item timeline of warp q == 0 (clock64, diagnostics only).
-template <int kEpi, int h, bool kProf>
+template <int kEpi, int h, bool kProf, bool kDiag>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtensorMap* map_o,
                                               uint8_t* obuf, ScalePage* pages, uint64_t* tfull,
                                               uint64_t* tempty, uint64_t* sfull, uint64_t* sempty,
@@ -204,7 +194,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + slot);
           } else {
-            if (p.diag & 1) {  // diagnostic: release the slot without epilogue math
+            if (kDiag && (p.diag & 1)) {  // diagnostic: release the slot without epilogue math
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(tempty + slot);
@@ -220,17 +210,17 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
             tmem_ld32(tb + 32, vb);
             tmem_ld_wait();
             if constexpr (kProf) t2 = (uint32_t)clock();
-            consume<kEpi, false>(va, acc + 0, s, p.one);
+            consume<kEpi>(va, acc + 0, s, p.one);
             tmem_ld32(tb + 64, va);
-            consume<kEpi, false>(vb, acc + 16, s, p.one);
+            consume<kEpi>(vb, acc + 16, s, p.one);
             tmem_ld32(tb + 96, vb);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + slot);
             if constexpr (kProf) t3 = (uint32_t)clock();
-            consume<kEpi, false>(va, acc + 32, s, p.one);
-            consume<kEpi, false>(vb, acc + 48, s, p.one);
+            consume<kEpi>(va, acc + 32, s, p.one);
+            consume<kEpi>(vb, acc + 48, s, p.one);
             if constexpr (kProf) {
               // a register dependency on the last FFMA2 makes the clock read wait for it
               const uint32_t t4 = (uint32_t)clock() + (acc[63].y == 12345.0f ? 1u : 0u);
@@ -243,7 +233,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
       __syncwarp();
       if (lane == 0) mbar_arrive(sempty + (pc & 1));
     }
-    if (kEpi != kEpiDump && !(p.diag & 4) && p.tma_store) {
+    if (kEpi != kEpiDump && !(kDiag && (p.diag & 4)) && p.tma_store) {
       // Staged TMA stores: the warp's 32 rows x 128 columns go out in 4 KiB
       // boxes (64 bf16 or 32 fp32 columns x 32 rows), written into a 128B-
       // swizzled staging buffer (16-byte chunk j of row r at chunk j ^ (r & 7):
@@ -303,7 +293,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
               const int c0 = bn * 128 + c * cols_per_box;
               // the output streams past the L2-resident operand: evict_first
               // (diag 1 << 24: default policy)
-              if (p.diag & (1 << 24)) {
+              if (kDiag && (p.diag & (1 << 24))) {
                 if (p.tma_store == 2) tma_reduce_add_2d(map_o, obuf, c0, (int)row0);
                 else tma_store_2d(map_o, obuf, c0, (int)row0);
               } else {
@@ -316,7 +306,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
           }
         }
       }
-    } else if (kEpi != kEpiDump && !(p.diag & 4)) {
+    } else if (kEpi != kEpiDump && !(kDiag && (p.diag & 4))) {
       const int64_t grow = (int64_t)bm * kBM + row_in_tile;
       const int64_t gcol0 = (int64_t)bn * 128;
       if (bn < p.NB && grow < p.M) {
@@ -399,7 +389,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, const CUtenso
   }
 }
 
-template <int kEpi>
+// kDiag: the diagnostic instantiation (performance experiments through
+// fbq_debug_set_gemm_diag); the production instances compile those branches out
+// of the issue loops.
+template <int kEpi, bool kDiag = false>
 __global__ void __launch_bounds__(kThreads, 1)
 fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_r,
                 const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_o,
@@ -476,7 +469,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       // operand is read by the ~148 concurrent tiles within a short window and
       // then dead, so it is marked evict-first (diag 1 << 23: all evict-last)
       const uint64_t pol_keep = l2_policy_evict_last();
-      const bool split_pol = !(p.diag & (1 << 23));
+      const bool split_pol = !(kDiag && (p.diag & (1 << 23)));
       const uint64_t pol_a = (split_pol && p.n_fastest) ? l2_policy_evict_first() : pol_keep;
       // B streams (evict_first) whenever A is the resident operand: all
       // block-rows (A pinned) or row-groups larger than the default
@@ -502,7 +495,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             uint8_t* sr = sa + kTileA;
             uint8_t* sb = sa + 2 * kTileA;
             if (lane == 0) {
-              if (p.diag & 2) {  // diagnostic: no operand traffic
+              if (kDiag && (p.diag & 2)) {  // diagnostic: no operand traffic
                 mbar_arrive(full + stage);
               } else {
                 mbar_arrive_expect_tx(full + stage, kTileA + kTileB + (masked ? kTileA : 0));
@@ -548,7 +541,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const long long t_start = p.prof ? clock64() : 0;
       // diag 512 (bare MMA loop, no scale pages): the static tile schedule
       for (int tile = blockIdx.x;; tile += gridDim.x) {
-        if (p.diag & 512) {
+        if (kDiag && (p.diag & 512)) {
           if (tile >= p.num_tiles) break;
         } else {
           mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
@@ -556,18 +549,18 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         }
         for (int pg = 0; pg < p.KB; pg += kPage, ++pc) {
           const ScalePage& sp = pages[pc & 1];
-          if (!(p.diag & 512) && pg > 0) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
+          if (!(kDiag && (p.diag & 512)) && pg > 0) mbar_wait_sleep(sfull + (pc & 1), (pc >> 1) & 1);
           const int nk = min(kPage, p.KB - pg);
           for (int j = 0; j < nk; ++j) {
-            const int n_items = (!(p.diag & 512) && sp.flag[j]) ? 2 : 1;
-            if (!(p.diag & 16)) mbar_wait_sleep(full + stage, phase);
-            if (!(p.diag & 64)) tc_fence_after();
+            const int n_items = (!(kDiag && (p.diag & 512)) && sp.flag[j]) ? 2 : 1;
+            if (!(kDiag && (p.diag & 16))) mbar_wait_sleep(full + stage, phase);
+            if (!(kDiag && (p.diag & 64))) tc_fence_after();
             const uint32_t sa = smem0 + stage * kStageBytes;
             const uint64_t bd0 = b_tmpl | ((sa + 2 * kTileA) >> 4);
             for (int r = 0; r < n_items; ++r) {
               const uint32_t slot = item & 1;
-              if (!(p.diag & 8)) mbar_wait_sleep(tempty + slot, ((item >> 1) & 1) ^ 1);
-              if (!(p.diag & 64)) tc_fence_after();
+              if (!(kDiag && (p.diag & 8))) mbar_wait_sleep(tempty + slot, ((item >> 1) & 1) ^ 1);
+              if (!(kDiag && (p.diag & 64))) tc_fence_after();
               const uint64_t ad0 = a_tmpl | ((sa + (r ? kTileA : 0)) >> 4);
               const uint32_t d = tmem_base + slot * 256;
               if (lane == 0) {
@@ -579,7 +572,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
               __syncwarp();
               ++item;
             }
-            if (!(p.diag & 128) && lane == 0) mma_commit(empty + stage);
+            if (!(kDiag && (p.diag & 128)) && lane == 0) mma_commit(empty + stage);
             __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
@@ -596,7 +589,7 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // schedule tile += gridDim.x.  Each tile's pages carry its index to the
     // other roles; a page with tile = -1 tells them to exit.
     uint32_t pc = 0;
-    int tile = (p.diag & 512) ? p.num_tiles : blockIdx.x;
+    int tile = (kDiag && (p.diag & 512)) ? p.num_tiles : blockIdx.x;
     for (;;) {
       if (tile >= p.num_tiles) {
         ScalePage& sp = pages[pc & 1];
@@ -658,11 +651,11 @@ fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // ===================== epilogue =====================
     setmaxnreg_inc<224>();
     if (p.prof) {
-      if (warp >= 8) epilogue_role<kEpi, 1, true>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
-      else epilogue_role<kEpi, 0, true>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      if (warp >= 8) epilogue_role<kEpi, 1, true, kDiag>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      else epilogue_role<kEpi, 0, true, kDiag>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
     } else {
-      if (warp >= 8) epilogue_role<kEpi, 1, false>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
-      else epilogue_role<kEpi, 0, false>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      if (warp >= 8) epilogue_role<kEpi, 1, false, kDiag>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
+      else epilogue_role<kEpi, 0, false, kDiag>(p, &map_o, ostage + (warp - 4) * kOutChunk, pages, tfull, tempty, sfull, sempty, tmem_holder, warp, lane, NT);
     }
   }
   tc_fence_before();
@@ -739,6 +732,10 @@ static cudaError_t gemm_attributes(int dev) {
                           cudaFuncSetAttribute(fbq_gemm_kernel<kEpiFma>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
                           cudaFuncSetAttribute(fbq_gemm_kernel<kEpiDump>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+                          cudaFuncSetAttribute(fbq_gemm_kernel<kEpiExact, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+                          cudaFuncSetAttribute(fbq_gemm_kernel<kEpiFma, true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)})
       if (e != cudaSuccess && g_attr_err[dev] == cudaSuccess) g_attr_err[dev] = e;
   });
@@ -783,7 +780,12 @@ template <int kEpi>
 static cudaError_t launch_typed(const CUtensorMap& ma, const CUtensorMap& mr,
                                 const CUtensorMap& mb, const CUtensorMap& mo, const GemmParams& p,
                                 int grid, cudaStream_t s) {
-  fbq_gemm_kernel<kEpi><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, mo, p);
+  // kernel-side diagnostic bits run the diagnostic instantiation (kDiag)
+  constexpr int kKernelDiag = 1 | 2 | 4 | 8 | 16 | 64 | 128 | 512 | (1 << 23) | (1 << 24);
+  if (kEpi != kEpiDump && (p.diag & kKernelDiag))
+    fbq_gemm_kernel<kEpi, kEpi != kEpiDump><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, mo, p);
+  else
+    fbq_gemm_kernel<kEpi><<<grid, kThreads, kSmemBytes, s>>>(ma, mr, mb, mo, p);
   return cudaGetLastError();
 }
 
