@@ -68,7 +68,7 @@ struct ScalePage {
 };
 
 constexpr size_t kSmemBytes =
-    1024 + (size_t)kStages * kStageBytes + (size_t)kEpiWarps * kOutChunk + 2 * sizeof(ScalePage) + 256;
+    (size_t)kStages * kStageBytes + (size_t)kEpiWarps * kOutChunk + 2 * sizeof(ScalePage) + 256;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 // Tile rasterisation, chosen per launch so that one operand stays resident in
@@ -397,11 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 fbq_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_r,
                 const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_o,
                 const GemmParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1 KiB alignment (128B-swizzle atoms) by pointer arithmetic on the shared
-  // array itself, so every derived pointer (pages, barriers, the TMEM holder)
-  // stays in the shared address space (LDS/STS, no generic LD/ST)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // The 128B-swizzle atoms need 1 KiB alignment: dynamic shared memory starts
+  // 1 KiB-aligned on sm_100 (after the 1 KiB reserved per CTA), which the kernel
+  // checks (trap) instead of re-deriving an aligned base -- the runtime
+  // arithmetic was rematerialised in every epilogue item under register pressure.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023u) __trap();
+  uint8_t* smem = smem_raw;
   uint8_t* ostage = smem + kStages * kStageBytes;  // [kEpiWarps][kOutChunk], 1 KiB aligned
   ScalePage* pages = reinterpret_cast<ScalePage*>(ostage + kEpiWarps * kOutChunk);
   uint64_t* bars = reinterpret_cast<uint64_t*>(pages + 2);
