@@ -81,6 +81,22 @@ __device__ __forceinline__ float block_max(float v, float* red) {
   return m;
 }
 
+// The same with ONE barrier: `red` must not be re-written before every thread
+// has read it -- callers give each call of a block its own 8-float slot and
+// have a CTA barrier between blocks (the register-resident K1: the second slot
+// serves the fallback residual, the TMA ring's slot-release barrier separates
+// blocks).
+__device__ __forceinline__ float block_max_1b(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float m = red[0];
+#pragma unroll
+  for (int w = 1; w < kQuantThreads / 32; ++w) m = fmaxf(m, red[w]);
+  return m;
+}
+
 // max over the VPR threads that share one block row (a 1 x 128 group)
 template <int VPR>
 __device__ __forceinline__ float row_max(float v) {
@@ -595,7 +611,7 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
       for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
     }
   }
-  const float amax = block_max(m, red);
+  const float amax = block_max_1b(m, red);  // slot 0 (red holds 2 x 8 floats)
   const float a = block_scale(amax);
   const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
   const int mode = round_mode(a);
@@ -693,7 +709,7 @@ __device__ __forceinline__ void quantize_block_reg(const QuantParams& p, int64_t
 #pragma unroll
     for (int ps = 0; ps < NP; ++ps) rm = fmaxf(rm, residual_absmax_raw<T>(raw[ps], a, inv_a, mode));
   }
-  const float ra = block_scale(block_max(rm, red));
+  const float ra = block_scale(block_max_1b(rm, red + kQuantThreads / 32));  // slot 1
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
   const int rmode = round_mode(ra);
   if (threadIdx.x == 0 && p.res_scales) p.res_scales[blk] = ra;
@@ -731,7 +747,7 @@ __device__ __forceinline__ void load_block_reg(const QuantParams& p, int64_t bi,
 template <typename T, int kSR>
 __global__ void __launch_bounds__(kQuantThreads, 2)
 fbq_quantize_reg_kernel(QuantParams p) {
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[2 * (kQuantThreads / 32)];  // quantize_block_reg: two reduction slots
   uint4 raw[Tiling<T>::NP];
   load_block_reg<T>(p, blockIdx.y, blockIdx.x, raw);
   quantize_block_reg<T, kSR>(p, blockIdx.y, blockIdx.x, (int64_t)blockIdx.y * gridDim.x + blockIdx.x, raw, red);
@@ -757,7 +773,7 @@ fbq_quantize_tma_reg_kernel(const __grid_constant__ CUtensorMap map_x, QuantPara
   T* tiles = reinterpret_cast<T*>(dsm);
   __shared__ __align__(8) uint64_t full[kQStages];
   __shared__ int slot_blk[kQStages];
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[2 * (kQuantThreads / 32)];  // quantize_block_reg: two reduction slots
   using Tl = Tiling<T>;
   constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   constexpr uint32_t kTileBytes = sizeof(T) * kTileElems;
