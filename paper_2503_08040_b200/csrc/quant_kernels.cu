@@ -68,24 +68,10 @@ struct Tiling {
 };
 constexpr int kTileElems = kBlock * kBlock;
 
-__device__ __forceinline__ float block_max(float v, float* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int warp = threadIdx.x >> 5;
-  __syncthreads();  // protect `red` reuse across calls
-  if ((threadIdx.x & 31) == 0) red[warp] = v;
-  __syncthreads();
-  float m = red[0];
-#pragma unroll
-  for (int w = 1; w < kQuantThreads / 32; ++w) m = fmaxf(m, red[w]);
-  return m;
-}
-
-// The same with ONE barrier: `red` must not be re-written before every thread
-// has read it -- callers give each call of a block its own 8-float slot and
-// have a CTA barrier between blocks (the register-resident K1: the second slot
-// serves the fallback residual, the TMA ring's slot-release barrier separates
-// blocks).
+// Block-wide max with ONE barrier: `red` must not be re-written before every
+// thread has read it -- callers give each call of a block its own 8-float slot
+// and have a CTA barrier between blocks (the second slot serves the fallback
+// residual; the TMA rings' slot-release barriers separate persistent blocks).
 __device__ __forceinline__ float block_max_1b(float v, float* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -310,7 +296,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
       for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
     }
   }
-  const float amax = block_max(m, red);
+  const float amax = block_max_1b(m, red);  // slot 0 (callers give red 2 x 8 floats)
   const float a = block_scale(amax);
   const float inv_a = a > 0.0f ? __frcp_rn(a) : 0.0f;
   const int mode = round_mode(a);
@@ -373,7 +359,7 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
 #pragma unroll
     for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
   }
-  const float ra = block_scale(block_max(m, red));
+  const float ra = block_scale(block_max_1b(m, red + kQuantThreads / 32));  // slot 1
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
   const int rmode = round_mode(ra);
   if (threadIdx.x == 0 && p.res_scales) p.res_scales[blk] = ra;
@@ -396,7 +382,7 @@ __global__ void __launch_bounds__(kQuantThreads, kMinBlocks)
 fbq_quantize_block_kernel(QuantParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   T* tile = reinterpret_cast<T*>(dsm);
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[2 * (kQuantThreads / 32)];
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
   const int64_t r0 = bi * kBlock, c0 = bj * kBlock;
   stage_tile<T, kVec>(tile, reinterpret_cast<const T*>(p.x), p.ldx, p.rows, p.cols, r0, c0);
@@ -861,7 +847,7 @@ fbq_quantize_tma_kernel(const __grid_constant__ CUtensorMap map_x, QuantParams p
   extern __shared__ __align__(128) uint8_t dsm[];
   T* tiles = reinterpret_cast<T*>(dsm);
   __shared__ __align__(8) uint64_t full[kQStages];
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[2 * (kQuantThreads / 32)];
   constexpr int V = Tiling<T>::V;
   constexpr uint32_t kTileBytes = sizeof(T) * kTileElems;
   if (threadIdx.x == 0) {
@@ -967,7 +953,7 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
   constexpr int kRowF = kRow * (int)sizeof(T) / 4;      // fp32 per smem row
   T* tab = reinterpret_cast<T*>(dsm);
   float* th = reinterpret_cast<float*>(dsm);
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[2 * (kQuantThreads / 32)];
   using Tl = Tiling<T>;
   constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   const int64_t bj = blockIdx.x, bi = blockIdx.y;
@@ -1220,8 +1206,8 @@ fbq_glu_backward_kernel(GluBwdParams g) {
       }
     }
   }
-  const float a_s = block_scale(block_max(ma, red));
-  const float b_s = block_scale(block_max(mb, red2));
+  const float a_s = block_scale(block_max_1b(ma, red));  // one block per CTA: no reuse
+  const float b_s = block_scale(block_max_1b(mb, red2));
   const float inv_a = a_s > 0.0f ? __frcp_rn(a_s) : 0.0f, inv_b = b_s > 0.0f ? __frcp_rn(b_s) : 0.0f;
   const int mode_a = round_mode(a_s), mode_b = round_mode(b_s);
   if (threadIdx.x == 0) {
@@ -1393,7 +1379,7 @@ fbq_rms_quant_kernel(QuantParams p, const float* __restrict__ gain, const float*
                      int16_t* __restrict__ ctx, int64_t ld_ctx, float* __restrict__ ctx_scales) {
   extern __shared__ __align__(16) uint8_t dsm[];
   T* tile = reinterpret_cast<T*>(dsm);  // y of the block (zeros outside the tensor), as the K1 tile
-  __shared__ float red[kQuantThreads / 32];
+  __shared__ float red[2 * (kQuantThreads / 32)];
   using Tl = Tiling<T>;
   constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
   const int64_t bi = blockIdx.y, bj = blockIdx.x;
