@@ -573,15 +573,20 @@ def gemm_sweep(device):
 
 
 # ----------------------------------------------------------------- C3 comparators
-def mlp_thresholds(x, wg, wu, device, q=0.85):
+def mlp_thresholds(x, wg, wu, device, q=0.85, pooled=True):
     """Start the delay-threshold controllers inside their target band (the
     reference starts at 1.0 and walks there by x1.3 per step): the q-quantile of
     the block AbsMax scores of X (gate/up input) and of a bf16 estimate of h
-    (down input), pooled over ranks so every rank starts from the same values."""
+    (down input), pooled over ranks so every rank starts from the same values.
+    pooled=False: this rank's scores only -- for the rank-0-only measurements,
+    where a collective would wait for ranks that never call it."""
     import torch
     from paper_2503_08040_b200 import fbq
     from paper_2503_08040_b200.dist import global_quantile
-    th_gu = global_quantile(fbq.score_blocks(x).flatten(), q)
+
+    def quantile(v):
+        return global_quantile(v, q) if pooled else float(torch.quantile(v.reshape(-1).float(), q))
+    th_gu = quantile(fbq.score_blocks(x).flatten())
     with torch.no_grad():
         xs = x[:1024].float()
         wg_t = wg if isinstance(wg, torch.Tensor) else torch.from_numpy(wg)
@@ -589,7 +594,7 @@ def mlp_thresholds(x, wg, wu, device, q=0.85):
         a = xs @ wg_t.to(device).float().t()
         b = xs @ wu_t.to(device).float().t()
         h = torch.nn.functional.silu(a) * b
-        th_d = global_quantile(fbq.score_blocks(h).flatten(), q)
+        th_d = quantile(fbq.score_blocks(h).flatten())
         del xs, a, b, h
     return th_gu, th_d
 
@@ -722,7 +727,7 @@ def exact_mode_rate(device, T=TOKENS, steps=5, warmup=2):
     wg, wu, wd = make_weights()
     m = linear.GluMlp(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.float32, exact=True)
     x = make_activations(T, D_MODEL, 1000, device, torch.float32)
-    m.set_thresholds(*mlp_thresholds(x, wg, wu, device))
+    m.set_thresholds(*mlp_thresholds(x, wg, wu, device, pooled=False))  # rank 0 only: no collective
     gy = make_grads(T, D_MODEL, 2000, device, torch.float32)
     y, gx = torch.empty_like(x), torch.empty_like(x)
     i = [0]
@@ -763,7 +768,7 @@ def context_memory(device, T=TOKENS, steps=10, warmup=3):
         out["bf16_MB"] = round(bf / 1e6, 1)
         out[f"{key}_frac_of_bf16"] = round(ours / bf, 4)
         if packed != CTX_PACKED:  # the headline's storage is timed by the main arm
-            m.set_thresholds(*mlp_thresholds(x, wg, wu, device))
+            m.set_thresholds(*mlp_thresholds(x, wg, wu, device, pooled=False))  # rank 0 only
             i = [0]
 
             def step():
