@@ -247,6 +247,28 @@ __device__ __forceinline__ int round_mode(float a) {
   return a == 0.0f ? 0 : (a < kTinyScale ? 1 : 2);
 }
 
+// x -> fl(x - fl(c a)) in place, c = RTN code of x (the fallback residual,
+// quant.cpp:150-156).  Fast mode: c from the magic words (n = m - M exactly).
+template <int V>
+__device__ __forceinline__ void residual_vec(float (&v)[V], float a, float inv_a, int mode) {
+  if (mode == 2) {
+    uint32_t w[V];
+    if (rtn_fast_vec_x<V>(v, a, inv_a, w)) rtn_fix_vec<V>(v, a, w);
+    const float2 nmag = make_float2(-kMagic, -kMagic), a2 = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const float2 n = __fadd2_rn(make_float2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), nmag);
+      const float2 rec = __fmul2_rn(n, a2);                       // fl(c * a)
+      const float2 r = __fadd2_rn(make_float2(v[i], v[i + 1]), make_float2(-rec.x, -rec.y));
+      v[i] = r.x;
+      v[i + 1] = r.y;
+    }
+  } else if (mode == 1) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)rtn_code_slow(v[i], a, 127.0f), a));
+  }  // mode 0: a == 0, codes 0, residual = x
+}
+
 // Quantize one 128 x 128 block whose values are produced on demand by
 // `val(row_in_block, col_in_block, float (&v)[V])` (V consecutive columns).
 // Fused outputs per QuantParams: scale, fallback flag, RTN codes, kSR (0-2)
@@ -346,6 +368,11 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   //      from the staged values (no fp32 residual tile) ----
   auto res = [&](int rb, float (&v)[V]) {
     val(rb, lc, v);
+    if (mode == 2) {
+      // code as a float straight from the magic words (n = m - M exactly): no I2F
+      residual_vec<V>(v, a, inv_a, mode);
+      return;
+    }
     uint32_t c[V];
     rtn_vec<V>(v, a, inv_a, mode, c);
 #pragma unroll
@@ -471,28 +498,6 @@ __device__ __noinline__ uint2 rtn_raw_call(uint4 raw, float a, float inv_a, int 
 __device__ __forceinline__ float code_of(const uint2& c, int i) {
   const uint32_t w = i < 4 ? c.x : c.y;
   return (float)(int8_t)(uint8_t)(w >> (8 * (i & 3)));
-}
-
-// x -> fl(x - fl(c a)) in place, c = RTN code of x (the fallback residual,
-// quant.cpp:150-156).  Fast mode: c from the magic words (n = m - M exactly).
-template <int V>
-__device__ __forceinline__ void residual_vec(float (&v)[V], float a, float inv_a, int mode) {
-  if (mode == 2) {
-    uint32_t w[V];
-    if (rtn_fast_vec_x<V>(v, a, inv_a, w)) rtn_fix_vec<V>(v, a, w);
-    const float2 nmag = make_float2(-kMagic, -kMagic), a2 = make_float2(a, a);
-#pragma unroll
-    for (int i = 0; i < V; i += 2) {
-      const float2 n = __fadd2_rn(make_float2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), nmag);
-      const float2 rec = __fmul2_rn(n, a2);                       // fl(c * a)
-      const float2 r = __fadd2_rn(make_float2(v[i], v[i + 1]), make_float2(-rec.x, -rec.y));
-      v[i] = r.x;
-      v[i + 1] = r.y;
-    }
-  } else if (mode == 1) {
-#pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)rtn_code_slow(v[i], a, 127.0f), a));
-  }  // mode 0: a == 0, codes 0, residual = x
 }
 
 // Out of line (flagged blocks only; keeps the main path's registers): the
