@@ -338,6 +338,9 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
   }
 
   // ---- RTN codes + stochastic context planes (kernels.cpp:24-40, quant.cpp:66-80) ----
+  // (a flagged block's residual absmax rides along with its code pass)
+  float rm = 0.0f;
+  const bool fuse_rm = (V % 2 == 0) && flagged && mode == 2 && p.codes != nullptr;  // words = magic words
   if (lane_ok && (p.codes || kSR > 0)) {
 #pragma unroll 1
     for (int ps = 0; ps < NP; ++ps) {
@@ -349,6 +352,13 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
       uint32_t code[V];
       if (p.codes) {
         rtn_vec<V>(v, a, inv_a, mode, code);
+        if (fuse_rm) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) {  // fl(x - fl(c a)), c = m - M exactly
+            const float n = __fsub_rn(__uint_as_float(code[i]), kMagic);
+            rm = fmaxf(rm, fabsf(__fsub_rn(v[i], __fmul_rn(n, a))));
+          }
+        }
         store_codes<V>(p.codes + r * p.ldq + cc, code, nvalid, p.vec_store);
       }
       if constexpr (kSR >= 1) {
@@ -378,15 +388,16 @@ __device__ __forceinline__ void quantize_block(const QuantParams& p, int64_t blk
 #pragma unroll
     for (int i = 0; i < V; ++i) v[i] = __fsub_rn(v[i], __fmul_rn((float)(int8_t)(uint8_t)c[i], a));
   };
-  m = 0.0f;
+  if (!fuse_rm) {
 #pragma unroll 1
-  for (int ps = 0; ps < NP; ++ps) {
-    float v[V];
-    res(lr + ps * RPP, v);
+    for (int ps = 0; ps < NP; ++ps) {
+      float v[V];
+      res(lr + ps * RPP, v);
 #pragma unroll
-    for (int i = 0; i < V; ++i) m = fmaxf(m, fabsf(v[i]));
+      for (int i = 0; i < V; ++i) rm = fmaxf(rm, fabsf(v[i]));
+    }
   }
-  const float ra = block_scale(block_max_1b(m, red + kQuantThreads / 32));  // slot 1
+  const float ra = block_scale(block_max_1b(rm, red + kQuantThreads / 32));  // slot 1
   const float inv_ra = ra > 0.0f ? __frcp_rn(ra) : 0.0f;
   const int rmode = round_mode(ra);
   if (threadIdx.x == 0 && p.res_scales) p.res_scales[blk] = ra;
