@@ -1,8 +1,9 @@
-"""Run bench.py's C2 quantizer sweep alone (GB/s and HBM fraction per case)."""
+"""bench.quant_sweep alone (C2, events + CUDA-graph timings + copy comparator), compact print."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
-peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
-r = bench.quant_sweep("cuda", peaks.get("hbm_gbs", 6522.1))
+peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
+r = bench.quant_sweep("cuda", peak)
 for k, v in r["cases"].items():
-    print(f"{k:32s} {v}")
+    print(f"{k:42s} us {v['us']:7.1f} frac {v['frac_hbm']:.3f}  graph {v['graph_us']:7.1f} {v['frac_hbm_graph']:.3f}"
+          + (f"  flagged {v['flagged']:.3f}" if "flagged" in v else ""), flush=True)
