@@ -802,6 +802,46 @@ def exact_mode_rate(device, T=TOKENS, steps=5, warmup=2):
             "ms_per_step": ms, "fallback_rates": rates}
 
 
+def train_step_rate(device, T=TOKENS, steps=10, warmup=3, lr=1e-6):
+    """The headline configuration as a full training step: zero_grad + fwd +
+    bwd + controller + apply_sgd on gate, up and down (QuantLinearLayer::
+    apply_sgd, trainsim.cpp:137-143), the update fused with the next forward's
+    weight quantization (fbq_mlp_apply_sgd).  The headline metric is the
+    paper's fwd+bwd rate, which the reference arm times the same way.  A small
+    learning rate keeps the weights (and so the fallback rates) where the
+    headline has them, so the two rates are comparable; the update does the
+    same work at any lr."""
+    import torch
+    from paper_2503_08040_b200 import linear
+    wg, wu, wd = make_weights()
+    m = linear.GluMlp(wg, wu, wd, T, ctx_packed=CTX_PACKED)
+    x = make_activations(T, D_MODEL, 1000, device, torch.bfloat16)
+    m.set_thresholds(*mlp_thresholds(x, wg, wu, device, pooled=False))  # rank 0 only: no collective
+    gy = make_grads(T, D_MODEL, 2000, device, torch.bfloat16)
+    y, gx = torch.empty_like(x), torch.empty_like(x)
+    i = [0]
+
+    def step(sgd):
+        def run():
+            m.zero_grad()
+            m.forward(x, i[0], out=y)
+            m.backward(gy, i[0], out=gx)
+            m.controller_step()
+            if sgd:
+                m.apply_sgd(lr)
+            i[0] += 1
+        return run
+
+    ms_fb = _event_time(step(False), steps, warmup)
+    ms_sgd = _event_time(step(True), steps, warmup)
+    del m, x, gy, y, gx
+    torch.cuda.empty_cache()
+    return {"workload": "C3 MLP training step: zero_grad + fwd + bwd + controller + SGD (lr 1e-6) on "
+                        "W_gate, W_up, W_down, fused with the next forward's weight RTN",
+            "tokens_per_s": T / (ms_sgd * 1e-3), "ms_per_step": ms_sgd,
+            "fwd_bwd_same_run_ms": ms_fb, "sgd_cost_ms": ms_sgd - ms_fb}
+
+
 def context_memory(device, T=TOKENS, steps=10, warmup=3):
     """Activation contexts saved for the backward vs BF16 (PAPER.md:55, 527, 535:
     62 %), for both storages of the 10-bit GluCombine contexts, and the step
@@ -1020,7 +1060,7 @@ def run_ours(args, rank, world, local):
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
-        comparator = exact = ctxmem = None
+        comparator = exact = ctxmem = train = None
         if not args.no_sweep:
             try:
                 comparator = bf16_mlp_comparator(device, T)
@@ -1035,6 +1075,10 @@ def run_ours(args, rank, world, local):
                 ctxmem = context_memory(device, T)
             except Exception as ex:  # pragma: no cover
                 ctxmem = {"error": str(ex)[:200]}
+            try:
+                train = train_step_rate(device, T)
+            except Exception as ex:  # pragma: no cover
+                train = {"error": str(ex)[:200]}
         sweep = qsweep = c4 = rms = None
         if not args.no_sweep and world == 1:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
@@ -1104,6 +1148,7 @@ def run_ours(args, rank, world, local):
             "clocks": clk.summary(),
             "bf16_mlp_comparator": comparator,
             "exact_mode": exact,
+            "train_step": train,
             "context_memory": ctxmem,
             "gemm_sweep": sweep,
             "quant_sweep": qsweep,

@@ -217,6 +217,15 @@ int fbq_cuda_controller_update_rate(double* theta_dev, const double* observed_ra
 /* QuantLinearLayer::apply_sgd (trainsim.cpp:137-143): w[i] -= float(lr * double(grad[i])) */
 int fbq_cuda_sgd_update(float* w, const float* grad, int64_t n, double lr, fbq_stream_t stream);
 
+/* apply_sgd fused with the next forward's weight quantization: w (rows x cols,
+ * contiguous fp32) -= float(lr * double(grad)), then quantize_rtn of the updated
+ * w (128 x 128 blocks, quant.cpp:36-53; trainsim.cpp:96) into codes (ldq) and
+ * scales -- one pass over w and grad.  Bit-identical to fbq_cuda_sgd_update
+ * followed by fbq_cuda_quantize_rtn (which it runs instead when cols % 4, ldq %
+ * 16 or a pointer's 16-byte alignment rules out the fused kernel). */
+int fbq_cuda_sgd_quantize_rtn(float* w, const float* grad, int64_t rows, int64_t cols, double lr,
+                              int8_t* codes, int64_t ldq, float* scales, fbq_stream_t stream);
+
 /* controller_update (policy.cpp:97-109) on device: rate = *masked_count /
  * n_blocks; *theta_dev /= alpha if rate < r_min, *= alpha if rate > r_max;
  * *last_rate_dev = rate (may be NULL). */

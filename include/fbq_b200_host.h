@@ -121,6 +121,16 @@ int fbq_mlp_wait_grad(void* mlp, int which, fbq_stream_t stream);
 int fbq_mlp_get_grads(void* mlp, float* g_gate, float* g_up, float* g_down);
 /* rates[2] = last fallback rate of gate/up and down; thresholds[2] likewise */
 int fbq_mlp_get_controller(void* mlp, double* rates, double* thresholds);
+/* QuantLinearLayer::apply_sgd (trainsim.cpp:137-143) on gate, up and down,
+ * stream-ordered after the last backward (data parallel: after the dW
+ * all-reduce).  Fused with the weight quantization the next forward would run
+ * (fbq_cuda_sgd_quantize_rtn): that forward then uses the codes written here
+ * instead of re-quantizing W -- the same codes, one pass over W instead of two.
+ * A pending zero_grad makes it a no-op (the reference: w -= lr * 0). */
+int fbq_mlp_apply_sgd(void* mlp, double lr, fbq_stream_t stream);
+/* synchronous host copies of the fp32 master weights (gate, up: d_ff x
+ * d_model; down: d_model x d_ff) */
+int fbq_mlp_get_weights(void* mlp, float* w_gate, float* w_up, float* w_down);
 
 /* ---- one fallback-quantized linear layer: QuantLinearLayer (trainsim.hpp:38-73,
  * trainsim.cpp:61-135) with 128 x 128 blocks, 8-bit operands, the stochastic X

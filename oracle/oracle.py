@@ -390,6 +390,8 @@ class RefMlp:
         lib.ref_mlp_step.argtypes = [C.c_void_p, F32, F32, i64, i64, cint, F32, F32]
         lib.ref_mlp_grads.argtypes = [C.c_void_p, F32, F32, F32]
         lib.ref_mlp_controller.argtypes = [C.c_void_p, F64, F64]
+        lib.ref_mlp_sgd.argtypes = [C.c_void_p, dbl]
+        lib.ref_mlp_weights.argtypes = [C.c_void_p, F32, F32, F32]
         self.wg = np.ascontiguousarray(w_gate, np.float32)
         self.wu = np.ascontiguousarray(w_up, np.float32)
         self.wd = np.ascontiguousarray(w_down, np.float32)
@@ -415,6 +417,18 @@ class RefMlp:
         gd = np.zeros((self.d_model, self.d_ff), np.float32)
         self.lib.ref_mlp_grads(self.h, gg, gu, gd)
         return gg, gu, gd
+
+    def apply_sgd(self, lr):
+        if self.lib.ref_mlp_sgd(self.h, lr):
+            raise RuntimeError(self._err().decode())
+
+    def weights(self):
+        wg = np.zeros((self.d_ff, self.d_model), np.float32)
+        wu = np.zeros_like(wg)
+        wd = np.zeros((self.d_model, self.d_ff), np.float32)
+        if self.lib.ref_mlp_weights(self.h, wg, wu, wd):
+            raise RuntimeError(self._err().decode())
+        return wg, wu, wd
 
     def controller(self):
         rates = np.zeros(3)
@@ -446,6 +460,8 @@ class RefLinear:
         lib.ref_linear_grad.argtypes = [C.c_void_p, F32]
         lib.ref_linear_controller.argtypes = [C.c_void_p, F64, F64]
         lib.ref_linear_zero_grad.argtypes = [C.c_void_p]
+        lib.ref_linear_sgd.argtypes = [C.c_void_p, dbl]
+        lib.ref_linear_weight.argtypes = [C.c_void_p, F32]
         self.w = np.ascontiguousarray(w, np.float32)
         self.out_features, self.in_features = self.w.shape
         mode = {"threshold": 0, "fixed_rate": 1, "off": 2}[fallback_mode]
@@ -484,6 +500,14 @@ class RefLinear:
 
     def zero_grad(self):
         self._rc(self.lib.ref_linear_zero_grad(self.h))
+
+    def apply_sgd(self, lr):
+        self._rc(self.lib.ref_linear_sgd(self.h, lr))
+
+    def weight(self):
+        w = np.zeros_like(self.w)
+        self._rc(self.lib.ref_linear_weight(self.h, w))
+        return w
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -347,6 +347,24 @@ int ref_mlp_grads(void* h, float* g_gate, float* g_up, float* g_down) {
     });
 }
 
+// QuantLinearLayer::apply_sgd (trainsim.cpp:137-143) of gate, up, down, and the weights
+int ref_mlp_sgd(void* h, double lr) {
+    return guarded([&] {
+        auto* m = static_cast<RefMlp*>(h);
+        m->gate->apply_sgd(lr);
+        m->up->apply_sgd(lr);
+        m->down->apply_sgd(lr);
+    });
+}
+int ref_mlp_weights(void* h, float* w_gate, float* w_up, float* w_down) {
+    return guarded([&] {
+        auto* m = static_cast<RefMlp*>(h);
+        std::memcpy(w_gate, m->gate->weight().data(), m->gate->weight().size() * 4);
+        std::memcpy(w_up, m->up->weight().data(), m->up->weight().size() * 4);
+        std::memcpy(w_down, m->down->weight().data(), m->down->weight().size() * 4);
+    });
+}
+
 // controller_step of every layer (trainsim.cpp:129-133); rates/thresholds of
 // gate, up, down after the update.
 int ref_mlp_controller(void* h, double* rates3, double* thresholds3) {
@@ -421,6 +439,15 @@ int ref_linear_controller(void* h, double* rate, double* threshold) {
 }
 int ref_linear_zero_grad(void* h) {
     return guarded([&] { static_cast<RefLinear*>(h)->l->zero_grad(); });
+}
+int ref_linear_sgd(void* h, double lr) {
+    return guarded([&] { static_cast<RefLinear*>(h)->l->apply_sgd(lr); });
+}
+int ref_linear_weight(void* h, float* w) {
+    return guarded([&] {
+        auto* r = static_cast<RefLinear*>(h);
+        std::memcpy(w, r->l->weight().data(), r->l->weight().size() * 4);
+    });
 }
 
 // ---------------------------------------------------------------------------

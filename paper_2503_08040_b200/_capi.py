@@ -43,6 +43,8 @@ _SIGS = {
     "fbq_cuda_quantize_fallback": (cint, [vp, cint, i64, i64, i64, cint, dbl, vp, vp, i64, vp, vp,
                                           vp, vp, vp, vp, u64, i64, vp]),
     "fbq_cuda_quantize_rtn": (cint, [vp, cint, i64, i64, i64, vp, i64, vp, vp]),
+    "fbq_cuda_sgd_update": (cint, [vp, vp, i64, dbl, vp]),
+    "fbq_cuda_sgd_quantize_rtn": (cint, [vp, vp, i64, i64, dbl, vp, i64, vp, vp]),
     "fbq_cuda_quantize_stochastic": (cint, [vp, cint, i64, i64, i64, u64, i64, vp, i64, vp, vp]),
     "fbq_cuda_gemm": (cint, [vp, i64, vp, cint, vp, i64, vp, cint, vp, vp, vp, i64, i64, i64, vp,
                              cint, i64, cint, cint, vp]),

@@ -333,6 +333,22 @@ int fbq_cuda_sgd_update(float* w, const float* grad, int64_t n, double lr, fbq_s
   return cuda_status(fbq::launch_sgd(w, grad, n, lr, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int fbq_cuda_sgd_quantize_rtn(float* w, const float* grad, int64_t rows, int64_t cols, double lr,
+                              int8_t* codes, int64_t ldq, float* scales, fbq_stream_t stream) {
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!w || !grad || !codes || !scales || ldq < cols) return FBQ_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // one fused pass needs 16-byte vectors of W / dW rows and of the code rows
+  // (grid.y <= 65535); any other layout runs the same two steps as two kernels
+  if (cols % 4 || !aligned16(w) || !aligned16(grad) || ldq % 16 || !aligned16(codes) ||
+      cdiv(rows, 128) > 65535) {
+    if (int st = fbq_cuda_sgd_update(w, grad, rows * cols, lr, stream)) return st;
+    return fbq_cuda_quantize_rtn(w, FBQ_F32, rows, cols, cols, codes, ldq, scales, stream);
+  }
+  return cuda_status(fbq::launch_sgd_quantize(w, grad, rows, cols, lr, codes, ldq, scales, s));
+}
+
 int fbq_cuda_quantize_rtn(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx,
                           int8_t* codes, int64_t ldq, float* scales, fbq_stream_t stream) {
   if ((codes == nullptr || scales == nullptr) && rows > 0 && cols > 0) return FBQ_ERR_ARG;

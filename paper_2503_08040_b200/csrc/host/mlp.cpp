@@ -259,16 +259,22 @@ struct Mlp {
     double* th = theta.as<double>();
     // weights: one RTN quantization serves forward (K-major) and dgrad (MN-major);
     // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97, 121)
-    launches += 5;  // 2 x RTN(W), K1(X), GLU forward (+ the 2 GEMMs counted in gemm())
+    // after a fused apply_sgd the weight codes already hold RTN(W) of the
+    // current W (written in the same pass as the update): used once as they are
+    const bool w_fresh = w_codes_fresh;
+    w_codes_fresh = false;
+    launches += w_fresh ? 3 : 5;  // 2 x RTN(W), K1(X), GLU forward (+ the 2 GEMMs counted in gemm())
     // side stream: RTN(W_gate|up) then RTN(W_down), joined right before the
     // GEMM that consumes each
     CU_TRY(cudaEventRecord(ev_ffork, s));
     CU_TRY(cudaStreamWaitEvent(side, ev_ffork, 0));
-    FBQ_TRY(fbq_cuda_quantize_rtn(w_gu.p, FBQ_F32, 2 * F, D, D, wgu_codes.as<int8_t>(), ldD,
-                                  wgu_scales.as<float>(), side));
+    if (!w_fresh)
+      FBQ_TRY(fbq_cuda_quantize_rtn(w_gu.p, FBQ_F32, 2 * F, D, D, wgu_codes.as<int8_t>(), ldD,
+                                    wgu_scales.as<float>(), side));
     CU_TRY(cudaEventRecord(ev_wgu, side));
-    FBQ_TRY(fbq_cuda_quantize_rtn(w_d.p, FBQ_F32, D, F, F, wd_codes.as<int8_t>(), ldF,
-                                  wd_scales.as<float>(), side));
+    if (!w_fresh)
+      FBQ_TRY(fbq_cuda_quantize_rtn(w_d.p, FBQ_F32, D, F, F, wd_codes.as<int8_t>(), ldF,
+                                    wd_scales.as<float>(), side));
     CU_TRY(cudaEventRecord(ev_wd, side));
     // X: score + threshold mask + fallback codes + gate/up contexts (trainsim.cpp:80-102)
     FBQ_TRY(fbq_cuda_quantize_linear_input(
@@ -482,6 +488,22 @@ struct Mlp {
         if (e) cudaEventDestroy(e);
   }
 
+  // QuantLinearLayer::apply_sgd on gate, up, down (trainsim.cpp:137-143) fused
+  // with the RTN quantization of the updated weights (fbq_cuda_sgd_quantize_rtn):
+  // W and dW are read once and the next forward uses the codes written here
+  // (w_codes_fresh) instead of re-quantizing W.  Only apply_sgd writes W, so the
+  // codes stay those of the current W until the forward consumes them.
+  bool w_codes_fresh = false;
+  void apply_sgd(double lr, cudaStream_t s) {
+    if (grad_zero_pending) return;  // the gradient is (pending) zero: w - float(lr * 0) == w
+    launches += 2;
+    FBQ_TRY(fbq_cuda_sgd_quantize_rtn(w_gu.as<float>(), g_gu.as<float>(), 2 * F, D, lr,
+                                      wgu_codes.as<int8_t>(), ldD, wgu_scales.as<float>(), s));
+    FBQ_TRY(fbq_cuda_sgd_quantize_rtn(w_d.as<float>(), g_d.as<float>(), D, F, lr,
+                                      wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), s));
+    w_codes_fresh = true;
+  }
+
   // zero_grad is deferred: the next backward's dW GEMMs then WRITE their
   // products instead of reduce-adding them into zeroed buffers (bit-identical:
   // the accumulators are never -0, so fl(0 + x) == x), which saves a 0.7 GB
@@ -558,6 +580,7 @@ struct QuantLinear {
   int64_t In, Out, T, ldIn, ldOut, gIn, gOut, gT;
   DevBuf w, g, w_codes, w_scales, x_codes, x_scales, x_res, x_res_scales, x_mask, ctx, gy_codes,
       gy_scales, theta, count, rate, amax;
+  bool w_codes_fresh = false;  // set by the fused apply_sgd, consumed by the next forward
   int64_t last_blocks = 1;
   double last_fixed_rate = 0.0;  // FixedRate / Off: mask_rate of the last forward (k / n)
 
@@ -602,9 +625,12 @@ struct QuantLinear {
   void forward(const void* x, int64_t tok, int64_t row_off, int step, void* y, cudaStream_t s) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
     if (tok == 0) return;
-    // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97)
-    FBQ_TRY(fbq_cuda_quantize_rtn(w.p, FBQ_F32, Out, In, In, w_codes.as<int8_t>(), ldIn,
-                                  w_scales.as<float>(), s));
+    // quantize_rtn(transpose(W)) == transpose(quantize_rtn(W)) (trainsim.cpp:96-97);
+    // after a fused apply_sgd the codes already hold RTN of the current W (used once)
+    if (!w_codes_fresh)
+      FBQ_TRY(fbq_cuda_quantize_rtn(w.p, FBQ_F32, Out, In, In, w_codes.as<int8_t>(), ldIn,
+                                    w_scales.as<float>(), s));
+    w_codes_fresh = false;
     // score_blocks + mask (trainsim.cpp:80-93) + fallback_quantize + the SR context (:95-102)
     int mode = FBQ_MASK_THRESHOLD;
     const int64_t nblk = cdiv(tok, 128) * gIn;
@@ -852,6 +878,23 @@ int fbq_mlp_get_grads(void* m, float* g_gate, float* g_up, float* g_down) {
   });
 }
 
+int fbq_mlp_apply_sgd(void* m, double lr, fbq_stream_t stream) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<Mlp*>(m)->apply_sgd(lr, reinterpret_cast<cudaStream_t>(stream)); });
+}
+
+int fbq_mlp_get_weights(void* m, float* w_gate, float* w_up, float* w_down) {
+  if (!m) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* mlp = static_cast<Mlp*>(m);
+    CU_TRY(cudaDeviceSynchronize());
+    const size_t n = mlp->F * mlp->D * 4;
+    if (w_gate) CU_TRY(cudaMemcpy(w_gate, mlp->w_gu.p, n, cudaMemcpyDeviceToHost));
+    if (w_up) CU_TRY(cudaMemcpy(w_up, mlp->w_gu.as<float>() + mlp->F * mlp->D, n, cudaMemcpyDeviceToHost));
+    if (w_down) CU_TRY(cudaMemcpy(w_down, mlp->w_d.p, n, cudaMemcpyDeviceToHost));
+  });
+}
+
 int fbq_mlp_get_controller(void* m, double* rates, double* thresholds) {
   if (!m) return FBQ_ERR_ARG;
   return guarded([&] {
@@ -938,7 +981,10 @@ int fbq_linear_apply_sgd(void* l, double lr, fbq_stream_t stream) {
     auto* q = static_cast<QuantLinear*>(l);
     auto s = reinterpret_cast<cudaStream_t>(stream);
     if (q->grad_zero_pending) return;  // grad is (pending) zero: w unchanged
-    FBQ_TRY(fbq_cuda_sgd_update(q->w.as<float>(), q->g.as<float>(), q->Out * q->In, lr, s));
+    // fused with the next forward's RTN(W) (fbq_cuda_sgd_quantize_rtn; see Mlp::apply_sgd)
+    FBQ_TRY(fbq_cuda_sgd_quantize_rtn(q->w.as<float>(), q->g.as<float>(), q->Out, q->In, lr,
+                                      q->w_codes.as<int8_t>(), q->ldIn, q->w_scales.as<float>(), s));
+    q->w_codes_fresh = true;
   });
 }
 int fbq_linear_get_weight(void* l, float* w_host) {

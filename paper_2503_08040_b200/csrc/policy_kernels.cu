@@ -117,15 +117,47 @@ cudaError_t launch_controller_rate(double* theta, const double* rate, double r_m
 }
 
 // QuantLinearLayer::apply_sgd (trainsim.cpp:137-143): w -= float(lr * double(g))
+__device__ __forceinline__ float sgd_elem(float w, float g, double lr) {
+  return __fsub_rn(w, (float)(lr * (double)g));
+}
+// 16-byte vectors, four per thread per iteration (loads issued together) when
+// both pointers are 16-byte aligned; the scalar loop covers the rest
 __global__ void fbq_sgd_kernel(float* w, const float* g, int64_t n, double lr) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    w[i] = __fsub_rn(w[i], (float)(lr * (double)g[i]));
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15u) == 0) {
+    const int64_t nv = n / 4;
+    float4* w4 = reinterpret_cast<float4*>(w);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    for (int64_t i = tid; i < nv; i += 4 * nth) {
+      float4 wv[4], gv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t j = i + k * nth;
+        if (j < nv) {
+          wv[k] = __ldcs(w4 + j);
+          gv[k] = __ldcs(g4 + j);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t j = i + k * nth;
+        if (j < nv)
+          __stcs(w4 + j, make_float4(sgd_elem(wv[k].x, gv[k].x, lr), sgd_elem(wv[k].y, gv[k].y, lr),
+                                     sgd_elem(wv[k].z, gv[k].z, lr), sgd_elem(wv[k].w, gv[k].w, lr)));
+      }
+    }
+    done = nv * 4;
+  }
+  for (int64_t i = done + tid; i < n; i += nth) w[i] = sgd_elem(w[i], g[i], lr);
 }
 
 cudaError_t launch_sgd(float* w, const float* g, int64_t n, double lr, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  int64_t blocks = (n / 4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
   fbq_sgd_kernel<<<(unsigned)blocks, 256, 0, s>>>(w, g, n, lr);
   return cudaGetLastError();
 }

@@ -755,6 +755,54 @@ fbq_quantize_reg_kernel(QuantParams p) {
   quantize_block_reg<T, kSR>(p, blockIdx.y, blockIdx.x, (int64_t)blockIdx.y * gridDim.x + blockIdx.x, raw, red);
 }
 
+// QuantLinearLayer::apply_sgd (trainsim.cpp:137-143), w -= float(lr * double(g)),
+// fused with the RTN quantization of the updated weight that the next forward
+// runs (quantize_rtn(W), trainsim.cpp:96): one 128 x 128 fp32 block per CTA;
+// W and dW are read once, W' is written back and its codes and block scale
+// come out of the same registers.  Bit-identical to fbq_sgd_kernel followed by
+// the RTN quantizer (same per-element expression, same quantize_block_reg).
+__global__ void __launch_bounds__(kQuantThreads, 2)
+fbq_sgd_quantize_kernel(QuantParams p, float* w, const float* g, double lr) {
+  __shared__ float red[2 * (kQuantThreads / 32)];
+  using Tl = Tiling<float>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  uint4 raw[NP];
+  load_block_reg<float>(p, bi, bj, raw);
+  const int lc = (threadIdx.x % VPR) * V, lrow = threadIdx.x / VPR;
+  const int64_t r0 = bi * kBlock + lrow, cc = bj * kBlock + lc;
+  const int64_t left = p.rows - r0;
+  const int nrow = left <= 0 ? 0 : (left >= (int64_t)NP * RPP ? NP : (int)((left + RPP - 1) / RPP));
+  if (cc < p.cols) {
+    // dW in two halves of NP / 2 vectors, each half's loads issued together (64
+    // raw + 32 registers: one latency round per half instead of one per vector)
+    constexpr int H = NP / 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4 gv[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const int ps = h * H + k;
+        gv[k] = ps < nrow ? __ldcs(reinterpret_cast<const float4*>(g + (r0 + (int64_t)ps * RPP) * p.ldx + cc))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const int ps = h * H + k;
+        if (ps >= nrow) break;
+        const float4 wv = make_float4(__fsub_rn(__uint_as_float(raw[ps].x), (float)(lr * (double)gv[k].x)),
+                                      __fsub_rn(__uint_as_float(raw[ps].y), (float)(lr * (double)gv[k].y)),
+                                      __fsub_rn(__uint_as_float(raw[ps].z), (float)(lr * (double)gv[k].z)),
+                                      __fsub_rn(__uint_as_float(raw[ps].w), (float)(lr * (double)gv[k].w)));
+        raw[ps] = make_uint4(__float_as_uint(wv.x), __float_as_uint(wv.y), __float_as_uint(wv.z),
+                             __float_as_uint(wv.w));
+        __stcs(reinterpret_cast<float4*>(w + (r0 + (int64_t)ps * RPP) * p.ldx + cc), wv);
+      }
+    }
+  }
+  quantize_block_reg<float, 0>(p, bi, bj, bi * (int64_t)gridDim.x + bj, raw, red);
+}
+
 // Persistent + TMA ring + register compute (bf16): tiles land in a kQStages
 // shared-memory ring by TMA while the CTA quantizes the current tile from
 // registers; a slot is handed back to TMA as soon as its values are in registers.
@@ -2156,6 +2204,23 @@ cudaError_t launch_rmsnorm_quantize(const QuantParams& p, bool bf16, const float
   if (nsr == 1) FBQ_RQ(float, 1, 1, t32);
   FBQ_RQ(float, 0, 1, t32);
 #undef FBQ_RQ
+}
+
+// (after launch_ex)
+cudaError_t launch_sgd_quantize(float* w, const float* g, int64_t rows, int64_t cols, double lr,
+                                int8_t* codes, int64_t ldq, float* scales, cudaStream_t s) {
+  QuantParams p = {};
+  p.x = w;
+  p.rows = rows;
+  p.cols = cols;
+  p.ldx = cols;
+  p.ldq = ldq;
+  p.vec_store = 1;
+  p.mask_mode = kMaskNone;
+  p.codes = codes;
+  p.scales = scales;
+  const dim3 grid((unsigned)((cols + kBlock - 1) / kBlock), (unsigned)((rows + kBlock - 1) / kBlock));
+  return launch_ex(fbq_sgd_quantize_kernel, grid, dim3(kQuantThreads), 0, s, false, p, w, g, lr);
 }
 
 }  // namespace fbq

@@ -96,6 +96,8 @@ cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
 cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s);
 cudaError_t launch_zero_count(int* count, cudaStream_t s);
+cudaError_t launch_sgd_quantize(float* w, const float* g, int64_t rows, int64_t cols, double lr,
+                                int8_t* codes, int64_t ldq, float* scales, cudaStream_t s);
 cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,
                               double r_min, double r_max, double alpha, double* last_rate,
                               cudaStream_t s);

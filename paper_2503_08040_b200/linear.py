@@ -55,6 +55,8 @@ _sigs = {
     "fbq_mlp_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "fbq_mlp_gemm_time": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "fbq_mlp_launch_count": (C.c_int64, [C.c_void_p]),
+    "fbq_mlp_apply_sgd": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
+    "fbq_mlp_get_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 for _n, (_r, _a) in _sigs.items():
     _f = getattr(lib, _n)
@@ -84,6 +86,8 @@ for _name, (_res, _args) in {
     "fbq_linear_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fbq_linear_grad_ptr": (C.c_void_p, [C.c_void_p]),
     "fbq_linear_get_controller": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "fbq_linear_apply_sgd": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
+    "fbq_linear_get_weight": (C.c_int, [C.c_void_p, C.c_void_p]),
 }.items():
     _f = getattr(lib, _name)
     _f.restype, _f.argtypes = _res, _args
@@ -250,6 +254,19 @@ class GluMlp:
                "get_grads")
         return gg, gu, gd
 
+    def apply_sgd(self, lr: float):
+        """QuantLinearLayer::apply_sgd on gate, up, down (trainsim.cpp:137-143), on the
+        current stream after the backward; fused with the next forward's RTN(W)."""
+        _check(lib.fbq_mlp_apply_sgd(self._h, lr, _stream()), "apply_sgd")
+
+    def weights_host(self):
+        wg = np.empty((self.d_ff, self.d_model), np.float32)
+        wu = np.empty_like(wg)
+        wd = np.empty((self.d_model, self.d_ff), np.float32)
+        _check(lib.fbq_mlp_get_weights(self._h, wg.ctypes.data, wu.ctypes.data, wd.ctypes.data),
+               "get_weights")
+        return wg, wu, wd
+
     def set_thresholds(self, theta_gate_up: float, theta_down: float):
         _check(lib.fbq_mlp_set_thresholds(self._h, theta_gate_up, theta_down), "set_thresholds")
 
@@ -356,3 +373,12 @@ class QuantLinear:
         r, t = C.c_double(), C.c_double()
         _check(lib.fbq_linear_get_controller(self._h, C.byref(r), C.byref(t)), "linear get_controller")
         return r.value, t.value
+
+    def apply_sgd(self, lr: float):
+        """QuantLinearLayer::apply_sgd (trainsim.cpp:137-143), fused with the next forward's RTN(W)."""
+        _check(lib.fbq_linear_apply_sgd(self._h, lr, _stream()), "linear apply_sgd")
+
+    def weight_host(self):
+        w = np.empty((self.out_features, self.in_features), np.float32)
+        _check(lib.fbq_linear_get_weight(self._h, w.ctypes.data), "linear get_weight")
+        return w
