@@ -10,4 +10,4 @@ timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 if [ "$1" = "ncu" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu-baseline --e2e-steps 0 > gpurun_out/b_ncu.log 2>&1
 fi
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; cat gpurun_out/bench.json gpurun_out/bench_ref.json
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; cat gpurun_out/bench.json gpurun_out/bench_ref.json
