@@ -164,7 +164,7 @@ class GluMlp:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are gone at interpreter exit)
             lib.fbq_mlp_destroy(h)
             self._h = None
 
@@ -323,7 +323,7 @@ class QuantLinear:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:
             lib.fbq_linear_destroy(h)
             self._h = None
 

@@ -91,18 +91,23 @@ def test_mlp_multi_step_with_controller(mods):
 
 
 def test_mlp_bf16_fast_path_within_tolerance(mods):
-    """bf16 activations/intermediates + FMA epilogue: tolerance vs the fp32 reference."""
+    """bf16 activations/intermediates + FMA epilogue: tolerance vs the reference
+    fed the SAME bf16-rounded inputs (so the bound measures the kernels, not the
+    input rounding; the BASELINE-shape version with the stated bounds is
+    test_gpu_baseline_shapes.py::test_c3_bench_fast_path_vs_reference_same_inputs)."""
     import torch
+    from tests.helpers import bf16_round
     linear, RefMlp = mods
     wg, wu, wd = weights(5)
     x, gy = inputs(6)
+    x, gy = bf16_round(x), bf16_round(gy)
     ref = RefMlp(wg, wu, wd, threshold=4.0)
     y_r, gx_r = ref.step(x, gy, 0)
     m = linear.GluMlp(wg, wu, wd, T, threshold_init=4.0)  # bf16 / FMA defaults
     y = m.forward(_dev(x, torch.bfloat16), 0).float().cpu().numpy()
     gx = m.backward(_dev(gy, torch.bfloat16), 0).float().cpu().numpy()
-    assert rel_fro(y, y_r) < 3e-2
-    assert rel_fro(gx, gx_r) < 5e-2
+    assert rel_fro(y, y_r) < 1e-2   # bf16 a|b, h and y roundings (~3e-3 measured at C3 shape)
+    assert rel_fro(gx, gx_r) < 5e-2  # + stochastic-rounding decisions moved by bf16 intermediates
     for g, g_r in zip(m.grads_host(), ref.grads()):
         assert rel_fro(g, g_r) < 5e-2
 
