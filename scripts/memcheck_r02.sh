@@ -12,4 +12,5 @@ run tests/test_gpu_rounding.py -k packed
 run tests/test_gpu_mlp.py
 run tests/test_gpu_linear.py
 run tests/test_gpu_abi_contract.py
+run tests/test_gpu_sgd.py
 cat $out
