@@ -582,10 +582,24 @@ def gemm_sweep(device):
         scores = fbq.score_blocks(x)
         y = torch.empty(M, N, device=device, dtype=torch.bfloat16)
         row = {}
-        for rate in (0.0, 0.05, 0.10, 0.20):
-            fa = fbq.fallback_quantize(x, fbq.mask_topk(scores, rate))
-            t = timeit(lambda: fbq.fallback_gemm(fa, wq, out=y, exact=False))
-            row[f"rate_{rate:.2f}"] = round(2 * M * N * K / t / 1e12, 1)
+        # the four rates interleaved over three rounds, median per rate (a
+        # sequential sweep hands the later rates a hotter, more power-capped part)
+        rates = (0.0, 0.05, 0.10, 0.20)
+        fas = {r: fbq.fallback_quantize(x, fbq.mask_topk(scores, r)) for r in rates}
+        ts = {r: [] for r in rates}
+        for _ in range(3):
+            for r in rates:
+                ts[r].append(timeit(lambda: fbq.fallback_gemm(fas[r], wq, out=y, exact=False)))
+        for r in rates:
+            row[f"rate_{r:.2f}"] = round(2 * M * N * K / sorted(ts[r])[1] / 1e12, 1)
+        if M == 4096:
+            # C1 as SURVEY 8d states it: fp32 output (the reference's DenseMatrix)
+            y32 = torch.empty(M, N, device=device, dtype=torch.float32)
+            for r in rates:
+                t = timeit(lambda: fbq.fallback_gemm(fas[r], wq, out=y32, exact=False))
+                row[f"rate_{r:.2f}_fp32_out"] = round(2 * M * N * K / t / 1e12, 1)
+            del y32
+        del fas
         fa = fbq.fallback_quantize(x, fbq.mask_topk(scores, 0.10))
         t = timeit(lambda: fbq.fallback_gemm(fa, wq, out=y, exact=True))
         row["rate_0.10_exact_epilogue"] = round(2 * M * N * K / t / 1e12, 1)
@@ -609,11 +623,11 @@ def gemm_sweep(device):
     wq = fbq.transpose(fbq.quantize_rtn(w))
     wb = w.to(torch.bfloat16)
     msweep = {}
-    for M in (1024, 4096, 16384, 65536):
+    for M in (1024, 2048, 4096, 8192, 16384, 32768, 65536):
         x = make_activations(M, K, 12, device, torch.bfloat16)
         fa = fbq.fallback_quantize(x, fbq.mask_topk(fbq.score_blocks(x), 0.05))
         y = torch.empty(M, N, device=device, dtype=torch.bfloat16)
-        iters = 3 if M >= 65536 else 10
+        iters = 3 if M >= 32768 else 10
         t = timeit(lambda: fbq.fallback_gemm(fa, wq, out=y, exact=False), iters=iters)
         tb = timeit(lambda: torch.matmul(x, wb.t(), out=y), iters=iters)
         msweep[f"M={M}"] = {"fbq_TOPS": round(2 * M * N * K / t / 1e12, 1),
