@@ -321,7 +321,86 @@ ingress(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensor
       for (int i = 0; i < 64; ++i) a += acc[i].x + acc[i].y;
       if (a == 1234.5f) sink[0] = a;
     }
-  } else if (kEpi != 3 && kEpi != 4 && kEpi != 8 && warp >= 4) {
+  } else if ((kEpi == 9 || kEpi == 10) && warp >= 4) {
+    if constexpr (kEpi == 9 || kEpi == 10) {
+      // De-phased warp pair: the two epilogue warps of a sub-partition (same TMEM
+      // lane quadrant q, column halves h) alternate -- while one loads two
+      // 32-column chunks from TMEM the other converts two, so the TMEM read port
+      // and the ALU (I2F) work at the same time instead of both warps loading,
+      // then both converting.  The odd warp converts the previous item's last two
+      // chunks while the even warp loads.  kEpi 9: a named barrier per phase
+      // (bar.sync 1+q, 64 threads); kEpi 10: the same orders without barriers.
+      setmaxnreg_inc<224>();
+      const int q = warp & 3, h = (warp - 4) >> 2;
+      const uint32_t lane_base = tmem + ((q * 32) << 16) + h * 128;
+      const uint32_t tempty_r = kCta == 2 ? mapa_shared(smem_u32(tempty), 0) : smem_u32(tempty);
+      float2 acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = make_float2(0.f, 0.f);
+      const float s = 1.0f + blockIdx.x * 1e-7f;
+      const int n_items = ((tiles - unit + units - 1) / units) * KB;
+      const int bar = 1 + q;
+      auto pair_sync = [&]() {
+        if constexpr (kEpi == 9) asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+      };
+      uint32_t va[32], vb[32];
+      for (int it = 0; it < n_items; ++it) {
+        const int slot = it & 1;
+        const uint32_t tb = lane_base + slot * 256;
+        if (h == 0) {
+          mbar_wait(tfull + slot, (it >> 1) & 1);
+          tc_fence_after();
+          ld32p(tb, va);
+          ld32p(tb + 32, vb);
+          tmem_ld_wait();
+          pair_sync();
+          consume32(va, acc, s);
+          consume32(vb, acc + 16, s);
+          pair_sync();
+          ld32p(tb + 64, va);
+          ld32p(tb + 96, vb);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_any(tempty + slot, tempty_r + slot * 8, kCta == 2);
+          pair_sync();
+          consume32(va, acc + 32, s);
+          consume32(vb, acc + 48, s);
+          pair_sync();
+        } else {
+          if (it > 0) {
+            consume32(va, acc + 32, s);
+            consume32(vb, acc + 48, s);
+          }
+          pair_sync();
+          mbar_wait(tfull + slot, (it >> 1) & 1);
+          tc_fence_after();
+          ld32p(tb, va);
+          ld32p(tb + 32, vb);
+          tmem_ld_wait();
+          pair_sync();
+          consume32(va, acc, s);
+          consume32(vb, acc + 16, s);
+          pair_sync();
+          ld32p(tb + 64, va);
+          ld32p(tb + 96, vb);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_any(tempty + slot, tempty_r + slot * 8, kCta == 2);
+          pair_sync();
+        }
+      }
+      if (h == 1 && n_items > 0) {
+        consume32(va, acc + 32, s);
+        consume32(vb, acc + 48, s);
+      }
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) a += acc[i].x + acc[i].y;
+      if (a == 1234.5f) sink[0] = a;
+    }
+  } else if (kEpi != 3 && kEpi != 4 && kEpi != 8 && kEpi != 9 && kEpi != 10 && warp >= 4) {
     setmaxnreg_inc<224>();
     const int q = warp & 3, h = (warp - 4) >> 2;
     const uint32_t lane_base = tmem + ((q * 32) << 16) + h * 128;
@@ -495,10 +574,11 @@ int main() {
   fill<<<1024, 256>>>((uint32_t*)b, (size_t)kN * kK / 4, 2);
   run<1, 4, 0>(a, b);
   run<1, 4, 1>(a, b);
+  run<1, 4, 9>(a, b);
+  run<1, 4, 10>(a, b);
   run<1, 4, 4>(a, b);
-  run<1, 4, 6>(a, b);
-  run<1, 4, 8>(a, b);
-  run<1, 3, 6>(a, b);
   run<1, 4, 7>(a, b);
+  run<1, 4, 1>(a, b);
+  run<1, 4, 9>(a, b);
   return 0;
 }
