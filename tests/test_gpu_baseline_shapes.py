@@ -178,6 +178,8 @@ def _c3_inputs(step):
 
 
 def test_c3_mlp_full_dims_exact_vs_reference(F, R, c3_weights):
+    """C3 at full dims, exact mode: two training steps (fwd, bwd, controller, SGD
+    between them) bit-identical to the reference."""
     import torch
     from oracle.oracle import RefMlp
     from paper_2503_08040_b200 import linear
@@ -199,6 +201,13 @@ def test_c3_mlp_full_dims_exact_vs_reference(F, R, c3_weights):
         r_rates, r_th = ref.controller()
         assert rates[0] == r_rates[0] and rates[1] == r_rates[2], (step, rates, r_rates)
         assert th_g[0] == r_th[0] and th_g[1] == r_th[2], (step, th_g, r_th)
+        if step == 0:
+            # QuantLinearLayer::apply_sgd on the three weights (trainsim.cpp:137-143); the
+            # device update is fused with the weight RTN that step 1's forward then uses
+            m.apply_sgd(0.05)
+            ref.apply_sgd(0.05)
+            for w, w_r in zip(m.weights_host(), ref.weights()):
+                assert np.array_equal(w.view(np.int32), w_r.view(np.int32))
     for g, g_r in zip(m.grads_host(), ref.grads()):
         assert np.array_equal(g.view(np.int32), g_r.view(np.int32)), rel_fro(g, g_r)
 
