@@ -81,13 +81,15 @@ int fbq_mlp_step_host(void* mlp, const float* x, const float* gy, int64_t tokens
                       float* y, float* gx);
 
 /* Pipelined host API: enqueue one step (zero_grad if FBQ_STEP_ZERO_GRAD, fwd,
- * bwd, controller_step if FBQ_STEP_CONTROLLER) over host fp32 buffers and
+ * bwd, controller_step if FBQ_STEP_CONTROLLER, apply_sgd at fbq_mlp_set_sgd_lr's
+ * rate if FBQ_STEP_SGD -- the reference trainer's step) over host fp32 buffers and
  * return.  Step i's H2D copies overlap step i-1's compute and step i-1's D2H
  * copies overlap step i's (two device slots).  Host buffers must stay valid,
  * and outputs must not be read, until fbq_mlp_host_sync returns; pinned
  * buffers make the copies truly asynchronous. */
 #define FBQ_STEP_ZERO_GRAD 1
 #define FBQ_STEP_CONTROLLER 2
+#define FBQ_STEP_SGD 4
 int fbq_mlp_step_host_async(void* mlp, const float* x, const float* gy, int64_t tokens, int step,
                             float* y, float* gx, int flags);
 int fbq_mlp_host_sync(void* mlp);
@@ -128,6 +130,8 @@ int fbq_mlp_get_controller(void* mlp, double* rates, double* thresholds);
  * instead of re-quantizing W -- the same codes, one pass over W instead of two.
  * A pending zero_grad makes it a no-op (the reference: w -= lr * 0). */
 int fbq_mlp_apply_sgd(void* mlp, double lr, fbq_stream_t stream);
+/* learning rate of the FBQ_STEP_SGD flag of fbq_mlp_step_host_async (default 0) */
+int fbq_mlp_set_sgd_lr(void* mlp, double lr);
 /* synchronous host copies of the fp32 master weights (gate, up: d_ff x
  * d_model; down: d_model x d_ff) */
 int fbq_mlp_get_weights(void* mlp, float* w_gate, float* w_up, float* w_down);

@@ -494,6 +494,7 @@ struct Mlp {
   // (w_codes_fresh) instead of re-quantizing W.  Only apply_sgd writes W, so the
   // codes stay those of the current W until the forward consumes them.
   bool w_codes_fresh = false;
+  double sgd_lr = 0.0;  // the host step API's learning rate (FBQ_STEP_SGD)
   void apply_sgd(double lr, cudaStream_t s) {
     if (grad_zero_pending) return;  // the gradient is (pending) zero: w - float(lr * 0) == w
     launches += 2;
@@ -547,6 +548,7 @@ struct Mlp {
       CU_TRY(cudaEventRecord(a_fwd[slot], a_cs));
       backward(agy[slot].p, tok, 0, step, agx[slot].p, a_cs, /*gy_ready=*/true);
       if (flags & FBQ_STEP_CONTROLLER) controller(a_cs);
+      if (flags & FBQ_STEP_SGD) apply_sgd(sgd_lr, a_cs);
       CU_TRY(cudaEventRecord(a_done[slot], a_cs));
     } catch (...) {
       c.act_dtype = saved;
@@ -783,7 +785,7 @@ int fbq_mlp_zero_grad(void* m, fbq_stream_t stream) {
 int fbq_mlp_step_host_async(void* m, const float* x, const float* gy, int64_t tokens, int step,
                             float* y, float* gx, int flags) {
   if (!m || (tokens > 0 && (!x || !gy || !y || !gx))) return FBQ_ERR_ARG;
-  if (flags & ~(FBQ_STEP_ZERO_GRAD | FBQ_STEP_CONTROLLER)) return FBQ_ERR_ARG;
+  if (flags & ~(FBQ_STEP_ZERO_GRAD | FBQ_STEP_CONTROLLER | FBQ_STEP_SGD)) return FBQ_ERR_ARG;
   return guarded([&] { static_cast<Mlp*>(m)->step_host_async(x, gy, tokens, step, y, gx, flags); });
 }
 
@@ -881,6 +883,12 @@ int fbq_mlp_get_grads(void* m, float* g_gate, float* g_up, float* g_down) {
 int fbq_mlp_apply_sgd(void* m, double lr, fbq_stream_t stream) {
   if (!m) return FBQ_ERR_ARG;
   return guarded([&] { static_cast<Mlp*>(m)->apply_sgd(lr, reinterpret_cast<cudaStream_t>(stream)); });
+}
+
+int fbq_mlp_set_sgd_lr(void* m, double lr) {
+  if (!m) return FBQ_ERR_ARG;
+  static_cast<Mlp*>(m)->sgd_lr = lr;
+  return FBQ_OK;
 }
 
 int fbq_mlp_get_weights(void* m, float* w_gate, float* w_up, float* w_down) {

@@ -57,6 +57,7 @@ _sigs = {
     "fbq_mlp_launch_count": (C.c_int64, [C.c_void_p]),
     "fbq_mlp_apply_sgd": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
     "fbq_mlp_get_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fbq_mlp_set_sgd_lr": (C.c_int, [C.c_void_p, C.c_double]),
 }
 for _n, (_r, _a) in _sigs.items():
     _f = getattr(lib, _n)
@@ -232,7 +233,7 @@ class GluMlp:
                "step_host")
         return y, gx
 
-    STEP_ZERO_GRAD, STEP_CONTROLLER = 1, 2
+    STEP_ZERO_GRAD, STEP_CONTROLLER, STEP_SGD = 1, 2, 4
 
     def step_host_async(self, x, gy, step: int, y, gx, flags: int = 0):
         """Enqueue one pipelined host-buffer step (fbq_mlp_step_host_async); the
@@ -258,6 +259,10 @@ class GluMlp:
         """QuantLinearLayer::apply_sgd on gate, up, down (trainsim.cpp:137-143), on the
         current stream after the backward; fused with the next forward's RTN(W)."""
         _check(lib.fbq_mlp_apply_sgd(self._h, lr, _stream()), "apply_sgd")
+
+    def set_sgd_lr(self, lr: float):
+        """Learning rate of STEP_SGD in step_host_async."""
+        _check(lib.fbq_mlp_set_sgd_lr(self._h, lr), "set_sgd_lr")
 
     def weights_host(self):
         wg = np.empty((self.d_ff, self.d_model), np.float32)

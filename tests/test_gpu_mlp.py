@@ -294,3 +294,36 @@ def test_mlp_context_bytes_vs_bf16(mods):
         ours, bf = m.context_bytes(t)
         r[packed] = ours / bf
     assert 0.55 < r[True] < 0.70 and 0.80 < r[False] < 0.92, r
+
+
+def test_mlp_pipelined_host_api_training_steps_with_sgd(mods):
+    """fbq_mlp_step_host_async with FBQ_STEP_SGD (zero_grad, fwd, bwd, controller,
+    fused SGD + weight RTN per step) == the device API doing the same steps:
+    outputs, weights and controller state bit-identical over four steps."""
+    import torch
+    linear, _ = mods
+    wg, wu, wd = weights(13)
+    kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True, threshold_init=2.0)
+    m1 = linear.GluMlp(wg, wu, wd, T, **kw)
+    m2 = linear.GluMlp(wg, wu, wd, T, **kw)
+    steps = [inputs(40 + i) for i in range(4)]
+    want = []
+    for i, (x, gy) in enumerate(steps):
+        m1.zero_grad()
+        y = m1.forward(_dev(x), i).cpu().numpy()
+        gx = m1.backward(_dev(gy), i).cpu().numpy()
+        m1.controller_step()
+        m1.apply_sgd(0.1)
+        want.append((y, gx))
+    outs = [(np.empty_like(x), np.empty_like(x)) for x, _ in steps]
+    m2.set_sgd_lr(0.1)
+    flags = m2.STEP_ZERO_GRAD | m2.STEP_CONTROLLER | m2.STEP_SGD
+    for i, ((x, gy), (y, gx)) in enumerate(zip(steps, outs)):
+        m2.step_host_async(x, gy, i, y, gx, flags)
+    m2.host_sync()
+    for (y, gx), (yw, gxw) in zip(outs, want):
+        assert np.array_equal(y, yw) and np.array_equal(gx, gxw)
+    for a, b in zip(m1.weights_host(), m2.weights_host()):
+        assert np.array_equal(a.view(np.int32), b.view(np.int32))
+    assert m1.controller_state() == m2.controller_state()
+
