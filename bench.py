@@ -274,6 +274,92 @@ def cpu_reference_c1(rate=0.10):
             "score+mask+fallback_quantize_s": round(t_q, 3)}
 
 
+def cpu_reference_sweep():
+    """C2 and C5 (M <= 4K) in full on the reference's own CPU path,
+    timed on this box's host cores beside the GPU sweeps (the GPU arm's input
+    recipes; AVX2 backend; quantizers single-threaded as shipped, GEMMs with
+    set_gemm_threads(nproc)).  Only the reference calls are timed (raw C entry
+    points on preallocated buffers: no Python conversion inside the timing).
+    C2: score_blocks + mask_threshold (the GPU sweep's theta) + fallback_quantize
+    on fp32 input (the reference has no bf16), GB/s of the same algorithmic
+    bytes as the GPU rows.  C5: fallback_gemm at 5 % topk fallback, GOPS = 2MNK/t."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from oracle.oracle import REF_oracle, cdiv, dense_to_compact
+    from paper_2503_08040_b200 import fbq
+    ref = REF_oracle()
+    if ref is None:
+        raise FileNotFoundError("oracle/_ref/libfbq_ref.so not built")
+    cores = os.cpu_count() or 1
+    ref.set_gemm_threads(cores)
+    g = 128
+    out = {"cores": cores, "cpu_model": cpu_model(), "kind": "reference",
+           "backend": "AVX2 (auto-selected), fallback_quantize single-threaded, fallback_gemm on all cores"}
+
+    def fq_timed(x, mask):
+        r, c = x.shape
+        gr, gc = cdiv(r, g), cdiv(c, g)
+        n_mask = int(mask.sum())
+        codes = np.zeros((r, c), np.int16)
+        scales = np.zeros((gr, gc), np.float32)
+        rcomp = np.zeros((max(n_mask, 1), g, g), np.int16)
+        rsc = np.zeros(max(n_mask, 1), np.float32)
+        ridx = np.zeros((gr, gc), np.int32)
+        nres = C.c_int64(0)
+        t0 = time.perf_counter()
+        rc = ref._fq(x, r, c, g, mask, codes, scales, rcomp, rsc, ridx, C.byref(nres))
+        t = time.perf_counter() - t0
+        if rc:
+            raise RuntimeError(ref._err().decode())
+        return t, codes, scales, rcomp, rsc
+
+    c2 = {}
+    for (R, Cc) in [(8192, 4096), (8192, 14336)]:
+        x = np.ascontiguousarray(make_activations(R, Cc, 5, "cpu", torch.float32).numpy())
+        nb = (R // g) * (Cc // g)
+        for rate in (0.0, 0.05, 0.20):
+            t0 = time.perf_counter()
+            sc = ref.score_blocks_absmax(x)
+            t_s = time.perf_counter() - t0
+            theta, _ = fbq.theta_for_rate(sc, rate)
+            t0 = time.perf_counter()
+            mask = ref.mask_threshold(sc, theta)
+            t_m = time.perf_counter() - t0
+            t_q, *_ = fq_timed(x, mask.reshape(R // g, Cc // g))
+            f = float(mask.sum()) / nb
+            t = t_s + t_m + t_q
+            byt = R * Cc * (4 + 1) + f * R * Cc + nb * 4 * (1 + f) + nb / 8
+            c2[f"{R}x{Cc} float32 rate={rate:.2f}"] = {"s": round(t, 3), "GBps": round(byt / t / 1e9, 2),
+                                                       "flagged": round(f, 4)}
+        del x
+    out["C2"] = c2
+
+    N, K = 28672, 8192
+    rng = np.random.default_rng(12)
+    w = (rng.standard_normal((N, K), dtype=np.float32) * 0.02)
+    t0 = time.perf_counter()
+    wc, ws = ref.quantize_rtn(np.ascontiguousarray(w.T))  # quantize_rtn(W^T), trainsim.cpp:96-97
+    out["C5 quantize_rtn(W^T) 8192x28672 s"] = round(time.perf_counter() - t0, 2)
+    del w
+    c5 = {}
+    for M in (1024, 2048, 4096):
+        x = np.ascontiguousarray(make_activations(M, K, 12, "cpu", torch.float32).numpy())
+        mask = ref.mask_topk(ref.score_blocks_absmax(x), 0.05)
+        _, ac, asc, rcomp, rsc = fq_timed(x, mask)
+        yo = np.zeros((M, N), np.float32)
+        mk = np.ascontiguousarray(mask, np.uint8)
+        t0 = time.perf_counter()
+        rc = ref._fbg(ac, asc, mk, rcomp, rsc, wc, ws, M, N, K, g, yo)
+        t = time.perf_counter() - t0
+        if rc:
+            raise RuntimeError(ref._err().decode())
+        c5[f"M={M}"] = {"fallback_gemm_s": round(t, 2), "GOPS": round(2 * M * N * K / t / 1e9, 1)}
+        del x, yo
+    out["C5 28672x8192 rate 0.05"] = c5
+    return out
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return  # rank 0 alone runs and prints the CPU reference
@@ -1126,6 +1212,13 @@ def run_ours(args, rank, world, local):
                 sweep["C1 cpu reference (same box)"] = cpu_reference_c1()
             except Exception as ex:  # pragma: no cover
                 sweep["C1 cpu reference (same box)"] = {"error": str(ex)[:200]}
+            try:
+                cref = cpu_reference_sweep()
+                sweep["C5 cpu reference (same box)"] = {k: v for k, v in cref.items() if k != "C2"}
+                if isinstance(qsweep, dict):
+                    qsweep["cpu reference (same box)"] = {k: cref[k] for k in ("cores", "cpu_model", "kind", "C2")}
+            except Exception as ex:  # pragma: no cover
+                sweep["C5 cpu reference (same box)"] = {"error": str(ex)[:200]}
         if not args.no_cpu_baseline and world == 1:
             try:
                 cb = cpu_reference(REF_SAMPLE_TOKENS, 1, 0)
