@@ -125,6 +125,15 @@ int fbq_cuda_rmsnorm_backward(const int16_t* ctx_codes, int64_t ld_ctx, const fl
                               const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
                               const float* gain, void* gx, int64_t ldgx, float* grad_gain,
                               double* row_ws, float* term_ws, fbq_stream_t stream);
+/* The same, with the pre-norm residual block's gradient add fused into the
+ * output: gx = fl(norm.backward(gy) + residual), GluBlock::backward's
+ * add(norm.backward(grad_xn), grad_out) (trainsim.cpp:303-307); residual has
+ * the activation dtype and row stride ld_res.  gx may alias residual. */
+int fbq_cuda_rmsnorm_backward_residual(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales,
+                                       const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
+                                       const float* gain, const void* residual, int64_t ld_res, void* gx,
+                                       int64_t ldgx, float* grad_gain, double* row_ws, float* term_ws,
+                                       fbq_stream_t stream);
 
 /* mask_topk -- policy.cpp:56-71 / policy.hpp:30-31: exactly k = ceil(rate * n)
  * (clamped to n) blocks with the largest scores, ties toward the lower block

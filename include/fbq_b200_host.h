@@ -136,6 +136,32 @@ int fbq_mlp_set_sgd_lr(void* mlp, double lr);
  * d_model; down: d_model x d_ff) */
 int fbq_mlp_get_weights(void* mlp, float* w_gate, float* w_up, float* w_down);
 
+/* ---- the reference's pre-norm residual GLU block: GluBlock (trainsim.hpp:136-146,
+ * trainsim.cpp:294-308), out = h + down(silu(gate(norm(h))) * up(norm(h))), on the
+ * MLP driver above plus an RmsNorm (gain initialised to 1, its 10-bit 1 x 128 input
+ * context).  The norm runs fused into the gate/up input quantizer
+ * (fbq_cuda_rmsnorm_quantize_input: norm(h) is never materialised), the residual
+ * add rides on the down GEMM's accumulate epilogue, and the backward's norm
+ * gradient and residual add are one pass (fbq_cuda_rmsnorm_backward_residual).
+ * fbq_glublock_mlp returns the block's gate/up/down driver: fbq_mlp_controller_step,
+ * _get_grads, _get_weights, _get_controller, _set_thresholds, _wait_grad, ... apply
+ * to it.  h / out / grad_out / grad_h: device, tokens x d_model, act_dtype;
+ * out must not alias h. */
+void* fbq_glublock_create(const fbq_mlp_config* cfg, const float* w_gate, const float* w_up,
+                          const float* w_down);
+void fbq_glublock_destroy(void* block);
+void* fbq_glublock_mlp(void* block);
+int fbq_glublock_forward_device(void* block, const void* h, int64_t tokens, int64_t row_offset, int step,
+                                void* out, fbq_stream_t stream);
+int fbq_glublock_backward_device(void* block, const void* grad_out, int64_t tokens, int64_t row_offset,
+                                 int step, void* grad_h, fbq_stream_t stream);
+/* zero_grad of gate / up / down (deferred, as fbq_mlp_zero_grad) and of the gain */
+int fbq_glublock_zero_grad(void* block, fbq_stream_t stream);
+/* apply_sgd of gate / up / down (fused with the next weight RTN) and RmsNorm::apply_sgd */
+int fbq_glublock_apply_sgd(void* block, double lr, fbq_stream_t stream);
+/* synchronous host copies of the RmsNorm gain and its gradient (d_model floats) */
+int fbq_glublock_get_gain(void* block, float* gain, float* grad_gain);
+
 /* ---- one fallback-quantized linear layer: QuantLinearLayer (trainsim.hpp:38-73,
  * trainsim.cpp:61-135) with 128 x 128 blocks, 8-bit operands, the stochastic X
  * context, threshold fallback and the delay-threshold controller on device.

@@ -515,6 +515,66 @@ class RefLinear:
             self.h = None
 
 
+class RefGluBlock:
+    """The reference's own pre-norm residual GLU block (GluBlock, trainsim.hpp:136-146,
+    trainsim.cpp:294-308) through oracle/_ref (test infrastructure)."""
+
+    def __init__(self, w_gate, w_up, w_down, threshold=1.0, g=128):
+        r = REF_oracle()
+        if r is None:
+            raise FileNotFoundError("oracle/_ref not built")
+        lib = r._l.lib
+        self.lib = lib
+        lib.ref_block_create.restype = C.c_void_p
+        lib.ref_block_create.argtypes = [F32, F32, F32, i64, i64, i64, dbl]
+        lib.ref_block_destroy.argtypes = [C.c_void_p]
+        lib.ref_block_step.argtypes = [C.c_void_p, F32, F32, i64, cint, F32, F32]
+        lib.ref_block_controller.argtypes = [C.c_void_p, F64]
+        lib.ref_block_sgd.argtypes = [C.c_void_p, dbl]
+        lib.ref_block_state.argtypes = [C.c_void_p] + [F32] * 8
+        self.wg = np.ascontiguousarray(w_gate, np.float32)
+        self.wu = np.ascontiguousarray(w_up, np.float32)
+        self.wd = np.ascontiguousarray(w_down, np.float32)
+        self.d_ff, self.d_model = self.wg.shape
+        self.h = lib.ref_block_create(self.wg, self.wu, self.wd, self.d_model, self.d_ff, g, threshold)
+        if not self.h:
+            raise RuntimeError(r._err().decode())
+        self._err = r._err
+
+    def _rc(self, rc):
+        if rc:
+            raise RuntimeError(self._err().decode())
+
+    def step(self, x, grad_out, step):
+        x = np.ascontiguousarray(x, np.float32)
+        grad_out = np.ascontiguousarray(grad_out, np.float32)
+        y, gh = np.zeros_like(x), np.zeros_like(x)
+        self._rc(self.lib.ref_block_step(self.h, x, grad_out, x.shape[0], step, y, gh))
+        return y, gh
+
+    def controller(self):
+        th = np.zeros(3)
+        self._rc(self.lib.ref_block_controller(self.h, th))
+        return th
+
+    def apply_sgd(self, lr):
+        self._rc(self.lib.ref_block_sgd(self.h, lr))
+
+    def state(self):
+        """gain, grad_gain, (W_gate, W_up, W_down), (dW_gate, dW_up, dW_down)"""
+        d, f = self.d_model, self.d_ff
+        gain, gg = np.zeros(d, np.float32), np.zeros(d, np.float32)
+        w = [np.zeros((f, d), np.float32), np.zeros((f, d), np.float32), np.zeros((d, f), np.float32)]
+        g = [np.zeros_like(a) for a in w]
+        self._rc(self.lib.ref_block_state(self.h, gain, gg, *w, *g))
+        return gain, gg, tuple(w), tuple(g)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_block_destroy(self.h)
+            self.h = None
+
+
 class RefRmsNorm:
     """The reference's own RmsNorm (trainsim.cpp:145-219) through oracle/_ref."""
 

@@ -515,4 +515,82 @@ int ref_rms_sgd(void* h, double lr) {
     return guarded([&] { static_cast<RefRms*>(h)->n->apply_sgd(lr); });
 }
 
+// ---------------------------------------------------------------------------
+// The reference's own pre-norm residual GLU block (trainsim.hpp:136-146,
+// trainsim.cpp:294-308): h + down(silu(gate(norm(h))) * up(norm(h))); layer
+// ids 0 / 1 / 2 as RefMlp, block side g.
+struct RefBlock {
+    QuantConfig cfg;
+    std::unique_ptr<GluBlock> b;
+    int64_t d = 0, f = 0;
+};
+void* ref_block_create(const float* w_gate, const float* w_up, const float* w_down, int64_t d_model,
+                       int64_t d_ff, int64_t g, double threshold) {
+    try {
+        auto* r = new RefBlock;
+        r->cfg.block = g;
+        r->cfg.threshold_init = threshold;
+        r->d = d_model;
+        r->f = d_ff;
+        r->b = std::unique_ptr<GluBlock>(new GluBlock{
+            RmsNorm("norm", d_model, r->cfg),
+            QuantLinearLayer("gate", 0, make_dense(w_gate, d_ff, d_model), r->cfg),
+            QuantLinearLayer("up", 1, make_dense(w_up, d_ff, d_model), r->cfg),
+            QuantLinearLayer("down", 2, make_dense(w_down, d_model, d_ff), r->cfg),
+            GluCombine(r->cfg)});
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_block_destroy(void* h) { delete static_cast<RefBlock*>(h); }
+// one forward + backward: out = block(x), grad_h = block.backward(grad_out)
+int ref_block_step(void* h, const float* x, const float* grad_out, int64_t tokens, int step, float* out,
+                   float* grad_h) {
+    return guarded([&] {
+        auto* r = static_cast<RefBlock*>(h);
+        const DenseMatrix y = r->b->forward(make_dense(x, tokens, r->d), step);
+        std::memcpy(out, y.data(), y.size() * sizeof(float));
+        const DenseMatrix gx = r->b->backward(make_dense(grad_out, tokens, r->d), step);
+        std::memcpy(grad_h, gx.data(), gx.size() * sizeof(float));
+    });
+}
+// controller_step of gate, up, down; thresholds after the update
+int ref_block_controller(void* h, double* thresholds3) {
+    return guarded([&] {
+        auto* r = static_cast<RefBlock*>(h);
+        QuantLinearLayer* ls[3] = {&r->b->gate, &r->b->up, &r->b->down};
+        for (int i = 0; i < 3; ++i) {
+            ls[i]->controller_step();
+            thresholds3[i] = ls[i]->threshold();
+        }
+    });
+}
+int ref_block_sgd(void* h, double lr) {
+    return guarded([&] {
+        auto* r = static_cast<RefBlock*>(h);
+        r->b->norm.apply_sgd(lr);
+        r->b->gate.apply_sgd(lr);
+        r->b->up.apply_sgd(lr);
+        r->b->down.apply_sgd(lr);
+    });
+}
+// gain, grad_gain (d_model); weights and their gradients of gate, up, down
+int ref_block_state(void* h, float* gain, float* grad_gain, float* wg, float* wu, float* wd, float* gg,
+                    float* gu, float* gd) {
+    return guarded([&] {
+        auto* r = static_cast<RefBlock*>(h);
+        std::memcpy(gain, r->b->norm.gain().data(), r->d * 4);
+        std::memcpy(grad_gain, r->b->norm.grad_gain().data(), r->d * 4);
+        const size_t n = (size_t)(r->d * r->f) * 4;
+        std::memcpy(wg, r->b->gate.weight().data(), n);
+        std::memcpy(wu, r->b->up.weight().data(), n);
+        std::memcpy(wd, r->b->down.weight().data(), n);
+        std::memcpy(gg, r->b->gate.grad_weight().data(), n);
+        std::memcpy(gu, r->b->up.grad_weight().data(), n);
+        std::memcpy(gd, r->b->down.grad_weight().data(), n);
+    });
+}
+
 } // extern "C"

@@ -298,6 +298,23 @@ int fbq_cuda_rmsnorm_backward(const int16_t* ctx_codes, int64_t ld_ctx, const fl
                                                   term_ws, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int fbq_cuda_rmsnorm_backward_residual(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales,
+                                       const void* gy, int dtype, int64_t rows, int64_t cols, int64_t ldgy,
+                                       const float* gain, const void* residual, int64_t ld_res, void* gx,
+                                       int64_t ldgx, float* grad_gain, double* row_ws, float* term_ws,
+                                       fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!ctx_codes || !ctx_scales || !gy || !gain || !residual || !gx || !grad_gain || !row_ws || !term_ws)
+    return FBQ_ERR_ARG;
+  if (ldgy < cols || ldgx < cols || ld_ctx < cols || ld_res < cols) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_rmsnorm_backward(ctx_codes, ld_ctx, ctx_scales, gy, dtype == FBQ_BF16,
+                                                  rows, cols, ldgy, gain, gx, ldgx, grad_gain, row_ws,
+                                                  term_ws, reinterpret_cast<cudaStream_t>(stream),
+                                                  residual, ld_res));
+}
+
 int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* mask_bits,
                        int32_t* masked_count, fbq_stream_t stream) {
   if (!(rate >= 0.0 && rate <= 1.0)) return FBQ_ERR_ARG;  // policy.cpp:57

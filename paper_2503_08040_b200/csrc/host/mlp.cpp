@@ -251,7 +251,19 @@ struct Mlp {
     return total;
   }
 
-  void forward(const void* x, int64_t tok, int64_t row_off, int step, void* y, cudaStream_t s) {
+  // GluBlock (below): the block's RmsNorm fused into the gate/up input quantizer
+  struct NormIn {
+    const float* gain;
+    int16_t* ctx;
+    int64_t ld_ctx;
+    float* ctx_scales;
+    float* rms_ws;
+  };
+  // norm: quantize norm(x) instead of x (the RmsNorm context is written too);
+  // residual: y = fl(x + down(...)) -- x is copied into y and the down GEMM
+  // accumulates onto it (GluBlock::forward's add(h, d), trainsim.cpp:294-301)
+  void forward(const void* x, int64_t tok, int64_t row_off, int step, void* y, cudaStream_t s,
+               const NormIn* norm = nullptr, bool residual = false) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
     if (tok == 0) return;
     const int64_t gTt = cdiv(tok, 128);
@@ -277,12 +289,21 @@ struct Mlp {
                                     wd_scales.as<float>(), side));
     CU_TRY(cudaEventRecord(ev_wd, side));
     // X: score + threshold mask + fallback codes + gate/up contexts (trainsim.cpp:80-102)
-    FBQ_TRY(fbq_cuda_quantize_linear_input(
-        x, c.act_dtype, tok, D, D, FBQ_MASK_THRESHOLD, c.threshold_init, th,
-        x_mask.as<uint32_t>(), x_codes.as<int8_t>(), ldD, x_scales.as<float>(),
-        x_res.as<int8_t>(), x_res_scales.as<float>(), cnt, ctx_g.as<int8_t>(),
-        layer_seed(c.seed, layer(0), 0, step), ctx_u.as<int8_t>(),
-        layer_seed(c.seed, layer(1), 0, step), row_off, s));
+    if (norm) {
+      FBQ_TRY(fbq_cuda_rmsnorm_quantize_input(
+          x, c.act_dtype, tok, D, D, norm->gain, norm->ctx, norm->ld_ctx, norm->ctx_scales, norm->rms_ws,
+          FBQ_MASK_THRESHOLD, c.threshold_init, th, x_mask.as<uint32_t>(), x_codes.as<int8_t>(), ldD,
+          x_scales.as<float>(), x_res.as<int8_t>(), x_res_scales.as<float>(), cnt, ctx_g.as<int8_t>(),
+          layer_seed(c.seed, layer(0), 0, step), ctx_u.as<int8_t>(), layer_seed(c.seed, layer(1), 0, step),
+          row_off, s));
+    } else {
+      FBQ_TRY(fbq_cuda_quantize_linear_input(
+          x, c.act_dtype, tok, D, D, FBQ_MASK_THRESHOLD, c.threshold_init, th,
+          x_mask.as<uint32_t>(), x_codes.as<int8_t>(), ldD, x_scales.as<float>(),
+          x_res.as<int8_t>(), x_res_scales.as<float>(), cnt, ctx_g.as<int8_t>(),
+          layer_seed(c.seed, layer(0), 0, step), ctx_u.as<int8_t>(),
+          layer_seed(c.seed, layer(1), 0, step), row_off, s));
+    }
     // [a | b] = fallback_gemm(X, [W_g; W_u]^T)
     CU_TRY(cudaStreamWaitEvent(s, ev_wgu, 0));
     gemm([&] { return fbq_cuda_gemm(x_codes.as<int8_t>(), ldD, x_scales.as<float>(), FBQ_K_MAJOR,
@@ -296,12 +317,13 @@ struct Mlp {
         h_mask.as<uint32_t>(), h_codes.as<int8_t>(), ldF, h_scales.as<float>(),
         h_res.as<int8_t>(), h_res_scales.as<float>(), cnt + 1, ctx_h.as<int8_t>(),
         layer_seed(c.seed, layer(2), 0, step), row_off, nullptr, 0, s));
-    // y = fallback_gemm(h, W_d^T)
+    // y = fallback_gemm(h, W_d^T)   (GluBlock: y = x + fallback_gemm(...), accumulated onto x)
+    if (residual) CU_TRY(cudaMemcpyAsync(y, x, (size_t)tok * D * esize(c.act_dtype), cudaMemcpyDeviceToDevice, s));
     CU_TRY(cudaStreamWaitEvent(s, ev_wd, 0));
     gemm([&] { return fbq_cuda_gemm(h_codes.as<int8_t>(), ldF, h_scales.as<float>(), FBQ_K_MAJOR,
                           wd_codes.as<int8_t>(), ldF, wd_scales.as<float>(), FBQ_K_MAJOR,
                           h_mask.as<uint32_t>(), h_res.as<int8_t>(), h_res_scales.as<float>(),
-                          tok, D, F, y, c.act_dtype, D, 0, c.epilogue, s); }, s);
+                          tok, D, F, y, c.act_dtype, D, residual ? 1 : 0, c.epilogue, s); }, s);
     (void)gTt;
   }
 
@@ -569,6 +591,58 @@ struct Mlp {
     if (!a_cs) return;
     CU_TRY(cudaStreamSynchronize(a_cs));
     CU_TRY(cudaStreamSynchronize(a_d2h));
+  }
+};
+
+// The reference's pre-norm residual GLU block (GluBlock, trainsim.hpp:136-146,
+// trainsim.cpp:294-308): out = h + down(silu(gate(norm(h))) * up(norm(h))).
+// The RmsNorm runs fused into the gate/up input quantizer (its output is never
+// materialised), the residual add rides on the down GEMM's accumulate epilogue,
+// and the backward's norm gradient and residual add are one pass
+// (fbq_cuda_rmsnorm_backward_residual).  Gain starts at 1 (trainsim.cpp:148-152).
+struct GluBlockDrv {
+  Mlp m;
+  int64_t ldn;
+  DevBuf gain, grad_gain, nctx, nctx_s, rms_ws, row_ws, term_ws, gxn;
+  GluBlockDrv(const fbq_mlp_config& cfg, const float* wg, const float* wu, const float* wd)
+      : m(cfg, wg, wu, wd) {
+    const int64_t D = m.D, T = m.T;
+    if (D % 8) throw CudaError(FBQ_ERR_UNSUPPORTED, "GluBlock needs d_model % 8 == 0");
+    ldn = ld16(D);
+    gain = DevBuf(D * 4);
+    grad_gain = DevBuf(D * 4);
+    const std::vector<float> ones((size_t)D, 1.0f);
+    CU_TRY(cudaMemcpy(gain.p, ones.data(), D * 4, cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemset(grad_gain.p, 0, D * 4));
+    nctx = DevBuf(T * ldn * 2);
+    nctx_s = DevBuf(T * cdiv(D, 128) * 4);
+    rms_ws = DevBuf(T * 4);
+    row_ws = DevBuf(2 * T * 8);
+    term_ws = DevBuf(T * D * 4);
+    gxn = DevBuf(T * D * esize(m.c.act_dtype));
+  }
+  void forward(const void* h, int64_t tok, int64_t row_off, int step, void* out, cudaStream_t s) {
+    Mlp::NormIn n{gain.as<float>(), nctx.as<int16_t>(), ldn, nctx_s.as<float>(), rms_ws.as<float>()};
+    m.forward(h, tok, row_off, step, out, s, &n, /*residual=*/true);
+    m.last_blocks[0] = cdiv(tok, 128) * m.gD;
+    m.last_blocks[1] = cdiv(tok, 128) * m.gF;
+  }
+  void backward(const void* gout, int64_t tok, int64_t row_off, int step, void* gh, cudaStream_t s) {
+    if (tok == 0) return;
+    m.backward(gout, tok, row_off, step, gxn.p, s);  // grad of the norm output (trainsim.cpp:303-306)
+    FBQ_TRY(fbq_cuda_rmsnorm_backward_residual(nctx.as<int16_t>(), ldn, nctx_s.as<float>(), gxn.p,
+                                               m.c.act_dtype, tok, m.D, m.D, gain.as<float>(), gout, m.D, gh,
+                                               m.D, grad_gain.as<float>(), row_ws.as<double>(),
+                                               term_ws.as<float>(), s));
+    m.launches += 3;
+  }
+  void zero_grad(cudaStream_t s) {
+    m.zero_grad(s);
+    CU_TRY(cudaMemsetAsync(grad_gain.p, 0, m.D * 4, s));
+  }
+  void apply_sgd(double lr, cudaStream_t s) {
+    m.apply_sgd(lr, s);
+    FBQ_TRY(fbq_cuda_sgd_update(gain.as<float>(), grad_gain.as<float>(), m.D, lr, s));  // RmsNorm::apply_sgd
   }
 };
 
@@ -877,6 +951,52 @@ int fbq_mlp_get_grads(void* m, float* g_gate, float* g_up, float* g_down) {
     if (g_gate) CU_TRY(cudaMemcpy(g_gate, mlp->g_gu.p, n, cudaMemcpyDeviceToHost));
     if (g_up) CU_TRY(cudaMemcpy(g_up, mlp->g_gu.as<float>() + mlp->F * mlp->D, n, cudaMemcpyDeviceToHost));
     if (g_down) CU_TRY(cudaMemcpy(g_down, mlp->g_d.p, n, cudaMemcpyDeviceToHost));
+  });
+}
+
+void* fbq_glublock_create(const fbq_mlp_config* cfg, const float* w_gate, const float* w_up,
+                          const float* w_down) {
+  if (!cfg || !w_gate || !w_up || !w_down) return nullptr;
+  try {
+    return new GluBlockDrv(*cfg, w_gate, w_up, w_down);
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return nullptr;
+  }
+}
+void fbq_glublock_destroy(void* b) { delete static_cast<GluBlockDrv*>(b); }
+void* fbq_glublock_mlp(void* b) { return b ? &static_cast<GluBlockDrv*>(b)->m : nullptr; }
+int fbq_glublock_forward_device(void* b, const void* h, int64_t tokens, int64_t row_offset, int step,
+                                void* out, fbq_stream_t stream) {
+  if (!b || (tokens > 0 && (!h || !out)) || row_offset < 0) return FBQ_ERR_ARG;
+  if (h == out && tokens > 0) return FBQ_ERR_ARG;  // out is written before the input is consumed
+  return guarded([&] {
+    static_cast<GluBlockDrv*>(b)->forward(h, tokens, row_offset, step, out, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int fbq_glublock_backward_device(void* b, const void* grad_out, int64_t tokens, int64_t row_offset, int step,
+                                 void* grad_h, fbq_stream_t stream) {
+  if (!b || (tokens > 0 && (!grad_out || !grad_h)) || row_offset < 0) return FBQ_ERR_ARG;
+  return guarded([&] {
+    static_cast<GluBlockDrv*>(b)->backward(grad_out, tokens, row_offset, step, grad_h,
+                                           reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int fbq_glublock_zero_grad(void* b, fbq_stream_t stream) {
+  if (!b) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<GluBlockDrv*>(b)->zero_grad(reinterpret_cast<cudaStream_t>(stream)); });
+}
+int fbq_glublock_apply_sgd(void* b, double lr, fbq_stream_t stream) {
+  if (!b) return FBQ_ERR_ARG;
+  return guarded([&] { static_cast<GluBlockDrv*>(b)->apply_sgd(lr, reinterpret_cast<cudaStream_t>(stream)); });
+}
+int fbq_glublock_get_gain(void* b, float* gain, float* grad_gain) {
+  if (!b) return FBQ_ERR_ARG;
+  return guarded([&] {
+    auto* g = static_cast<GluBlockDrv*>(b);
+    CU_TRY(cudaDeviceSynchronize());
+    if (gain) CU_TRY(cudaMemcpy(gain, g->gain.p, g->m.D * 4, cudaMemcpyDeviceToHost));
+    if (grad_gain) CU_TRY(cudaMemcpy(grad_gain, g->grad_gain.p, g->m.D * 4, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -1583,8 +1583,9 @@ __global__ void fbq_rms_apply_bwd_kernel(const int16_t* __restrict__ ctx, int64_
                                          const float* __restrict__ ctx_scales, const T* __restrict__ gy,
                                          int64_t ldgy, int64_t rows, int64_t cols,
                                          const float* __restrict__ gain, const double* __restrict__ inv,
-                                         const double* __restrict__ corr, T* __restrict__ gx,
-                                         int64_t ldgx, float* __restrict__ term) {
+                                         const double* __restrict__ corr, T* gx,
+                                         int64_t ldgx, float* __restrict__ term,
+                                         const T* res, int64_t ldres) {  // res may alias gx
   const int64_t gcols = (cols + kBlock - 1) / kBlock;
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1593,7 +1594,9 @@ __global__ void fbq_rms_apply_bwd_kernel(const int16_t* __restrict__ ctx, int64_
     const float x = __fmul_rn((float)ctx[r * ld_ctx + c], ctx_scales[r * gcols + c / kBlock]);
     const float dy = to_f32(gy[r * ldgy + c]);
     const double h = __dmul_rn((double)gain[c], (double)dy);
-    const float o = __double2float_rn(__dsub_rn(__dmul_rn(h, inv[r]), __dmul_rn((double)x, corr[r])));
+    float o = __double2float_rn(__dsub_rn(__dmul_rn(h, inv[r]), __dmul_rn((double)x, corr[r])));
+    // GluBlock's residual: add(norm.backward(grad_xn), grad_out) (trainsim.cpp:303-307)
+    if (res) o = __fadd_rn(o, to_f32(res[r * ldres + c]));
     if constexpr (sizeof(T) == 2) gx[r * ldgx + c] = __float2bfloat16_rn(o);
     else gx[r * ldgx + c] = o;
     term[i] = __double2float_rn(__dmul_rn((double)__fmul_rn(dy, x), inv[r]));
@@ -1690,7 +1693,8 @@ cudaError_t launch_rmsnorm_forward(const void* x, bool bf16, int64_t rows, int64
 cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales,
                                     const void* gy, bool bf16, int64_t rows, int64_t cols,
                                     int64_t ldgy, const float* gain, void* gx, int64_t ldgx,
-                                    float* grad_gain, double* row_ws, float* term, cudaStream_t s) {
+                                    float* grad_gain, double* row_ws, float* term, cudaStream_t s,
+                                    const void* res, int64_t ldres) {
   const unsigned rb = (unsigned)((rows + 31) / 32);  // one warp per 32 rows
   const size_t sm16 = (size_t)kRsBwdStages * RsBwdLayout<__nv_bfloat16>::kStage;
   const size_t sm32 = (size_t)kRsBwdStages * RsBwdLayout<float>::kStage;
@@ -1707,14 +1711,14 @@ cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const fl
                                                                       rows, cols, gain, inv, corr);
     fbq_rms_apply_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
         ctx, ld_ctx, ctx_scales, g, ldgy, rows, cols, gain, inv, corr,
-        reinterpret_cast<__nv_bfloat16*>(gx), ldgx, term);
+        reinterpret_cast<__nv_bfloat16*>(gx), ldgx, term, reinterpret_cast<const __nv_bfloat16*>(res), ldres);
   } else {
     auto g = reinterpret_cast<const float*>(gy);
     fbq_rms_rowstat_bwd_kernel<float><<<rb, 32, sm32, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows,
                                                               cols, gain, inv, corr);
     fbq_rms_apply_bwd_kernel<float><<<blocks, 256, 0, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy, rows, cols,
                                                            gain, inv, corr, reinterpret_cast<float*>(gx),
-                                                           ldgx, term);
+                                                           ldgx, term, reinterpret_cast<const float*>(res), ldres);
   }
   fbq_rms_grad_gain_kernel<<<(unsigned)((cols + 31) / 32), 32, 0, s>>>(term, rows, cols, grad_gain);
   return cudaGetLastError();

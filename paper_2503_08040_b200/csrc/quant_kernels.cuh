@@ -88,7 +88,8 @@ cudaError_t launch_rmsnorm_quantize(const QuantParams& p, bool bf16, const float
 cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales,
                                     const void* gy, bool bf16, int64_t rows, int64_t cols,
                                     int64_t ldgy, const float* gain, void* gx, int64_t ldgx,
-                                    float* grad_gain, double* row_ws, float* term, cudaStream_t s);
+                                    float* grad_gain, double* row_ws, float* term, cudaStream_t s,
+                                    const void* res = nullptr, int64_t ldres = 0);
 // mask_topk (policy.cpp:56-71) on device: exactly k blocks (policy_kernels.cu)
 cudaError_t launch_topk(const float* scores, int64_t n, int64_t k, uint32_t* mask_bits,
                         int32_t* count, cudaStream_t s);  // 1 = one-block-per-CTA K1 (diagnostics, fbq_debug_set_quant_diag)

@@ -58,6 +58,16 @@ _sigs = {
     "fbq_mlp_apply_sgd": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
     "fbq_mlp_get_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fbq_mlp_set_sgd_lr": (C.c_int, [C.c_void_p, C.c_double]),
+    "fbq_glublock_create": (C.c_void_p, [C.POINTER(MlpConfig), _F32P, _F32P, _F32P]),
+    "fbq_glublock_destroy": (None, [C.c_void_p]),
+    "fbq_glublock_mlp": (C.c_void_p, [C.c_void_p]),
+    "fbq_glublock_forward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                              C.c_void_p, C.c_void_p]),
+    "fbq_glublock_backward_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                               C.c_void_p, C.c_void_p]),
+    "fbq_glublock_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fbq_glublock_apply_sgd": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
+    "fbq_glublock_get_gain": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 for _n, (_r, _a) in _sigs.items():
     _f = getattr(lib, _n)
@@ -158,6 +168,9 @@ class GluMlp:
         self.cfg = cfg
         self.act_dtype = act_dtype
         self.max_tokens = max_tokens
+        self._create(cfg, wg, wu, wd)
+
+    def _create(self, cfg, wg, wu, wd):
         h = lib.fbq_mlp_create(C.byref(cfg), wg, wu, wd)
         if not h:
             raise K.FbqError(K.FBQ_ERR_ARG, f"fbq_mlp_create ({lib.fbq_host_last_error().decode()})")
@@ -299,6 +312,66 @@ class GluMlp:
         t = (C.c_double * 2)()
         _check(lib.fbq_mlp_get_controller(self._h, r, t), "get_controller")
         return list(r), list(t)
+
+
+class GluBlock(GluMlp):
+    """The reference's pre-norm residual GLU block (GluBlock, trainsim.hpp:136-146,
+    trainsim.cpp:294-308): out = h + down(silu(gate(norm(h))) * up(norm(h))), with
+    the RmsNorm (gain 1 at start) fused into the gate/up input quantizer and the
+    residual adds fused into the down GEMM / the norm backward
+    (include/fbq_b200_host.h, fbq_glublock_*).  Every GluMlp method that reads or
+    steers the linears (controller_step, grads_host, weights_host,
+    controller_state, set_thresholds, wait_grad, ...) acts on the block's
+    gate/up/down driver."""
+
+    def _create(self, cfg, wg, wu, wd):
+        b = lib.fbq_glublock_create(C.byref(cfg), wg, wu, wd)
+        if not b:
+            raise K.FbqError(K.FBQ_ERR_ARG, f"fbq_glublock_create ({lib.fbq_host_last_error().decode()})")
+        self._b = b
+        self._h = lib.fbq_glublock_mlp(b)  # owned by the block
+
+    def __del__(self):
+        b = getattr(self, "_b", None)
+        if b and lib is not None:
+            lib.fbq_glublock_destroy(b)
+            self._b = self._h = None
+
+    def forward(self, h: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        _check_act(h, self.act_dtype, self.d_model, "GluBlock.forward h")
+        _check_out(out, h.shape[0], self.d_model, self.act_dtype, "GluBlock.forward")
+        h = h.contiguous()
+        y = out if out is not None else torch.empty_like(h)
+        _check(lib.fbq_glublock_forward_device(self._b, h.data_ptr(), h.shape[0], row_offset, step,
+                                               y.data_ptr(), _stream()), "GluBlock forward")
+        return y
+
+    def backward(self, grad_out: torch.Tensor, step: int, row_offset: int = 0, out=None):
+        _check_act(grad_out, self.act_dtype, self.d_model, "GluBlock.backward grad_out")
+        _check_out(out, grad_out.shape[0], self.d_model, self.act_dtype, "GluBlock.backward")
+        grad_out = grad_out.contiguous()
+        gh = out if out is not None else torch.empty_like(grad_out)
+        _check(lib.fbq_glublock_backward_device(self._b, grad_out.data_ptr(), grad_out.shape[0], row_offset,
+                                                step, gh.data_ptr(), _stream()), "GluBlock backward")
+        return gh
+
+    def zero_grad(self):
+        _check(lib.fbq_glublock_zero_grad(self._b, _stream()), "GluBlock zero_grad")
+
+    def apply_sgd(self, lr: float):
+        _check(lib.fbq_glublock_apply_sgd(self._b, lr, _stream()), "GluBlock apply_sgd")
+
+    def gain_host(self):
+        """(gain, grad_gain) of the block's RmsNorm, host fp32 (synchronous)."""
+        g = np.empty(self.d_model, np.float32)
+        gg = np.empty(self.d_model, np.float32)
+        _check(lib.fbq_glublock_get_gain(self._b, g.ctypes.data, gg.ctypes.data), "GluBlock get_gain")
+        return g, gg
+
+    def step_host(self, *a, **k):  # the host-buffer step APIs belong to the bare MLP driver
+        raise NotImplementedError("GluBlock: use the device API")
+
+    step_host_async = step_host
 
 
 class QuantLinear:
