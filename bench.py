@@ -942,6 +942,41 @@ def train_step_rate(device, T=TOKENS, steps=10, warmup=3, lr=1e-6):
             "fwd_bwd_same_run_ms": ms_fb, "sgd_cost_ms": ms_sgd - ms_fb}
 
 
+def glu_block_rate(device, T=TOKENS, steps=10, warmup=3):
+    """The reference's pre-norm residual GLU block (GluBlock, trainsim.cpp:294-308)
+    at the C3 dims: RmsNorm + gate/up + GluCombine + down + residual, fwd+bwd
+    (zero_grad, controller), the headline's bf16 / FMA / packed-context setup; next
+    to the bare MLP in the same run (the norm is fused into the gate/up input
+    quantizer, the residual adds into the down GEMM and the norm backward)."""
+    import torch
+    from paper_2503_08040_b200 import linear
+    wg, wu, wd = make_weights()
+    x = make_activations(T, D_MODEL, 1000, device, torch.bfloat16)
+    gy = make_grads(T, D_MODEL, 2000, device, torch.bfloat16)
+    th = mlp_thresholds(x, wg, wu, device, pooled=False)  # rank 0 only: no collective
+    out = {}
+    for name, cls in (("mlp", linear.GluMlp), ("glu_block", linear.GluBlock)):
+        m = cls(wg, wu, wd, T, ctx_packed=CTX_PACKED)
+        m.set_thresholds(*th)
+        y, gx = torch.empty_like(x), torch.empty_like(x)
+        i = [0]
+
+        def step():
+            m.zero_grad()
+            m.forward(x, i[0], out=y)
+            m.backward(gy, i[0], out=gx)
+            m.controller_step()
+            i[0] += 1
+        ms = _event_time(step, steps, warmup)
+        out[name] = {"tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms}
+        del m
+    torch.cuda.empty_cache()
+    out["workload"] = ("GluBlock (RmsNorm + SwiGLU MLP + residual, trainsim.cpp:294-308) fwd+bwd at the C3 dims, "
+                       "8192 tokens, bf16 / FMA, next to the bare MLP in the same run")
+    out["norm_and_residual_cost_ms"] = out["glu_block"]["ms_per_step"] - out["mlp"]["ms_per_step"]
+    return out
+
+
 def context_memory(device, T=TOKENS, steps=10, warmup=3):
     """Activation contexts saved for the backward vs BF16 (PAPER.md:55, 527, 535:
     62 %), for both storages of the 10-bit GluCombine contexts, and the step
@@ -1160,7 +1195,7 @@ def run_ours(args, rank, world, local):
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
 
-        comparator = exact = ctxmem = train = None
+        comparator = exact = ctxmem = train = block = None
         if not args.no_sweep:
             try:
                 comparator = bf16_mlp_comparator(device, T)
@@ -1179,6 +1214,10 @@ def run_ours(args, rank, world, local):
                 train = train_step_rate(device, T)
             except Exception as ex:  # pragma: no cover
                 train = {"error": str(ex)[:200]}
+            try:
+                block = glu_block_rate(device, T)
+            except Exception as ex:  # pragma: no cover
+                block = {"error": str(ex)[:200]}
         sweep = qsweep = c4 = rms = None
         if not args.no_sweep and world == 1:
             try:  # first: the issue-bound quantizer is clock-sensitive (power cap after GEMMs)
@@ -1256,6 +1295,7 @@ def run_ours(args, rank, world, local):
             "bf16_mlp_comparator": comparator,
             "exact_mode": exact,
             "train_step": train,
+            "glu_block": block,
             "context_memory": ctxmem,
             "gemm_sweep": sweep,
             "quant_sweep": qsweep,
