@@ -1509,6 +1509,8 @@ fbq_rms_rowstat_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
                            double* __restrict__ inv_out, double* __restrict__ corr_out) {
   using L = RsBwdLayout<T>;
   extern __shared__ __align__(16) uint8_t rsm[];
+  __shared__ double gd[kRsCols];
+  static_assert(kRsCols == 128, "4 gains per lane");
   const int lane = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int64_t gcols = (cols + kBlock - 1) / kBlock;
@@ -1541,7 +1543,16 @@ fbq_rms_rowstat_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
     const uint8_t* crow = st + L::kCodes + lane * L::RSC;
     const uint8_t* drow = st + L::kDy + lane * L::RSD;
     const float sc = *reinterpret_cast<const float*>(st + L::kScale + lane * 4);
-    const float* gv = reinterpret_cast<const float*>(st + L::kGain);
+    // the chunk's gains widened to double once per chunk (4 per lane) instead of
+    // once per element: the F2F.F64.F32 pipe is what paces this kernel
+    {
+      const float4 g4 = *reinterpret_cast<const float4*>(st + L::kGain + lane * 16);
+      gd[lane * 4 + 0] = (double)g4.x;
+      gd[lane * 4 + 1] = (double)g4.y;
+      gd[lane * 4 + 2] = (double)g4.z;
+      gd[lane * 4 + 3] = (double)g4.w;
+    }
+    __syncwarp();
 #pragma unroll 2
     for (int pc = 0; pc < kRsCols / 8; ++pc) {  // 8 columns per step
       const uint4 cw4 = *reinterpret_cast<const uint4*>(crow + pc * 16);
@@ -1561,7 +1572,7 @@ fbq_rms_rowstat_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
         const int code = (int)(int16_t)(cw[e >> 1] >> (16 * (e & 1)));
         const double v = (double)__fmul_rn((float)code, sc);  // dequantize: fl(code * scale)
         ss = __fma_rn(v, v, ss);                               // zero-filled columns add nothing
-        const double h = __dmul_rn((double)gv[pc * 8 + e], (double)dy[e]);
+        const double h = __dmul_rn(gd[pc * 8 + e], (double)dy[e]);
         dot = __dadd_rn(dot, __dmul_rn(h, v));
       }
     }
@@ -1579,27 +1590,38 @@ fbq_rms_rowstat_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
 // gx = float(h * inv - x * corr), h = g * dy (double); and the per-element
 // grad_gain term float(float(dy * x) * inv) into `term` (trainsim.cpp:200-205)
 template <typename T>
-__global__ void fbq_rms_apply_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
-                                         const float* __restrict__ ctx_scales, const T* __restrict__ gy,
-                                         int64_t ldgy, int64_t rows, int64_t cols,
-                                         const float* __restrict__ gain, const double* __restrict__ inv,
-                                         const double* __restrict__ corr, T* gx,
-                                         int64_t ldgx, float* __restrict__ term,
-                                         const T* res, int64_t ldres) {  // res may alias gx
-  const int64_t gcols = (cols + kBlock - 1) / kBlock;
-  const int64_t n = rows * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cols, c = i % cols;
-    const float x = __fmul_rn((float)ctx[r * ld_ctx + c], ctx_scales[r * gcols + c / kBlock]);
-    const float dy = to_f32(gy[r * ldgy + c]);
-    const double h = __dmul_rn((double)gain[c], (double)dy);
-    float o = __double2float_rn(__dsub_rn(__dmul_rn(h, inv[r]), __dmul_rn((double)x, corr[r])));
-    // GluBlock's residual: add(norm.backward(grad_xn), grad_out) (trainsim.cpp:303-307)
-    if (res) o = __fadd_rn(o, to_f32(res[r * ldres + c]));
-    if constexpr (sizeof(T) == 2) gx[r * ldgx + c] = __float2bfloat16_rn(o);
-    else gx[r * ldgx + c] = o;
-    term[i] = __double2float_rn(__dmul_rn((double)__fmul_rn(dy, x), inv[r]));
+__global__ void __launch_bounds__(256)
+fbq_rms_apply_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx,
+                         const float* __restrict__ ctx_scales, const T* __restrict__ gy,
+                         int64_t ldgy, int64_t rows, int64_t cols,
+                         const float* __restrict__ gain, const double* __restrict__ inv,
+                         const double* __restrict__ corr, T* gx,
+                         int64_t ldgx, float* __restrict__ term,
+                         const T* res, int64_t ldres) {  // res may alias gx
+  // a thread owns columns (c, c + 1) and walks rows blockIdx.y, + gridDim.y, ...:
+  // no per-element index division, the two gains widened to double once
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= cols) return;
+  const bool two = c + 1 < cols;
+  const int64_t gcols = (cols + kBlock - 1) / kBlock, cb = c / kBlock;
+  const double g0 = (double)gain[c], g1 = two ? (double)gain[c + 1] : 0.0;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const float sc = ctx_scales[r * gcols + cb];
+    const double iv = inv[r], co = corr[r];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (e == 1 && !two) break;
+      const int64_t cc = c + e;
+      const float x = __fmul_rn((float)ctx[r * ld_ctx + cc], sc);
+      const float dy = to_f32(gy[r * ldgy + cc]);
+      const double h = __dmul_rn(e ? g1 : g0, (double)dy);
+      float o = __double2float_rn(__dsub_rn(__dmul_rn(h, iv), __dmul_rn((double)x, co)));
+      // GluBlock's residual: add(norm.backward(grad_xn), grad_out) (trainsim.cpp:303-307)
+      if (res) o = __fadd_rn(o, to_f32(res[r * ldres + cc]));
+      if constexpr (sizeof(T) == 2) gx[r * ldgx + cc] = __float2bfloat16_rn(o);
+      else gx[r * ldgx + cc] = o;
+      term[r * cols + cc] = __double2float_rn(__dmul_rn((double)__fmul_rn(dy, x), iv));
+    }
   }
 }
 
@@ -1702,9 +1724,12 @@ cudaError_t launch_rmsnorm_backward(const int16_t* ctx, int64_t ld_ctx, const fl
   if (cudaError_t e = smem_once<fbq_rms_rowstat_bwd_kernel<float>>(sm32)) return e;
   double* inv = row_ws;
   double* corr = row_ws + rows;
-  const int64_t n = rows * cols;
-  int blocks = (n + 255) / 256 < 148 * 16 ? (int)((n + 255) / 256) : 148 * 16;
-  if (blocks < 1) blocks = 1;
+  // apply: 256 threads x 2 columns across, rows strided over grid.y (~16 CTAs per SM)
+  const unsigned gxd = (unsigned)((cols + 511) / 512);
+  int64_t gyd = (148 * 16 + gxd - 1) / gxd;
+  if (gyd > rows) gyd = rows;
+  if (gyd > 65535) gyd = 65535;
+  const dim3 blocks(gxd, (unsigned)(gyd < 1 ? 1 : gyd));
   if (bf16) {
     auto g = reinterpret_cast<const __nv_bfloat16*>(gy);
     fbq_rms_rowstat_bwd_kernel<__nv_bfloat16><<<rb, 32, sm16, s>>>(ctx, ld_ctx, ctx_scales, g, ldgy,
