@@ -1638,13 +1638,21 @@ fbq_rms_grad_gain_kernel(const float* __restrict__ term, int64_t rows, int64_t c
   const int64_t c0 = (int64_t)blockIdx.x * 32, c = c0 + lane;
   const bool cok = c < cols;
   const int64_t nch = (rows + kGgRows - 1) / kGgRows;
+  // kGgRows rows x 128 B = 8 pieces per row (cols % 8 == 0 keeps pieces whole):
+  // lane copies piece (lane & 7) of rows (lane >> 3) + 4 k -- its column offset
+  // is fixed, so a piece costs one address add (the per-piece index arithmetic
+  // was most of this latency-bound kernel's instructions)
+  const int pcl = lane & 7, rrl = lane >> 3;
+  const bool pc_ok = c0 + pcl * 4 < cols;
+  const float* lane_base = term + (int64_t)rrl * cols + c0 + pcl * 4;
+  const int64_t step4 = 4 * cols;
   auto fill = [&](int sidx, int64_t ch) {
-    // kGgRows rows x 128 B = 8 pieces per row; cols % 8 == 0 keeps pieces whole
-    for (int i = lane; i < kGgRows * 8; i += 32) {
-      const int rr = i >> 3, pc = i & 7;
-      const int64_t r = ch * kGgRows + rr, col = c0 + pc * 4;
-      const bool ok = r < rows && col < cols;
-      cp_async16(&st[sidx][rr][pc * 4], term + (ok ? r * cols + col : 0), ok);
+    const float* src = lane_base + ch * kGgRows * cols;
+    const int64_t rlim = rows - ch * kGgRows - rrl;  // rows left for this lane's first piece
+#pragma unroll
+    for (int k = 0; k < kGgRows / 4; ++k, src += step4) {
+      const bool ok = pc_ok && 4 * k < rlim;
+      cp_async16(&st[sidx][rrl + 4 * k][pcl * 4], ok ? src : term, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
