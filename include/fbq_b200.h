@@ -135,6 +135,19 @@ int fbq_cuda_rmsnorm_backward_residual(const int16_t* ctx_codes, int64_t ld_ctx,
                                        int64_t ldgx, float* grad_gain, double* row_ws, float* term_ws,
                                        fbq_stream_t stream);
 
+/* SiluLayer (trainsim.hpp:118-131, trainsim.cpp:265-290).  forward: y = silu(x)
+ * and the input's ctx_bits (10) 1 x 128 RTN context (int16 codes rows x ld_ctx,
+ * scales rows x ceil(cols/128)); backward: gx = fl(gy * silu'(dequantize(ctx))).
+ * exact_math: the reference's double silu / silu' (silu_scalar,
+ * silu_grad_scalar, trainsim.cpp:37-46), bit-exact; 0: fp32 MUFU forms (a few
+ * ulp).  Layout rules as RmsNorm (cols % 8 == 0, 16-byte aligned rows). */
+int fbq_cuda_silu_forward(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx, void* y,
+                          int64_t ldy, int16_t* ctx_codes, int64_t ld_ctx, float* ctx_scales, int ctx_bits,
+                          int exact_math, fbq_stream_t stream);
+int fbq_cuda_silu_backward(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales, const void* gy,
+                           int dtype, int64_t rows, int64_t cols, int64_t ldgy, void* gx, int64_t ldgx,
+                           int exact_math, fbq_stream_t stream);
+
 /* mask_topk -- policy.cpp:56-71 / policy.hpp:30-31: exactly k = ceil(rate * n)
  * (clamped to n) blocks with the largest scores, ties toward the lower block
  * index, written as a bitmap (bit b = block b; the whole bitmap is rewritten).

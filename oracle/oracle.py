@@ -575,6 +575,43 @@ class RefGluBlock:
             self.h = None
 
 
+class RefSilu:
+    """The reference's own SiluLayer (trainsim.cpp:265-290) through oracle/_ref."""
+
+    def __init__(self):
+        r = REF_oracle()
+        if r is None:
+            raise FileNotFoundError("oracle/_ref not built")
+        lib = r._l.lib
+        self.lib = lib
+        lib.ref_silu_create.restype = C.c_void_p
+        lib.ref_silu_create.argtypes = []
+        lib.ref_silu_destroy.argtypes = [C.c_void_p]
+        lib.ref_silu_forward.argtypes = [C.c_void_p, F32, i64, i64, F32]
+        lib.ref_silu_backward.argtypes = [C.c_void_p, F32, i64, i64, F32]
+        self.h = lib.ref_silu_create()
+        self._err = r._err
+
+    def forward(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.zeros_like(x)
+        if self.lib.ref_silu_forward(self.h, x, x.shape[0], x.shape[1], y):
+            raise RuntimeError(self._err().decode())
+        return y
+
+    def backward(self, gy):
+        gy = np.ascontiguousarray(gy, np.float32)
+        gx = np.zeros_like(gy)
+        if self.lib.ref_silu_backward(self.h, gy, gy.shape[0], gy.shape[1], gx):
+            raise RuntimeError(self._err().decode())
+        return gx
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_silu_destroy(self.h)
+            self.h = None
+
+
 class RefRmsNorm:
     """The reference's own RmsNorm (trainsim.cpp:145-219) through oracle/_ref."""
 

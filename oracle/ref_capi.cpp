@@ -593,4 +593,34 @@ int ref_block_state(void* h, float* gain, float* grad_gain, float* wg, float* wu
     });
 }
 
+// ---------------------------------------------------------------------------
+// SiluLayer (trainsim.hpp:118-131, trainsim.cpp:265-290)
+struct RefSilu {
+    QuantConfig cfg;
+    std::unique_ptr<SiluLayer> l;
+};
+void* ref_silu_create() {
+    try {
+        auto* r = new RefSilu;
+        r->l = std::make_unique<SiluLayer>(r->cfg);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_silu_destroy(void* h) { delete static_cast<RefSilu*>(h); }
+int ref_silu_forward(void* h, const float* x, int64_t rows, int64_t cols, float* y) {
+    return guarded([&] {
+        const DenseMatrix out = static_cast<RefSilu*>(h)->l->forward(make_dense(x, rows, cols));
+        std::memcpy(y, out.data(), out.size() * sizeof(float));
+    });
+}
+int ref_silu_backward(void* h, const float* gy, int64_t rows, int64_t cols, float* gx) {
+    return guarded([&] {
+        const DenseMatrix out = static_cast<RefSilu*>(h)->l->backward(make_dense(gy, rows, cols));
+        std::memcpy(gx, out.data(), out.size() * sizeof(float));
+    });
+}
+
 } // extern "C"

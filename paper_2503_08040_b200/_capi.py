@@ -44,6 +44,10 @@ _SIGS = {
                                           vp, vp, vp, vp, u64, i64, vp]),
     "fbq_cuda_quantize_rtn": (cint, [vp, cint, i64, i64, i64, vp, i64, vp, vp]),
     "fbq_cuda_sgd_update": (cint, [vp, vp, i64, dbl, vp]),
+    "fbq_cuda_silu_forward": (cint, [vp, cint, i64, i64, i64, vp, i64, vp, i64, vp, cint, cint, vp]),
+    "fbq_cuda_silu_backward": (cint, [vp, i64, vp, vp, cint, i64, i64, i64, vp, i64, cint, vp]),
+    "fbq_cuda_rmsnorm_backward_residual": (cint, [vp, i64, vp, vp, cint, i64, i64, i64, vp, vp, i64, vp, i64,
+                                                  vp, vp, vp, vp]),
     "fbq_cuda_sgd_quantize_rtn": (cint, [vp, vp, i64, i64, dbl, vp, i64, vp, vp]),
     "fbq_cuda_quantize_stochastic": (cint, [vp, cint, i64, i64, i64, u64, i64, vp, i64, vp, vp]),
     "fbq_cuda_gemm": (cint, [vp, i64, vp, cint, vp, i64, vp, cint, vp, vp, vp, i64, i64, i64, vp,

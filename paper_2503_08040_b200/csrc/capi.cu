@@ -315,6 +315,35 @@ int fbq_cuda_rmsnorm_backward_residual(const int16_t* ctx_codes, int64_t ld_ctx,
                                                   residual, ld_res));
 }
 
+int fbq_cuda_silu_forward(const void* x, int dtype, int64_t rows, int64_t cols, int64_t ldx, void* y,
+                          int64_t ldy, int16_t* ctx_codes, int64_t ld_ctx, float* ctx_scales, int ctx_bits,
+                          int exact_math, fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!x || !y || !ctx_codes || !ctx_scales || ldx < cols || ldy < cols || ld_ctx < cols) return FBQ_ERR_ARG;
+  if (ctx_bits < 2 || ctx_bits > 16) return FBQ_ERR_UNSUPPORTED;
+  const size_t esz = dtype == FBQ_F32 ? 4 : 2;
+  if (!rms_layout_ok(cols, ldx, x, esz) || !rms_layout_ok(cols, ldy, y, esz) ||
+      !rms_layout_ok(cols, ld_ctx, ctx_codes, 2) || cdiv(rows, 128) > 65535)
+    return FBQ_ERR_UNSUPPORTED;
+  return cuda_status(fbq::launch_silu_forward(x, dtype == FBQ_BF16, rows, cols, ldx, y, ldy, ctx_codes, ld_ctx,
+                                              ctx_scales, (float)((1 << (ctx_bits - 1)) - 1), exact_math != 0,
+                                              reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fbq_cuda_silu_backward(const int16_t* ctx_codes, int64_t ld_ctx, const float* ctx_scales, const void* gy,
+                           int dtype, int64_t rows, int64_t cols, int64_t ldgy, void* gx, int64_t ldgx,
+                           int exact_math, fbq_stream_t stream) {
+  if (dtype != FBQ_F32 && dtype != FBQ_BF16) return FBQ_ERR_ARG;
+  if (rows < 0 || cols < 0) return FBQ_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return FBQ_OK;
+  if (!ctx_codes || !ctx_scales || !gy || !gx || ldgy < cols || ldgx < cols || ld_ctx < cols) return FBQ_ERR_ARG;
+  return cuda_status(fbq::launch_silu_backward(ctx_codes, ld_ctx, ctx_scales, gy, dtype == FBQ_BF16, rows, cols,
+                                               ldgy, gx, ldgx, exact_math != 0,
+                                               reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int fbq_cuda_mask_topk(const float* scores, int64_t n, double rate, uint32_t* mask_bits,
                        int32_t* masked_count, fbq_stream_t stream) {
   if (!(rate >= 0.0 && rate <= 1.0)) return FBQ_ERR_ARG;  // policy.cpp:57

@@ -1132,6 +1132,74 @@ fbq_glu_forward_kernel(GluParams g, QuantParams p) {
   }
 }
 
+// SiluLayer (trainsim.hpp:118-131, trainsim.cpp:265-290): y = silu(x), the
+// input kept as its 10-bit 1 x 128 RTN context (int16 codes, like RmsNorm's);
+// backward gx = fl(gy * silu'(dequantize(ctx))).  exact: the reference's double
+// silu / silu' (silu_ref / silu_grad_ref); else the fp32 MUFU forms of the GLU
+// fast path.  One 128 x 128 tile per CTA, K1's 1 x 128 row groups.
+template <typename T, bool kExact>
+__global__ void __launch_bounds__(kQuantThreads)
+fbq_silu_fwd_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, T* __restrict__ y,
+                    int64_t ldy, int16_t* __restrict__ ctx, int64_t ld_ctx, float* __restrict__ ctx_scales,
+                    float level) {
+  using Tl = Tiling<T>;
+  constexpr int V = Tl::V, VPR = Tl::VPR, RPP = Tl::RPP, NP = Tl::NP;
+  const int64_t bj = blockIdx.x, bi = blockIdx.y;
+  const int64_t gcols = (cols + kBlock - 1) / kBlock;
+  const int lc = (threadIdx.x % VPR) * V, lr = threadIdx.x / VPR;
+  const int64_t cc = bj * kBlock + lc;
+  const bool col_ok = cc < cols;  // cols % V == 0
+#pragma unroll 1
+  for (int ps = 0; ps < NP; ++ps) {
+    const int64_t r = bi * kBlock + lr + ps * RPP;
+    if (r >= rows) break;  // row-uniform across the VPR threads of the group
+    float v[V];
+    if (col_ok) {
+      load_vec<T, V>(x + r * ldx + cc, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = 0.0f;
+    }
+    uint32_t code[V];
+    const float s = group_rtn<V, VPR>(v, code, level);
+    if (!col_ok) continue;
+    store_codes16<V>(ctx + r * ld_ctx + cc, code);
+    if (lc == 0) ctx_scales[r * gcols + bj] = s;
+    T out[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float o = kExact ? silu_ref(v[i]) : silu_fast(v[i]);
+      if constexpr (sizeof(T) == 2) out[i] = __float2bfloat16_rn(o);
+      else out[i] = o;
+    }
+    *reinterpret_cast<uint4*>(y + r * ldy + cc) = *reinterpret_cast<const uint4*>(out);
+  }
+}
+
+template <typename T, bool kExact>
+__global__ void __launch_bounds__(256)
+fbq_silu_bwd_kernel(const int16_t* __restrict__ ctx, int64_t ld_ctx, const float* __restrict__ ctx_scales,
+                    const T* __restrict__ gy, int64_t ldgy, int64_t rows, int64_t cols, T* __restrict__ gx,
+                    int64_t ldgx) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= cols) return;
+  const bool two = c + 1 < cols;
+  const int64_t gcols = (cols + kBlock - 1) / kBlock, cb = c / kBlock;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const float sc = ctx_scales[r * gcols + cb];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (e == 1 && !two) break;
+      const int64_t cc = c + e;
+      const float xv = __fmul_rn((float)ctx[r * ld_ctx + cc], sc);  // dequantize: fl(code * scale)
+      const float d = kExact ? silu_grad_ref(xv) : silu_grad_fast(xv);
+      const float o = __fmul_rn(to_f32(gy[r * ldgy + cc]), d);
+      if constexpr (sizeof(T) == 2) gx[r * ldgx + cc] = __float2bfloat16_rn(o);
+      else gx[r * ldgx + cc] = o;
+    }
+  }
+}
+
 // GluCombine backward (trainsim.cpp:248-263) fused with the two dY
 // quantizers: ga = fl(fl(gy * b) * silu'(a)), gb = fl(gy * silu(a)) from the
 // staged dH and 10-bit contexts; one pass for both block absmaxes, one pass
@@ -2258,6 +2326,45 @@ cudaError_t launch_sgd_quantize(float* w, const float* g, int64_t rows, int64_t 
   p.scales = scales;
   const dim3 grid((unsigned)((cols + kBlock - 1) / kBlock), (unsigned)((rows + kBlock - 1) / kBlock));
   return launch_ex(fbq_sgd_quantize_kernel, grid, dim3(kQuantThreads), 0, s, false, p, w, g, lr);
+}
+
+cudaError_t launch_silu_forward(const void* x, bool bf16, int64_t rows, int64_t cols, int64_t ldx, void* y,
+                                int64_t ldy, int16_t* ctx, int64_t ld_ctx, float* ctx_scales, float level,
+                                bool exact, cudaStream_t s) {
+  const dim3 grid((unsigned)((cols + kBlock - 1) / kBlock), (unsigned)((rows + kBlock - 1) / kBlock));
+#define FBQ_SF(T, E) fbq_silu_fwd_kernel<T, E><<<grid, kQuantThreads, 0, s>>>(                      \
+      reinterpret_cast<const T*>(x), rows, cols, ldx, reinterpret_cast<T*>(y), ldy, ctx, ld_ctx,  \
+      ctx_scales, level)
+  if (bf16) {
+    if (exact) FBQ_SF(__nv_bfloat16, true);
+    else FBQ_SF(__nv_bfloat16, false);
+  } else {
+    if (exact) FBQ_SF(float, true);
+    else FBQ_SF(float, false);
+  }
+#undef FBQ_SF
+  return cudaGetLastError();
+}
+
+cudaError_t launch_silu_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales, const void* gy,
+                                 bool bf16, int64_t rows, int64_t cols, int64_t ldgy, void* gx, int64_t ldgx,
+                                 bool exact, cudaStream_t s) {
+  const unsigned gxd = (unsigned)((cols + 511) / 512);
+  int64_t gyd = (148 * 16 + gxd - 1) / gxd;
+  if (gyd > rows) gyd = rows;
+  if (gyd > 65535) gyd = 65535;
+  const dim3 grid(gxd, (unsigned)(gyd < 1 ? 1 : gyd));
+#define FBQ_SB(T, E) fbq_silu_bwd_kernel<T, E><<<grid, 256, 0, s>>>(                                 \
+      ctx, ld_ctx, ctx_scales, reinterpret_cast<const T*>(gy), ldgy, rows, cols, reinterpret_cast<T*>(gx), ldgx)
+  if (bf16) {
+    if (exact) FBQ_SB(__nv_bfloat16, true);
+    else FBQ_SB(__nv_bfloat16, false);
+  } else {
+    if (exact) FBQ_SB(float, true);
+    else FBQ_SB(float, false);
+  }
+#undef FBQ_SB
+  return cudaGetLastError();
 }
 
 }  // namespace fbq

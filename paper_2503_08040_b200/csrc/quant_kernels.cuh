@@ -97,6 +97,12 @@ cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
 cudaError_t launch_glu_forward(const GluParams& g, const QuantParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_glu_backward(const GluBwdParams& g, bool bf16, cudaStream_t s);
 cudaError_t launch_zero_count(int* count, cudaStream_t s);
+cudaError_t launch_silu_forward(const void* x, bool bf16, int64_t rows, int64_t cols, int64_t ldx, void* y,
+                                int64_t ldy, int16_t* ctx, int64_t ld_ctx, float* ctx_scales, float level,
+                                bool exact, cudaStream_t s);
+cudaError_t launch_silu_backward(const int16_t* ctx, int64_t ld_ctx, const float* ctx_scales, const void* gy,
+                                 bool bf16, int64_t rows, int64_t cols, int64_t ldgy, void* gx, int64_t ldgx,
+                                 bool exact, cudaStream_t s);
 cudaError_t launch_sgd_quantize(float* w, const float* g, int64_t rows, int64_t cols, double lr,
                                 int8_t* codes, int64_t ldq, float* scales, cudaStream_t s);
 cudaError_t launch_controller(double* theta, const int* masked_count, int64_t n_blocks,

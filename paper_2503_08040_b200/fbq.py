@@ -465,6 +465,46 @@ def layer_seed(base: int, layer_id: int, tag: int, step: int) -> int:
 
 
 # ------------------------------------------------------------------ RmsNorm
+class SiluLayer:
+    """SiluLayer (trainsim.hpp:118-131, trainsim.cpp:265-290) on the device: y =
+    silu(x), the input kept as its 10-bit 1 x 128 context; backward gx = gy *
+    silu'(dequantized context).  exact: the reference's double silu / silu'
+    (bit-exact); otherwise the fp32 fast forms of the GLU training path."""
+
+    def __init__(self, exact: bool = True, bits: int = 10):
+        self.exact = bool(exact)
+        self.bits = bits
+        self._ctx = None
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        x = _check_input(x)
+        r, c = x.shape
+        y = torch.empty_like(x)
+        ldc = _ld16(c)
+        codes = torch.empty((r, ldc), dtype=torch.int16, device=x.device)
+        scales = torch.empty((r, cdiv(c, BLOCK)), dtype=torch.float32, device=x.device)
+        K.call("fbq_cuda_silu_forward", x.data_ptr(), _dtype_code(x), r, c, x.stride(0), y.data_ptr(),
+               y.stride(0), codes.data_ptr(), ldc, scales.data_ptr(), self.bits, int(self.exact), _stream())
+        self._ctx = (codes, scales, r, c)
+        return y
+
+    def backward(self, gy: torch.Tensor) -> torch.Tensor:
+        if self._ctx is None:
+            raise RuntimeError("silu: backward without context")  # trainsim.cpp:280-282
+        codes, scales, r, c = self._ctx
+        gy = _check_input(gy)
+        if tuple(gy.shape) != (r, c):
+            raise ValueError("gradient shape does not match the forward input")
+        gx = torch.empty_like(gy)
+        K.call("fbq_cuda_silu_backward", codes.data_ptr(), codes.stride(0), scales.data_ptr(), gy.data_ptr(),
+               _dtype_code(gy), r, c, gy.stride(0), gx.data_ptr(), gx.stride(0), int(self.exact), _stream())
+        return gx
+
+    def context(self):
+        """(int16 codes [rows, ld], fp32 scales [rows, ceil(cols/128)]) of the last forward."""
+        return self._ctx[0], self._ctx[1]
+
+
 class RmsNorm:
     """RmsNorm (trainsim.hpp:75-97, trainsim.cpp:145-211) on the device: gain
     starts at 1, the input is kept as its 10-bit 1 x 128 context, backward

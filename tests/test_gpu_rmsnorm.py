@@ -3,7 +3,7 @@ reference's own RmsNorm (trainsim.cpp:145-219) through oracle/_ref."""
 import numpy as np
 import pytest
 
-from tests.helpers import outlier_matrix
+from tests.helpers import bf16_round, outlier_matrix
 
 pytestmark = pytest.mark.gpu
 
@@ -114,3 +114,42 @@ def test_rmsnorm_fused_input_quantizer(rows, dim, dtype, nsr, masking):
         assert torch.equal(got[2].codes[:, :dim], q2.codes[:, :dim])
     for u, v in zip(a.context(), b.context()):
         assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("rows,dim", [(256, 384), (129, 1024), (300, 200)])
+def test_silu_layer_bit_exact_vs_reference(rows, dim):
+    """SiluLayer (trainsim.cpp:265-290): y, the 10-bit 1 x 128 context and the
+    backward gx bit-identical to the reference's own layer (exact math)."""
+    import torch
+    from oracle.oracle import C_oracle, REF_oracle, RefSilu
+    from paper_2503_08040_b200 import fbq
+    if REF_oracle() is None:
+        pytest.skip("oracle/_ref not present")
+    ref = RefSilu()
+    dev = fbq.SiluLayer(exact=True)
+    x = outlier_matrix(rows, dim, seed=90, body=2.0, channels=[3], tokens=[rows // 2], mag_c=30.0, mag_t=12.0)
+    gy = outlier_matrix(rows, dim, seed=91, body=1e-2)
+    y = dev.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(y.view(np.int32), ref.forward(x).view(np.int32))
+    codes, scales = dev.context()
+    c_want, s_want = C_oracle().quantize_rtn(x, 1, 128, 10)
+    assert np.array_equal(codes.cpu().numpy()[:, :dim], c_want)
+    assert np.array_equal(scales.cpu().numpy().reshape(-1), s_want.reshape(-1))
+    gx = dev.backward(torch.from_numpy(gy).cuda()).cpu().numpy()
+    assert np.array_equal(gx.view(np.int32), ref.backward(gy).view(np.int32))
+
+
+def test_silu_layer_bf16_fast_within_tolerance():
+    """bf16 activations, fp32 fast silu: within bf16 rounding of the exact layer."""
+    import torch
+    from paper_2503_08040_b200 import fbq
+    from tests.helpers import rel_fro
+    x = bf16_round(outlier_matrix(512, 1024, seed=92, body=2.0))
+    gy = bf16_round(outlier_matrix(512, 1024, seed=93, body=1e-2))
+    ex, fa = fbq.SiluLayer(exact=True), fbq.SiluLayer(exact=False)
+    y_e = ex.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    y_f = fa.forward(torch.from_numpy(x).cuda().to(torch.bfloat16)).float().cpu().numpy()
+    assert rel_fro(y_f, y_e) < 8e-3
+    g_e = ex.backward(torch.from_numpy(gy).cuda()).cpu().numpy()
+    g_f = fa.backward(torch.from_numpy(gy).cuda().to(torch.bfloat16)).float().cpu().numpy()
+    assert rel_fro(g_f, g_e) < 8e-3
