@@ -13,4 +13,6 @@ run tests/test_gpu_mlp.py
 run tests/test_gpu_linear.py
 run tests/test_gpu_abi_contract.py
 run tests/test_gpu_sgd.py
+run tests/test_gpu_glublock.py
+run tests/test_gpu_determinism.py -k repeatable
 cat $out

@@ -13,6 +13,7 @@ run racecheck tests/test_gpu_rmsnorm.py -k "384 or 512"
 run racecheck tests/test_gpu_parity.py -k "dynamic_block_schedule"
 run racecheck tests/test_gpu_sgd.py -k "matches_update"
 run racecheck tests/test_gpu_mlp.py -k "step_bit_exact"
+run racecheck tests/test_gpu_glublock.py -k "equals_norm"
 run synccheck tests/test_gpu_rmsnorm.py -k "384 or 512"
 run synccheck tests/test_gpu_parity.py -k "dynamic_block_schedule"
 run synccheck tests/test_gpu_mlp.py -k "step_bit_exact"
