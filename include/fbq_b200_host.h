@@ -161,6 +161,9 @@ int fbq_glublock_zero_grad(void* block, fbq_stream_t stream);
 int fbq_glublock_apply_sgd(void* block, double lr, fbq_stream_t stream);
 /* synchronous host copies of the RmsNorm gain and its gradient (d_model floats) */
 int fbq_glublock_get_gain(void* block, float* gain, float* grad_gain);
+/* device pointers of the gain (which = 0) and grad_gain (1), d_model floats --
+ * data parallel: grad_gain is summed over ranks after the backward */
+float* fbq_glublock_gain_ptr(void* block, int which);
 
 /* ---- one fallback-quantized linear layer: QuantLinearLayer (trainsim.hpp:38-73,
  * trainsim.cpp:61-135) with 128 x 128 blocks, 8-bit operands, the stochastic X

@@ -990,6 +990,11 @@ int fbq_glublock_apply_sgd(void* b, double lr, fbq_stream_t stream) {
   if (!b) return FBQ_ERR_ARG;
   return guarded([&] { static_cast<GluBlockDrv*>(b)->apply_sgd(lr, reinterpret_cast<cudaStream_t>(stream)); });
 }
+float* fbq_glublock_gain_ptr(void* b, int which) {
+  if (!b || (which != 0 && which != 1)) return nullptr;
+  auto* g = static_cast<GluBlockDrv*>(b);
+  return which == 0 ? g->gain.as<float>() : g->grad_gain.as<float>();
+}
 int fbq_glublock_get_gain(void* b, float* gain, float* grad_gain) {
   if (!b) return FBQ_ERR_ARG;
   return guarded([&] {

@@ -60,6 +60,17 @@ def allreduce_mlp_grads_overlapped(mlp, gu_grad, d_grad, comm_stream, group=None
         w.wait()
 
 
+def allreduce_block_grads_overlapped(block, gu_grad, d_grad, comm_stream, group=None):
+    """GluBlock (trainsim.cpp:294-308): the MLP's three dW all-reduces overlapped
+    with the backward (allreduce_mlp_grads_overlapped), then the RmsNorm's
+    grad_gain (d_model floats, final once the norm backward -- the block
+    backward's last kernel -- has run on the current stream)."""
+    if not _dp(group):
+        return
+    allreduce_mlp_grads_overlapped(block, gu_grad, d_grad, comm_stream, group)
+    dist.all_reduce(block.gain_tensors()[1], op=dist.ReduceOp.SUM, group=group)
+
+
 def controller_step_global(module, global_tokens: int, group=None):
     """controller_step on the rate of the WHOLE batch (trainsim.cpp:93,129-133;
     policy.cpp:97-109): sum the device masked-block counters of the last

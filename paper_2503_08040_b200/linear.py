@@ -68,6 +68,7 @@ _sigs = {
     "fbq_glublock_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fbq_glublock_apply_sgd": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
     "fbq_glublock_get_gain": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fbq_glublock_gain_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
 }
 for _n, (_r, _a) in _sigs.items():
     _f = getattr(lib, _n)
@@ -367,6 +368,11 @@ class GluBlock(GluMlp):
         gg = np.empty(self.d_model, np.float32)
         _check(lib.fbq_glublock_get_gain(self._b, g.ctypes.data, gg.ctypes.data), "GluBlock get_gain")
         return g, gg
+
+    def gain_tensors(self):
+        """Device fp32 views (gain, grad_gain) of the block's RmsNorm (DP all-reduce)."""
+        return tuple(torch.as_tensor(_DevArray(lib.fbq_glublock_gain_ptr(self._b, w), (self.d_model,)),
+                                     device="cuda") for w in (0, 1))
 
     def step_host(self, *a, **k):  # the host-buffer step APIs belong to the bare MLP driver
         raise NotImplementedError("GluBlock: use the device API")

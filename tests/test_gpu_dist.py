@@ -41,7 +41,7 @@ def _inputs():
     return wg, wu, wd, x, gy
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, kind="mlp"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -49,12 +49,12 @@ def _worker(rank, world, port, q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2503_08040_b200 import linear
-    from paper_2503_08040_b200.dist import (allreduce_mlp_grads_overlapped, controller_step_global,
-                                            shard_rows)
+    from paper_2503_08040_b200.dist import (allreduce_block_grads_overlapped, allreduce_mlp_grads_overlapped,
+                                            controller_step_global, shard_rows)
     wg, wu, wd, x, gy = _inputs()
     r0, r1 = shard_rows(T, world, rank)
     kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True, threshold_init=4.0)
-    m = linear.GluMlp(wg, wu, wd, r1 - r0, **kw)
+    m = (linear.GluMlp if kind == "mlp" else linear.GluBlock)(wg, wu, wd, r1 - r0, **kw)
     gu, gd = m.grad_tensors()
     comm = torch.cuda.Stream()
     outs = []
@@ -62,23 +62,30 @@ def _worker(rank, world, port, q):
         m.zero_grad()
         y = m.forward(torch.from_numpy(x[r0:r1]).cuda(), step, row_offset=r0)
         gx = m.backward(torch.from_numpy(gy[r0:r1]).cuda(), step, row_offset=r0)
-        allreduce_mlp_grads_overlapped(m, gu, gd, comm)
+        if kind == "mlp":
+            allreduce_mlp_grads_overlapped(m, gu, gd, comm)
+        else:
+            allreduce_block_grads_overlapped(m, gu, gd, comm)
         controller_step_global(m, T)
         outs.append((y.cpu().numpy(), gx.cpu().numpy(), m.controller_state()))
     torch.cuda.synchronize()
-    q.put((rank, r0, r1, outs, gu.cpu().numpy(), gd.cpu().numpy()))
+    gg = m.gain_tensors()[1].cpu().numpy() if kind == "block" else None
+    q.put((rank, r0, r1, outs, gu.cpu().numpy(), gd.cpu().numpy(), gg))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_dp_world2_overlapped_allreduce_matches_full_batch():
+@pytest.mark.parametrize("kind", ["mlp", "block"])
+def test_dp_world2_overlapped_allreduce_matches_full_batch(kind):
+    """kind = block: the pre-norm residual GluBlock, whose RmsNorm grad_gain is
+    summed over ranks as well."""
     import torch
     import torch.multiprocessing as mp
     from paper_2503_08040_b200 import linear
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, kind)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
@@ -87,7 +94,7 @@ def test_dp_world2_overlapped_allreduce_matches_full_batch():
         assert p.exitcode == 0
     wg, wu, wd, x, gy = _inputs()
     kw = dict(act_dtype=torch.float32, mid_dtype=torch.float32, exact=True, threshold_init=4.0)
-    full = linear.GluMlp(wg, wu, wd, T, **kw)
+    full = (linear.GluMlp if kind == "mlp" else linear.GluBlock)(wg, wu, wd, T, **kw)
     gu, gd = full.grad_tensors()
     want = []
     for step in range(STEPS):
@@ -99,7 +106,9 @@ def test_dp_world2_overlapped_allreduce_matches_full_batch():
     torch.cuda.synchronize()
     # the controller must actually move theta in this test (else it proves nothing)
     assert want[0][2][1] != want[-1][2][1]
-    for rank, r0, r1, outs, g_gu, g_d in res:
+    for rank, r0, r1, outs, g_gu, g_d, g_gain in res:
+        if kind == "block":
+            assert rel_fro(g_gain, full.gain_tensors()[1].cpu().numpy()) < 1e-6
         for step, ((y, gx, ctl), (yw, gxw, ctlw)) in enumerate(zip(outs, want)):
             assert np.array_equal(y.view(np.int32), yw[r0:r1].view(np.int32)), step
             assert np.array_equal(gx.view(np.int32), gxw[r0:r1].view(np.int32)), step
