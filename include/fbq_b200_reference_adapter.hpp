@@ -496,4 +496,138 @@ class QuantLinearLayer {
   bool has_ctx_ = false;
 };
 
+// ------------------------------------------------------------------ trainsim.hpp:118-131
+// SiluLayer on the device (fbq_cuda_silu_*): y = silu(x) with the input kept as
+// its nonlinear_bits 1 x nonlinear_group RTN context; backward from that context.
+// Exact math (the reference's double silu / silu').  Needs nonlinear_group = 128,
+// 2..16 bits, not passthrough; cols % 8 == 0.
+class SiluLayer {
+ public:
+  explicit SiluLayer(QuantConfig cfg) : bits_(cfg.nonlinear_bits) {
+    if (cfg.passthrough || cfg.nonlinear_bits == 0 || cfg.nonlinear_group != 128)
+      throw std::invalid_argument("SiluLayer config unsupported on B200 (10-bit 1 x 128 context)");
+  }
+  DenseMatrix forward(const DenseMatrix& x) {
+    rows_ = x.rows();
+    cols_ = x.cols();
+    ld_ = detail::ld16(cols_);
+    dx_ = std::make_unique<detail::Dev>(rows_ * cols_ * 4 + 4);
+    dy_ = std::make_unique<detail::Dev>(rows_ * cols_ * 4 + 4);
+    ctx_ = std::make_unique<detail::Dev>(rows_ * ld_ * 2 + 4);
+    sc_ = std::make_unique<detail::Dev>(rows_ * detail::cdiv(cols_, 128) * 4 + 4);
+    detail::upload(x, *dx_);
+    detail::check(fbq_cuda_silu_forward(dx_->p, FBQ_F32, rows_, cols_, cols_, dy_->p, cols_, ctx_->as<int16_t>(),
+                                        ld_, sc_->as<float>(), bits_, 1, nullptr),
+                  "silu forward");
+    return DenseMatrix(rows_, cols_, detail::download_f32(*dy_, static_cast<size_t>(rows_ * cols_)));
+  }
+  DenseMatrix backward(const DenseMatrix& grad_y) {
+    if (!ctx_) throw std::logic_error("silu: backward without context");  // trainsim.cpp:280-282
+    if (grad_y.rows() != rows_ || grad_y.cols() != cols_) throw std::invalid_argument("silu: grad shape");
+    detail::upload(grad_y, *dx_);
+    detail::check(fbq_cuda_silu_backward(ctx_->as<int16_t>(), ld_, sc_->as<float>(), dx_->p, FBQ_F32, rows_, cols_,
+                                         cols_, dy_->p, cols_, 1, nullptr),
+                  "silu backward");
+    return DenseMatrix(rows_, cols_, detail::download_f32(*dy_, static_cast<size_t>(rows_ * cols_)));
+  }
+  bool holds_full_precision_context() const { return false; }
+
+ private:
+  int bits_;
+  int64_t rows_ = 0, cols_ = 0, ld_ = 0;
+  std::unique_ptr<detail::Dev> dx_, dy_, ctx_, sc_;
+};
+
+// ------------------------------------------------------------------ trainsim.hpp:136-146
+// GluBlock on the device driver (fbq_glublock_*): h + down(silu(gate(norm(h))) *
+// up(norm(h))) with the reference's layer ids (gate 0, up 1, down 2 from
+// layer_id_base), forward / backward over host DenseMatrix values.  The
+// reference's GluBlock is an aggregate of its layers; their state is reached
+// here through the accessors below (which: 0 gate, 1 up, 2 down).  Same config
+// rules as QuantLinearLayer (block = 128, 8-bit operands, 10-bit contexts).
+class GluBlock {
+ public:
+  GluBlock(const DenseMatrix& w_gate, const DenseMatrix& w_up, const DenseMatrix& w_down, QuantConfig cfg,
+           index_t max_tokens = 4096, int layer_id_base = 0)
+      : d_(w_gate.cols()), f_(w_gate.rows()), max_tokens_(max_tokens) {
+    if (cfg.passthrough || cfg.block != 128 || cfg.bits_x != 8 || cfg.bits_w != 8 || cfg.bits_grad != 8 ||
+        cfg.context_bits != 8 || cfg.nonlinear_group != 128 || cfg.nonlinear_bits != 10 ||
+        cfg.fallback_mode != FallbackMode::Threshold)
+      throw std::invalid_argument("QuantConfig unsupported on B200 GluBlock (block 128, 8-bit, 10-bit contexts, "
+                                  "threshold fallback)");
+    fbq_mlp_config c;
+    fbq_mlp_default_config(&c);
+    c.d_model = d_;
+    c.d_ff = f_;
+    c.max_tokens = max_tokens;
+    c.act_dtype = FBQ_F32;
+    c.mid_dtype = FBQ_F32;
+    c.epilogue = FBQ_EPI_EXACT;  // bit-exact with the reference
+    c.layer_id_base = layer_id_base;
+    c.seed = cfg.seed;
+    c.threshold_init = cfg.threshold_init;
+    c.r_min = cfg.controller.r_min;
+    c.r_max = cfg.controller.r_max;
+    c.alpha = cfg.controller.alpha;
+    b_ = fbq_glublock_create(&c, w_gate.data(), w_up.data(), w_down.data());
+    if (!b_) throw std::invalid_argument(std::string("fbq_glublock_create: ") + fbq_host_last_error());
+  }
+  ~GluBlock() {
+    if (b_) fbq_glublock_destroy(b_);
+  }
+  GluBlock(const GluBlock&) = delete;
+  GluBlock& operator=(const GluBlock&) = delete;
+
+  DenseMatrix forward(const DenseMatrix& h, int step) { return run(h, step, true); }
+  DenseMatrix backward(const DenseMatrix& grad_out, int step) {
+    if (!has_ctx_) throw std::logic_error("GluBlock: backward without context");
+    return run(grad_out, step, false);
+  }
+  void zero_grads() { detail::check(fbq_glublock_zero_grad(b_, nullptr), "zero_grad"); }
+  void controller_step() { detail::check(fbq_mlp_controller_step(fbq_glublock_mlp(b_), nullptr), "controller"); }
+  void apply_sgd(double lr) { detail::check(fbq_glublock_apply_sgd(b_, lr, nullptr), "apply_sgd"); }
+  std::vector<float> gain() const { return gains().first; }
+  std::vector<float> grad_gain() const { return gains().second; }
+  DenseMatrix weight(int which) const { return mats(which, false); }
+  DenseMatrix grad_weight(int which) const { return mats(which, true); }
+  // thresholds of gate / up (shared: same input, same controller) and down
+  double threshold(int which) const {
+    double rates[2], th[2];
+    detail::check(fbq_mlp_get_controller(fbq_glublock_mlp(b_), rates, th), "get_controller");
+    return th[which == 2 ? 1 : 0];
+  }
+
+ private:
+  DenseMatrix run(const DenseMatrix& in, int step, bool fwd) {
+    const int64_t t = in.rows();
+    if (in.cols() != d_) throw std::invalid_argument("GluBlock: width != d_model");
+    if (t > max_tokens_) throw std::invalid_argument("tokens exceed max_tokens of the B200 block");
+    detail::Dev di(t * d_ * 4 + 4), dout(t * d_ * 4 + 4);
+    detail::upload(in, di);
+    const int st = fwd ? fbq_glublock_forward_device(b_, di.p, t, 0, step, dout.p, nullptr)
+                       : fbq_glublock_backward_device(b_, di.p, t, 0, step, dout.p, nullptr);
+    detail::check(st, fwd ? "GluBlock forward" : "GluBlock backward");
+    if (fwd) has_ctx_ = true;
+    return DenseMatrix(t, d_, detail::download_f32(dout, static_cast<size_t>(t * d_)));
+  }
+  std::pair<std::vector<float>, std::vector<float>> gains() const {
+    std::vector<float> g(static_cast<size_t>(d_)), gg(static_cast<size_t>(d_));
+    detail::check(fbq_glublock_get_gain(b_, g.data(), gg.data()), "get_gain");
+    return {std::move(g), std::move(gg)};
+  }
+  DenseMatrix mats(int which, bool grads) const {
+    std::vector<float> a(static_cast<size_t>(d_ * f_)), b(a.size()), c(a.size());
+    void* m = fbq_glublock_mlp(b_);
+    detail::check(grads ? fbq_mlp_get_grads(m, a.data(), b.data(), c.data())
+                        : fbq_mlp_get_weights(m, a.data(), b.data(), c.data()),
+                  "copy");
+    if (which == 2) return DenseMatrix(d_, f_, std::move(c));
+    return DenseMatrix(f_, d_, std::move(which == 0 ? a : b));
+  }
+  int64_t d_, f_;
+  index_t max_tokens_;
+  void* b_ = nullptr;
+  bool has_ctx_ = false;
+};
+
 }  // namespace fbq::b200

@@ -160,6 +160,50 @@ int main() {
     }
     check(threw, "backward without context");
   }
+  // ---- SiluLayer (trainsim.hpp:118-131)
+  {
+    QuantConfig cfg;
+    SiluLayer ref(cfg);
+    b200::SiluLayer gpu(cfg);
+    const DenseMatrix x = randm(200, 384, 81, 2.0f, 5);
+    const DenseMatrix gy = randm(200, 384, 82, 1e-2f, -1);
+    bool ok = same_dense(ref.forward(x), gpu.forward(x));
+    ok = ok && same_dense(ref.backward(gy), gpu.backward(gy));
+    check(ok, "SiluLayer fwd/bwd");
+  }
+  // ---- GluBlock (trainsim.hpp:136-146) over steps with the controller and SGD
+  {
+    QuantConfig cfg;
+    cfg.block = 128;
+    cfg.threshold_init = 1.5;
+    const index_t d = 256, f = 384;
+    const DenseMatrix wg = randm(f, d, 91, 0.05f, -1), wu = randm(f, d, 92, 0.05f, -1), wd = randm(d, f, 93, 0.05f, -1);
+    GluBlock ref{RmsNorm("norm", d, cfg), QuantLinearLayer("gate", 0, wg, cfg), QuantLinearLayer("up", 1, wu, cfg),
+                 QuantLinearLayer("down", 2, wd, cfg), GluCombine(cfg)};
+    b200::GluBlock gpu(wg, wu, wd, cfg, 512);
+    bool ok = true;
+    for (int step = 0; step < 3 && ok; ++step) {
+      const DenseMatrix h = randm(300, d, 100 + step, 0.7f, 3);
+      const DenseMatrix go = randm(300, d, 110 + step, 1e-2f, -1);
+      ok = ok && same_dense(ref.forward(h, step), gpu.forward(h, step));
+      ok = ok && same_dense(ref.backward(go, step), gpu.backward(go, step));
+      ok = ok && ref.norm.grad_gain() == gpu.grad_gain();
+      ok = ok && same_dense(ref.gate.grad_weight(), gpu.grad_weight(0)) &&
+           same_dense(ref.down.grad_weight(), gpu.grad_weight(2));
+      ref.gate.controller_step();
+      ref.up.controller_step();
+      ref.down.controller_step();
+      gpu.controller_step();
+      ok = ok && ref.gate.threshold() == gpu.threshold(0) && ref.down.threshold() == gpu.threshold(2);
+      ref.norm.apply_sgd(0.05);
+      ref.gate.apply_sgd(0.05);
+      ref.up.apply_sgd(0.05);
+      ref.down.apply_sgd(0.05);
+      gpu.apply_sgd(0.05);
+      ok = ok && ref.norm.gain() == gpu.gain() && same_dense(ref.up.weight(), gpu.weight(1));
+    }
+    check(ok, "GluBlock fwd/bwd/grads/controller/sgd over 3 steps");
+  }
   // error behaviour mirrors the reference
   bool threw = false;
   try {
