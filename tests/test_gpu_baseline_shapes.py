@@ -282,3 +282,32 @@ def test_dx_gemm_chunked_raster_bit_identical():
     assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
     fma = fbq.block_quant_gemm(qa, qb, exact=False)
     assert float((fma - outs[0]).norm() / outs[0].norm()) <= 1e-5
+
+
+def test_c3_glublock_full_dims_exact_vs_reference(F, R, c3_weights):
+    """The reference's GluBlock (RmsNorm + the C3 MLP + residual) at the full C3
+    dims, exact mode, two training steps with SGD of the gain and the weights
+    between them: out, grad_h, grad_gain and the gain bit-identical."""
+    import torch
+    from oracle.oracle import RefGluBlock
+    from paper_2503_08040_b200 import linear
+    wg, wu, wd = c3_weights
+    ref = RefGluBlock(wg, wu, wd, threshold=8.0)
+    blk = linear.GluBlock(wg, wu, wd, T, act_dtype=torch.float32, mid_dtype=torch.float32, exact=True,
+                          threshold_init=8.0)
+    for step in range(2):
+        h, gout = _c3_inputs(10 + step)
+        out_r, gh_r = ref.step(h, gout, step)
+        out = host(blk.forward(dev(h), step))
+        gh = host(blk.backward(dev(gout), step))
+        assert np.array_equal(out.view(np.int32), out_r.view(np.int32)), (step, rel_fro(out, out_r))
+        assert np.array_equal(gh.view(np.int32), gh_r.view(np.int32)), (step, rel_fro(gh, gh_r))
+        gain_r, gg_r, _, _ = ref.state()
+        gain, gg = blk.gain_host()
+        assert np.array_equal(gg.view(np.int32), gg_r.view(np.int32)), step
+        blk.controller_step()
+        ref.controller()
+        blk.apply_sgd(0.05)
+        ref.apply_sgd(0.05)
+        gain_r, _, _, _ = ref.state()
+        assert np.array_equal(blk.gain_host()[0].view(np.int32), gain_r.view(np.int32)), step
