@@ -343,8 +343,10 @@ struct Mlp {
     CU_TRY(cudaEventRecord(ev_gyq, side));
   }
 
+  // join = false (GluBlock): the caller enqueues more work that needs only dX
+  // on `s` first and joins the side stream's dW GEMMs itself (join_side)
   void backward(const void* gy, int64_t tok, int64_t row_off, int step, void* gx,
-                cudaStream_t s, bool gy_ready = false) {
+                cudaStream_t s, bool gy_ready = false, bool join = true) {
     if (tok < 0 || tok > T) throw CudaError(FBQ_ERR_SHAPE, "tokens exceed max_tokens");
     if (tok == 0) return;
     launches += 2;  // K2(dY), GLU backward (+ 6 GEMMs counted in gemm())
@@ -414,8 +416,9 @@ struct Mlp {
     // join: everything after the backward (controller, next step, readers of
     // dW) is ordered after the side stream's GEMMs
     CU_TRY(cudaEventRecord(ev_join, side));
-    CU_TRY(cudaStreamWaitEvent(s, ev_join, 0));
+    if (join) CU_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   }
+  void join_side(cudaStream_t s) { CU_TRY(cudaStreamWaitEvent(s, ev_join, 0)); }
 
   // observed rate = masked blocks / blocks of the last forward (policy.cpp:82-87).
   // Data parallel: the caller sums `counts` over ranks in place and passes the
@@ -629,11 +632,15 @@ struct GluBlockDrv {
   }
   void backward(const void* gout, int64_t tok, int64_t row_off, int step, void* gh, cudaStream_t s) {
     if (tok == 0) return;
-    m.backward(gout, tok, row_off, step, gxn.p, s);  // grad of the norm output (trainsim.cpp:303-306)
+    // grad of the norm output (trainsim.cpp:303-306); the norm backward needs only
+    // dX, so it runs before the join with the side stream's dW GEMMs (its
+    // latency-bound row / column chains fill those GEMMs' tails)
+    m.backward(gout, tok, row_off, step, gxn.p, s, /*gy_ready=*/false, /*join=*/false);
     FBQ_TRY(fbq_cuda_rmsnorm_backward_residual(nctx.as<int16_t>(), ldn, nctx_s.as<float>(), gxn.p,
                                                m.c.act_dtype, tok, m.D, m.D, gain.as<float>(), gout, m.D, gh,
                                                m.D, grad_gain.as<float>(), row_ws.as<double>(),
                                                term_ws.as<float>(), s));
+    m.join_side(s);
     m.launches += 3;
   }
   void zero_grad(cudaStream_t s) {
