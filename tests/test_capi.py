@@ -109,3 +109,14 @@ def test_ops_refuse_cpu_tensors():
         fbq.quantize_rtn(torch.zeros(4, 4))
     with pytest.raises(NotImplementedError):
         fbq.quantize_rtn(torch.zeros(4, 4), block=32)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the sm_100a library the package refuses to import."""
+    import subprocess
+    import sys
+    env = dict(os.environ, FBQ_B200_LIB_OVERRIDE=str(tmp_path / "absent" / "libfbq_b200.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2503_08040_b200.fbq"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "no CPU fallback" in r.stderr
